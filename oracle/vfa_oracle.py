@@ -1,0 +1,387 @@
+"""CPU oracle for the VFA / VSA / FA attention forward pass — TEST INFRASTRUCTURE ONLY.
+
+This module is a float64 numpy restatement of the reference `vfa_lab` algorithms
+(arXiv 2604.12798, /root/reference/pkg/src/vfa_lab). It exists to CHECK the B200
+kernels: only `tests/`, `__graft_entry__.smoke()` and the `cpu_baseline` /
+`--impl reference` legs of `bench.py` may import it. The product path
+(`paper_2604_12798_b200`) never calls it and has no CPU fallback.
+
+Parity pinning: `tests/golden/*.npz` were produced by running the reference package
+itself on the same (bf16-rounded) inputs (`tests/golden/make_golden.py`); the CPU
+test-suite asserts this restatement reproduces those outputs BIT-FOR-BIT (the same
+float64 expressions in the same order, same BLAS shapes), plus the reference's own
+known-answer tests (sabsmax / block_repr / schedule / counter laws).
+
+Extensions over the reference (each reduces to the reference at its default):
+  * LSE output  lse = m + log(l) captured at finalize (reference never returns it).
+  * (n_sink, n_local) schedule generalisation; (1, 1) is the reference schedule.
+  * [B, H, L, d] batching with grouped-query attention (kv head = h // (Hq/Hkv)).
+  * per-(q-block, visit) skip decisions and their decision margin, for VSA parity.
+
+Citations are `src/X.py:N` = /root/reference/pkg/src/vfa_lab/X.py line N.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+NEG_INF = float("-inf")
+KEY_REPRS = ("sabsmax", "k_max", "k_mean", "k_absmax_unsigned")  # src/vfa.py:39
+QUERY_REPRS = ("row_wise", "q_absmax", "q_sabsmax", "q_mean")  # src/vfa.py:40
+F16_EXP_LIMIT = float(np.log(65504.0))  # src/vfa.py:43
+F32_EXP_LIMIT = 88.7228  # src/vfa.py:44
+
+
+class FullyMaskedRow(Exception):
+    """Mirror of FullyMaskedRowError (src/errors.py:4-9)."""
+
+    def __init__(self, row):
+        self.row = row
+        super().__init__(f"query row {row} is fully masked; cannot normalize")
+
+
+class NormalizerUnderflow(Exception):
+    """Mirror of NormalizerUnderflowError (src/errors.py:12-17)."""
+
+    def __init__(self, row):
+        self.row = row
+        super().__init__(f"normalizer underflow at query row {row}")
+
+
+# ----------------------------------------------------------------------------- geometry
+def visible_key_blocks(i: int, qb: int, kb: int, t_c: int, causal: bool) -> int:
+    """src/core.py:112-117 — highest visible key block (1-based) for query block i."""
+    if not causal:
+        return t_c
+    return min((i * qb - 1) // kb + 1, t_c)
+
+
+def local_key_block(i: int, qb: int, kb: int, t_c: int) -> int:
+    """src/core.py:120-122 — key block aligned with query block i."""
+    return min((i * qb - 1) // kb + 1, t_c)
+
+
+def special_blocks(vmax: int, local: int, n_sink: int = 1, n_local: int = 1) -> list:
+    """Exact-update (rowmax + rescale) block set, ascending.
+
+    src/vfa.py:146 gives {1, local} & [1..vmax]; generalised to the first n_sink blocks
+    plus the n_local blocks ending at `local`.
+    """
+    s = set(range(1, n_sink + 1)) | set(range(local - n_local + 1, local + 1))
+    return sorted(j for j in s if 1 <= j <= vmax)
+
+
+def build_schedule(i: int, vmax: int, local: int, reorder: bool,
+                   n_sink: int = 1, n_local: int = 1):
+    """src/vfa.py:146-153 generalised: returns (order tuple, special frozenset).
+
+    reorder: specials first (ascending), then the remaining blocks ascending.
+    At (n_sink, n_local) = (1, 1) this is exactly the reference: head [1] or [1, local],
+    tail [2..vmax] minus local (src/vfa.py:151-153; SPEC.md:301 for i = 1).
+    """
+    spec = special_blocks(vmax, local, n_sink, n_local)
+    if not reorder:
+        return tuple(range(1, vmax + 1)), frozenset(spec)
+    sset = set(spec)
+    tail = [j for j in range(1, vmax + 1) if j not in sset]
+    return tuple(spec + tail), frozenset(spec)
+
+
+# ----------------------------------------------------------------------------- representations
+def sabsmax(block: np.ndarray) -> np.ndarray:
+    """src/vfa.py:47-53: per column, the entry of largest |.|, sign kept, first row on ties."""
+    idx = np.argmax(np.abs(block), axis=0)
+    return block[idx, np.arange(block.shape[1])]
+
+
+def block_repr(block: np.ndarray, kind: str) -> np.ndarray:
+    """src/vfa.py:56-66."""
+    if kind == "sabsmax":
+        return sabsmax(block)
+    if kind == "k_max":
+        return block.max(axis=0)
+    if kind == "k_mean":
+        return block.mean(axis=0)
+    if kind == "k_absmax_unsigned":
+        return np.abs(block).max(axis=0)
+    raise ValueError(f"unknown key representation {kind!r}")
+
+
+def query_repr(block: np.ndarray, kind: str) -> np.ndarray:
+    """src/vfa.py:69-76."""
+    if kind == "q_sabsmax":
+        return sabsmax(block)
+    if kind == "q_absmax":
+        return np.abs(block).max(axis=0)
+    if kind == "q_mean":
+        return block.mean(axis=0)
+    raise ValueError(f"unknown query representation {kind!r}")
+
+
+def precompute_kreprs(k: np.ndarray, kb: int, kind: str, tc1: int | None = None) -> list:
+    """src/vfa.py:79-88: one representation per key block j <= tc1 (default all)."""
+    t_c = k.shape[0] // kb
+    tc1 = t_c if tc1 is None else tc1
+    if not (1 <= tc1 <= t_c):
+        raise ValueError(f"tc1 must be in 1..{t_c}, got {tc1}")
+    return [block_repr(k[(j - 1) * kb: j * kb], kind) for j in range(1, tc1 + 1)]
+
+
+def m_init(qi: np.ndarray, kreprs: list, scale: float, qkind: str = "row_wise") -> np.ndarray:
+    """src/vfa.py:91-106: seed of the running max for one query block."""
+    if not kreprs:
+        raise ValueError("kreprs must be nonempty")
+    if qkind == "row_wise":
+        return np.stack([scale * (qi @ kr) for kr in kreprs]).max(axis=0)
+    qr = query_repr(qi, qkind)
+    best = max(scale * float(qr @ kr) for kr in kreprs)
+    return np.full(qi.shape[0], best)
+
+
+# ----------------------------------------------------------------------------- tile primitives
+def tile_scores(q, k, scale, causal, i, j, qb, kb):
+    """src/reference.py:83-97: scaled, entrywise-causally-masked score tile (1-based i, j)."""
+    qi = q[(i - 1) * qb: i * qb]
+    kj = k[(j - 1) * kb: j * kb]
+    s = (qi @ kj.T) * scale
+    if causal:
+        rows = (i - 1) * qb + np.arange(qb)
+        cols = (j - 1) * kb + np.arange(kb)
+        s[cols[None, :] > rows[:, None]] = NEG_INF
+    return s
+
+
+def _rowsum(x):
+    """src/tensor.py:81-89: strictly left-to-right per-row accumulation."""
+    return np.cumsum(x, axis=1)[:, -1]
+
+
+def _exp_args(s, m):
+    """src/core.py:67-73: S - m with masked entries kept at -inf."""
+    arg = s - m[:, None]
+    masked = np.isneginf(s)
+    if masked.any():
+        arg[masked] = NEG_INF
+    return arg
+
+
+def _rescale_factor(m_old, m_new):
+    """src/core.py:76-83: exp(m_old - m_new), 1 where m_new is still -inf."""
+    dead = np.isneginf(m_new)
+    with np.errstate(invalid="ignore"):
+        f = np.exp(m_old - m_new)
+    if dead.any():
+        f[dead] = 1.0
+    return f
+
+
+def _tile_skippable(m_tilde, m_merged, ln_lambda):
+    """src/sparse.py:99-109: every row strictly below threshold; dead rows pass unless -inf."""
+    with np.errstate(invalid="ignore"):
+        below = (m_tilde - m_merged) < ln_lambda
+    dead = np.isneginf(m_tilde) & np.isneginf(m_merged)
+    if ln_lambda != NEG_INF:
+        below |= dead
+    return bool(np.all(below))
+
+
+def _skip_margin(m_tilde, m_merged, ln_lambda):
+    """Distance of the all-rows skip decision from its threshold (inf when undecidable)."""
+    if ln_lambda == NEG_INF:
+        return math.inf
+    with np.errstate(invalid="ignore"):
+        g = m_tilde - m_merged
+    g = g[np.isfinite(g)]
+    if g.size == 0:
+        return math.inf
+    return abs(float(g.max()) - ln_lambda)
+
+
+@dataclass
+class Monitor:
+    """src/vfa.py:109-128 (OverflowMonitor.record), without the calibration gap."""
+
+    exp_arg_max: float = NEG_INF
+    count_over_f16: int = 0
+    count_over_f32: int = 0
+
+    def record(self, args):
+        finite = args[~np.isneginf(args)]
+        if finite.size == 0:
+            return
+        self.exp_arg_max = max(self.exp_arg_max, float(finite.max()))
+        self.count_over_f16 += int((finite > F16_EXP_LIMIT).sum())
+        self.count_over_f32 += int((finite > F32_EXP_LIMIT).sum())
+
+
+@dataclass
+class HeadResult:
+    out: np.ndarray
+    lse: np.ndarray
+    visited: int = 0
+    skipped: int = 0
+    special: int = 0
+    frozen: int = 0
+    monitor: Monitor = field(default_factory=Monitor)
+    # per q-block list of (block j, skipped?, margin) in visit order (VSA only)
+    decisions: list = field(default_factory=list)
+    error: Exception | None = None
+
+
+VARIANTS = ("fa", "vfa", "vsa")
+
+
+def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
+                 scale=None, kind="sabsmax", qkind="row_wise", reorder=True,
+                 use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None,
+                 raise_errors=True, record_decisions=False) -> HeadResult:
+    """One head of fa_forward (src/fa.py:28-61), vfa_forward (src/vfa.py:156-223) or
+    vsa_forward (src/sparse.py:256-329), float64, returning O, LSE and visit statistics.
+    """
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    nq, d = q.shape
+    nk = k.shape[0]
+    qb, kb = q_block, k_block
+    if nq % qb or nk % kb:
+        raise ValueError("sequence lengths must be divisible by the block sizes")
+    if causal and nq != nk:
+        raise ValueError("causal masking requires N_q == N_k")
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)  # src/reference.py:45-46
+    if variant == "fa":
+        reorder, use_m_init, n_sink = False, False, 0
+    if variant == "vsa":
+        reorder, use_m_init = True, True  # src/sparse.py:288-290
+    ln_lam = NEG_INF if (variant != "vsa" or lam is None) else math.log(lam)
+    if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
+        raise ValueError(f"lambda must be in (0, 1], got {lam}")
+    t_r, t_c = nq // qb, nk // kb
+    out = np.empty((nq, d))
+    lse = np.empty(nq)
+    res = HeadResult(out=out, lse=lse)
+    kreprs = precompute_kreprs(k, kb, kind, tc1) if use_m_init else None
+
+    for i in range(1, t_r + 1):
+        vmax = visible_key_blocks(i, qb, kb, t_c, causal)
+        local = local_key_block(i, qb, kb, t_c)
+        if variant == "fa":
+            order, special = tuple(range(1, vmax + 1)), frozenset(range(1, vmax + 1))
+        else:
+            order, special = build_schedule(i, vmax, local, reorder, n_sink, n_local)
+        qi = q[(i - 1) * qb: i * qb]
+        if use_m_init:
+            m = m_init(qi, kreprs[: min(vmax, len(kreprs))], scale, qkind)
+        else:
+            m = np.full(qb, NEG_INF)
+        l = np.zeros(qb)
+        o = np.zeros((qb, d))
+        dec = []
+        for j in order:
+            s = tile_scores(q, k, scale, causal, i, j, qb, kb)
+            v_j = v[(j - 1) * kb: j * kb]
+            res.visited += 1
+            need_max = (j in special) or variant == "vsa"
+            if need_max:
+                m_tilde = s.max(axis=1)
+                m_new = np.maximum(m, m_tilde)
+            if variant == "vsa":
+                skip = _tile_skippable(m_tilde, m_new, ln_lam)
+                if record_decisions:
+                    dec.append((j, skip, _skip_margin(m_tilde, m_new, ln_lam)))
+                if skip:
+                    res.skipped += 1
+                    continue
+            if j in special:
+                args = _exp_args(s, m_new)
+                res.monitor.record(args)
+                p_t = np.exp(args)
+                f = _rescale_factor(m, m_new)
+                l = f * l + _rowsum(p_t)
+                o = f[:, None] * o + p_t @ v_j
+                m = m_new
+                res.special += 1
+            else:
+                args = _exp_args(s, m)
+                res.monitor.record(args)
+                with np.errstate(over="ignore"):
+                    p_t = np.exp(args)
+                l = l + _rowsum(p_t)
+                o = o + p_t @ v_j
+                res.frozen += 1
+        if record_decisions:
+            res.decisions.append(dec)
+        zero = l == 0.0  # src/core.py:101-109
+        if zero.any():
+            row = int(np.argmax(zero))
+            err = (FullyMaskedRow if np.isneginf(m[row]) else NormalizerUnderflow)((i - 1) * qb + row)
+            if raise_errors:
+                raise err
+            if res.error is None:
+                res.error = err
+        with np.errstate(divide="ignore", invalid="ignore"):
+            out[(i - 1) * qb: i * qb] = o / l[:, None]
+            lse[(i - 1) * qb: i * qb] = m + np.log(l)
+    return res
+
+
+def forward(q, k, v, **kw):
+    """Batched [B, Hq, L, d] / [B, Hkv, L, d] forward with GQA; returns (O, LSE, stats).
+
+    O: float64 [B, Hq, Lq, d]; LSE: float64 [B, Hq, Lq]; stats: dict of summed counts.
+    """
+    q = np.asarray(q)
+    k = np.asarray(k)
+    v = np.asarray(v)
+    if q.ndim == 2:
+        r = forward_head(q, k, v, **kw)
+        return r.out, r.lse, _stats([r])
+    b, hq, lq, d = q.shape
+    hkv = k.shape[1]
+    if hq % hkv:
+        raise ValueError("Hq must be a multiple of Hkv")
+    grp = hq // hkv
+    out = np.empty((b, hq, lq, d))
+    lse = np.empty((b, hq, lq))
+    results = []
+    for bi in range(b):
+        for h in range(hq):
+            r = forward_head(q[bi, h], k[bi, h // grp], v[bi, h // grp], **kw)
+            out[bi, h] = r.out
+            lse[bi, h] = r.lse
+            results.append(r)
+    return out, lse, _stats(results)
+
+
+def _stats(results):
+    st = {"visited": 0, "skipped": 0, "special": 0, "frozen": 0,
+          "count_over_f16": 0, "count_over_f32": 0, "exp_arg_max": NEG_INF}
+    for r in results:
+        st["visited"] += r.visited
+        st["skipped"] += r.skipped
+        st["special"] += r.special
+        st["frozen"] += r.frozen
+        st["count_over_f16"] += r.monitor.count_over_f16
+        st["count_over_f32"] += r.monitor.count_over_f32
+        st["exp_arg_max"] = max(st["exp_arg_max"], r.monitor.exp_arg_max)
+    return st
+
+
+def causal_flops(b, hq, lq, d):
+    """Algorithmic FLOPs of a causal forward, 4*B*Hq*L^2*d/2."""
+    return 4.0 * b * hq * lq * lq * d / 2.0
+
+
+def max_rel_err(a, b):
+    """tests/conftest.py:42-46: max over rows of ||a_r - b_r||_inf / ||b_r||_inf."""
+    a = np.asarray(a, dtype=np.float64).reshape(-1, np.shape(a)[-1])
+    b = np.asarray(b, dtype=np.float64).reshape(-1, np.shape(b)[-1])
+    diff = np.abs(a - b).max(axis=1)
+    denom = np.maximum(np.abs(b).max(axis=1), np.finfo(np.float64).tiny)
+    return float((diff / denom).max())

@@ -1,0 +1,189 @@
+"""Generate golden vectors by running the REFERENCE package (vfa_lab) itself.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+The output `tests/golden/golden.npz` is committed; nothing at test time reads
+/root/reference. Inputs come from the reference's own generators
+(src/tensor.py:92-181), rounded to bf16 (the kernels' input precision), and the
+reference computes on the rounded values in float64.
+
+Call-time hooks (no fork of the reference):
+  * LSE capture: `finalize` is wrapped in vfa_lab.fa / vfa_lab.vfa / vfa_lab.sparse
+    (imported by name at src/fa.py:13-22, src/vfa.py:23-34, src/sparse.py:17-28) to
+    record m + log(l) per query block.
+  * (n_sink, n_local): `build_schedule` is replaced in vfa_lab.vfa and vfa_lab.sparse
+    by the generalisation of src/vfa.py:146-153 (identical at (1, 1)).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import vfa_lab  # noqa: E402
+import vfa_lab.fa as ref_fa  # noqa: E402
+import vfa_lab.sparse as ref_sparse  # noqa: E402
+import vfa_lab.vfa as ref_vfa  # noqa: E402
+from vfa_lab import (AttentionProblem, BlockSpec, SkipConfig, gen_gaussian,  # noqa: E402
+                     gen_structured)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def bf16_round(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def bf16_bits(x):
+    t = torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+_LSE = {}
+_orig_finalize = ref_vfa.finalize
+
+
+def _finalize_hook(state, row_base):
+    with np.errstate(divide="ignore"):
+        _LSE[row_base] = state.m + np.log(state.l)
+    return _orig_finalize(state, row_base)
+
+
+for mod in (ref_fa, ref_vfa, ref_sparse):
+    mod.finalize = _finalize_hook
+
+_orig_schedule = ref_vfa.build_schedule
+_SCHED = {"n_sink": 1, "n_local": 1}
+
+
+def _schedule_hook(i, vmax, local, reorder):
+    ns, nl = _SCHED["n_sink"], _SCHED["n_local"]
+    if (ns, nl) == (1, 1):
+        return _orig_schedule(i, vmax, local, reorder)
+    spec = sorted(j for j in (set(range(1, ns + 1)) | set(range(local - nl + 1, local + 1)))
+                  if 1 <= j <= vmax)
+    if not reorder:
+        return ref_vfa.Schedule(tuple(range(1, vmax + 1)), frozenset(spec))
+    tail = [j for j in range(1, vmax + 1) if j not in set(spec)]
+    return ref_vfa.Schedule(tuple(spec + tail), frozenset(spec))
+
+
+ref_vfa.build_schedule = _schedule_hook
+ref_sparse.build_schedule = _schedule_hook
+
+
+def run_case(name, spec, data, causal, variant, **kw):
+    q, k, v = (bf16_round(x) for x in data)
+    p = AttentionProblem(q=q, k=k, v=v, blocks=spec, causal=causal)
+    _LSE.clear()
+    _SCHED["n_sink"] = kw.pop("n_sink", 1)
+    _SCHED["n_local"] = kw.pop("n_local", 1)
+    rec = {"variant": variant, "causal": causal, "q_block": spec.q_block,
+           "k_block": spec.k_block, "n_sink": _SCHED["n_sink"], "n_local": _SCHED["n_local"]}
+    err = ""
+    out = np.full(q.shape, np.nan)
+    counters = stats = mon = None
+    try:
+        if variant == "fa":
+            out, counters, _ = vfa_lab.fa_forward(p)
+        elif variant == "vfa":
+            out, counters, _, mon = vfa_lab.vfa_forward(p, **kw)
+        elif variant == "vsa":
+            lam = kw.pop("lam")
+            out, counters, stats, mon = vfa_lab.vsa_forward(p, SkipConfig(lam=lam), **kw)
+            rec["lam"] = lam
+        else:
+            raise ValueError(variant)
+    except (vfa_lab.FullyMaskedRowError, vfa_lab.NormalizerUnderflowError) as e:
+        err = f"{type(e).__name__}:{e.row}"
+    rec.update({k2: v2 for k2, v2 in kw.items()})
+    lse = np.full(q.shape[0], np.nan)
+    for base, val in _LSE.items():
+        lse[base: base + spec.q_block] = val
+    arrays = {}
+    for t, x in (("q", q), ("k", k), ("v", v)):
+        bits = bf16_bits(x)
+        key = "in/" + hashlib.sha256(bits.tobytes()).hexdigest()[:16]
+        arrays[key] = bits  # inputs shared by several cases are stored once
+        rec[f"in_{t}"] = key
+    arrays.update({
+        # float32 copy for the GPU tolerance checks; the float64 result is pinned by
+        # its sha256 (the oracle must reproduce it bit-for-bit)
+        f"{name}/out": out.astype(np.float32), f"{name}/lse": lse,
+    })
+    rec["out_sha256"] = hashlib.sha256(np.ascontiguousarray(out, dtype=np.float64).tobytes()).hexdigest()
+    if counters is not None:
+        for f, val in counters.as_dict().items():
+            rec[f"counters.{f}"] = val
+    if stats is not None:
+        for f in ("blocks_visited", "blocks_skipped", "processed_special", "processed_frozen"):
+            rec[f"stats.{f}"] = getattr(stats, f)
+    if mon is not None:
+        rec["mon.count_over_f16"] = mon.count_over_f16
+        rec["mon.count_over_f32"] = mon.count_over_f32
+        rec["mon.exp_arg_max"] = mon.exp_arg_max
+    rec["error"] = err
+    return arrays, rec
+
+
+def main():
+    cases = []
+    # C1 exactly as BASELINE.json configs[0]: CPU oracle, block 64, 1 sink + 2 local.
+    s = BlockSpec(1024, 1024, 64, 64, 64)
+    cases.append(("c1_vfa_b64_s1l2", s, gen_gaussian(s, 0), True, "vfa", dict(n_local=2)))
+    # C1 shape on the GPU tile geometry (Br=128, Bc=64): local band = 2 blocks.
+    s = BlockSpec(1024, 1024, 64, 128, 64)
+    cases.append(("c1_vfa_q128k64_s1l2", s, gen_gaussian(s, 1), True, "vfa", dict(n_local=2)))
+    cases.append(("c1_fa_q128k64", s, gen_gaussian(s, 1), True, "fa", {}))
+    s = BlockSpec(512, 512, 128, 128, 128)
+    cases.append(("fa_d128_causal", s, gen_gaussian(s, 2), True, "fa", {}))
+    cases.append(("vfa_d128_causal", s, gen_gaussian(s, 2), True, "vfa", {}))
+    cases.append(("vfa_d128_causal_kmean", s, gen_gaussian(s, 3), True, "vfa", dict(kind="k_mean")))
+    cases.append(("vfa_d128_noncausal_kmax_seq", s, gen_gaussian(s, 4), False, "vfa",
+                  dict(kind="k_max", reorder=False)))
+    cases.append(("vfa_d128_causal_noinit", s, gen_gaussian(s, 5), True, "vfa", dict(use_m_init=False)))
+    cases.append(("vfa_d128_causal_tc1", s, gen_gaussian(s, 6), True, "vfa", dict(tc1=2)))
+    s = BlockSpec(1024, 1024, 64, 128, 128)
+    sd = gen_structured(s, 7, "middle_peak", 8.0)
+    cases.append(("vsa_midpeak_lam1e-2", s, (sd.q, sd.k, sd.v), True, "vsa", dict(lam=1e-2)))
+    cases.append(("vsa_midpeak_lam1e-9", s, (sd.q, sd.k, sd.v), True, "vsa", dict(lam=1e-9)))
+    # planted sink (coordinate-0 trick of src/tensor.py:153-165, applied to block 1)
+    q, k, v = gen_gaussian(s, 8)
+    amp = np.sqrt(8.0 * np.sqrt(64))
+    q[:, 0] = amp
+    k[:, 0] = 0.0
+    k[:128, 0] = amp
+    cases.append(("vsa_sink_lam1e-2", s, (q, k, v), True, "vsa", dict(lam=1e-2)))
+    cases.append(("vsa_sink_lam1e-1", s, (q, k, v), True, "vsa", dict(lam=1e-1)))
+    # frozen-max overflow without m-init (SURVEY.md §8d non-finite check)
+    s = BlockSpec(512, 512, 128, 128, 128)
+    sd = gen_structured(s, 9, "middle_peak", 120.0)
+    cases.append(("vfa_overflow_noinit", s, (sd.q, sd.k, sd.v), True, "vfa", dict(use_m_init=False)))
+    cases.append(("vfa_overflow_init", s, (sd.q, sd.k, sd.v), True, "vfa", dict(use_m_init=True)))
+    # normalizer-underflow KAT (tests/test_cli.py:177-193) lifted to a 128x128 tile
+    # (values scaled x5 so the seed gap exceeds float64's exp range at d=64, scale 1/8)
+    q = np.zeros((128, 64)); q[:, :2] = 1.0
+    k = np.zeros((128, 64)); k[0::2, 0], k[0::2, 1] = 6000.0, -6000.0
+    k[1::2, 0], k[1::2, 1] = -6000.0, 6000.0
+    v = np.ones((128, 64))
+    s = BlockSpec(128, 128, 64, 128, 128)
+    cases.append(("vfa_underflow_kmax", s, (q, k, v), False, "vfa", dict(kind="k_max")))
+
+    arrays, meta = {}, []
+    for name, spec, data, causal, variant, kw in cases:
+        a, rec = run_case(name, spec, data, causal, variant, **dict(kw))
+        rec["name"] = name
+        arrays.update(a)
+        meta.append(rec)
+        print(name, {k2: v2 for k2, v2 in rec.items() if k2.startswith(("stats", "error", "mon.count"))})
+    arrays["meta"] = np.array(repr(meta))
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
+
+
+if __name__ == "__main__":
+    main()
