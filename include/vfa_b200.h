@@ -1,0 +1,137 @@
+/*
+ * vfa_b200.h — C ABI of the B200 (sm_100a) VFA / VSA / FA attention forward pass.
+ *
+ * This is the drop-in boundary for the reference's attention entry points
+ * (/root/reference/pkg/src/vfa_lab):
+ *   fa_forward(p, order_hook=None)                       src/fa.py:28
+ *   vfa_forward(p, kind, reorder, use_m_init, qkind,
+ *               tc1, monitor)                             src/vfa.py:156-164
+ *   vsa_forward(p, cfg: SkipConfig, kind, qkind, tc1,
+ *               monitor)                                  src/sparse.py:256-263
+ *   AttentionProblem(q, k, v, blocks, scale, causal)     src/reference.py:20-46
+ *   BlockSpec(seq_len_q, seq_len_k, head_dim,
+ *             q_block, k_block)                          src/tensor.py:19-52
+ *   precompute_kreprs(p, kind, tc1)                      src/vfa.py:79-88
+ *   build_schedule(i, vmax, local, reorder)              src/vfa.py:146-153
+ *   variant dispatch _execute(cfg, p)                    src/cli.py:243-286
+ * The reference is Python; its "FFI" is the in-process call. The Python host
+ * package paper_2604_12798_b200 binds these symbols with ctypes (see
+ * INTEGRATION.md). No C++ or torch types cross this boundary: plain pointers,
+ * sizes and a cudaStream_t passed as void*.
+ *
+ * Ownership: all pointers are non-owning device pointers allocated by the caller.
+ * Inputs are const; outputs are written in stream order. The library keeps no
+ * per-call state except a thread-local error string.
+ *
+ * Return codes mirror the reference CLI exit codes (src/cli.py:69-72):
+ *   0 ok, 2 invalid configuration, 3 shape / stride / alignment (data) error,
+ *   4 numerical (only from vfa_status_code on a read-back status word),
+ *   5 CUDA launch or runtime error.
+ */
+#ifndef VFA_B200_H_
+#define VFA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VFA_OK 0
+#define VFA_ERR_CONFIG 2
+#define VFA_ERR_DATA 3
+#define VFA_ERR_NUMERICAL 4
+#define VFA_ERR_CUDA 5
+
+/* variant: src/cli.py:243-286 names */
+#define VFA_VARIANT_FA 0  /* fa_forward: rescale every block, ascending order */
+#define VFA_VARIANT_VFA 1 /* vfa_forward: m-init + sink/local reorder + frozen max */
+#define VFA_VARIANT_VSA 2 /* vsa_forward: VFA + BLASST block skip */
+
+/* key representation kind: KEY_REPRS, src/vfa.py:39 */
+#define VFA_KREPR_SABSMAX 0
+#define VFA_KREPR_K_MAX 1
+#define VFA_KREPR_K_MEAN 2
+#define VFA_KREPR_K_ABSMAX_UNSIGNED 3
+
+/* stats[] slots (int64, device; zeroed by vfa_fwd when non-NULL) */
+#define VFA_STAT_VISITED 0        /* SkipStats.blocks_visited */
+#define VFA_STAT_SKIPPED 1        /* SkipStats.blocks_skipped */
+#define VFA_STAT_SPECIAL 2        /* processed with rowmax + rescale */
+#define VFA_STAT_FROZEN 3         /* processed with the frozen max */
+#define VFA_STAT_OVER_F32 4       /* monitor: exp args > 88.7228 (OverflowMonitor) */
+#define VFA_STAT_OVER_F16 5       /* monitor: exp args > ln(65504) */
+#define VFA_STAT_COUNT 8
+
+/* status[] slots (uint32, device; initialised by vfa_fwd when non-NULL) */
+#define VFA_STATUS_FLAGS 0          /* bit0 fully-masked row, bit1 normalizer underflow, bit2 non-finite O */
+#define VFA_STATUS_UNDERFLOW_ROW 1  /* min linear row ((b*Hq+h)*Lq+r) with l==0, finite m; 0xffffffff none */
+#define VFA_STATUS_MASKED_ROW 2     /* min linear row with l==0 and m==-inf; 0xffffffff none */
+#define VFA_STATUS_NONFINITE_ROWS 3 /* number of rows with a non-finite output */
+#define VFA_STATUS_COUNT 4
+
+typedef struct VfaParams {
+  /* geometry: q [B, Hq, Lq, D], k/v [B, Hkv, Lk, D], o like q; bf16, last dim contiguous */
+  int64_t batch, heads_q, heads_kv, seq_q, seq_k, head_dim;
+  /* element strides for (batch, head, row); all must be multiples of 8 (16 bytes) */
+  int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+  /* lse is a contiguous float32 [B, Hq, Lq] */
+  double scale;         /* softmax scale; <= 0 selects 1/sqrt(D) (src/reference.py:45-46) */
+  int32_t causal;       /* entrywise causal mask (requires Lq == Lk, src/reference.py:43-44) */
+  int32_t q_block;      /* BlockSpec.q_block: must be 128 (tcgen05 M) */
+  int32_t k_block;      /* BlockSpec.k_block: 64 or 128 */
+  int32_t variant;      /* VFA_VARIANT_* */
+  int32_t kind;         /* VFA_KREPR_* */
+  int32_t qkind;        /* 0 = row_wise (the only query representation on the GPU path) */
+  int32_t reorder;      /* vfa_forward(reorder=...) */
+  int32_t use_m_init;   /* vfa_forward(use_m_init=...) */
+  int32_t tc1;          /* representations for key blocks 1..tc1; 0 = all (src/vfa.py:79-88) */
+  int32_t n_sink;       /* sink blocks taking the exact update (reference: 1) */
+  int32_t n_local;      /* local blocks ending at the diagonal (reference: 1) */
+  int32_t monitor;      /* count exp-argument overflows (OverflowMonitor, src/vfa.py:109-128) */
+  double lam;           /* VSA threshold lambda in (0, 1]; <= 0 disables skipping (SkipConfig.lam=None) */
+  int32_t krepr_precomputed; /* 1: workspace already holds vfa_krepr() output for this K; skip recomputing */
+  int32_t reserved;
+} VfaParams;
+
+/* Host-only validation (no GPU needed). Returns VFA_OK or VFA_ERR_CONFIG / VFA_ERR_DATA. */
+int vfa_check_params(const VfaParams* p);
+
+/* Bytes of device workspace vfa_fwd needs (key-block representations). */
+size_t vfa_workspace_bytes(const VfaParams* p);
+
+/* The attention forward. q,k,v: bf16 device; o: bf16 device; lse: float32 device
+ * [B,Hq,Lq] (nullable). workspace: >= vfa_workspace_bytes. stats: int64[VFA_STAT_COUNT]
+ * (nullable). status: uint32[VFA_STATUS_COUNT] (nullable). skip_trace: uint8
+ * [B, Hq, Lq/128, Lk/k_block] (nullable): per visit position, 1 = processed,
+ * 2 = skipped, 0 = not visited. stream: cudaStream_t (NULL = legacy default). */
+int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+            void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+            unsigned char* skip_trace, void* stream);
+
+/* Key-block representations only (precompute_kreprs): k bf16 [B,Hkv,Lk,D] ->
+ * out bf16 contiguous [B, Hkv, n_blocks, D], n_blocks = tc1 or Lk/k_block. */
+int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream);
+
+/* Host mirror of the device tile scheduler (build_schedule, src/vfa.py:146-153,
+ * generalised to n_sink/n_local). i is the 1-based query block. Writes up to `cap`
+ * visited key blocks (1-based) in visit order to order_out and their special
+ * flag to special_out; returns the number visited (vmax) or a negative error. */
+int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local,
+                 int reorder, int variant, int* order_out, unsigned char* special_out, int cap);
+
+/* Maps a host copy of the status word to VFA_OK / VFA_ERR_NUMERICAL. */
+int vfa_status_code(const unsigned int* status_host);
+
+/* Message for the last non-zero return on this thread. */
+const char* vfa_last_error(void);
+
+/* Library version string. */
+const char* vfa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VFA_B200_H_ */

@@ -237,9 +237,13 @@ VARIANTS = ("fa", "vfa", "vsa")
 def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
                  scale=None, kind="sabsmax", qkind="row_wise", reorder=True,
                  use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None,
-                 raise_errors=True, record_decisions=False) -> HeadResult:
+                 raise_errors=True, record_decisions=False, q_blocks=None) -> HeadResult:
     """One head of fa_forward (src/fa.py:28-61), vfa_forward (src/vfa.py:156-223) or
     vsa_forward (src/sparse.py:256-329), float64, returning O, LSE and visit statistics.
+
+    q_blocks: optional iterable of 1-based query blocks to compute (the others are left
+    NaN); used to time bounded samples of large problems. Query blocks are independent
+    (SPEC.md:212), so a sampled block is computed exactly as in the full pass.
     """
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
@@ -263,12 +267,12 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
     if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
         raise ValueError(f"lambda must be in (0, 1], got {lam}")
     t_r, t_c = nq // qb, nk // kb
-    out = np.empty((nq, d))
-    lse = np.empty(nq)
+    out = np.full((nq, d), np.nan)
+    lse = np.full(nq, np.nan)
     res = HeadResult(out=out, lse=lse)
     kreprs = precompute_kreprs(k, kb, kind, tc1) if use_m_init else None
 
-    for i in range(1, t_r + 1):
+    for i in (range(1, t_r + 1) if q_blocks is None else q_blocks):
         vmax = visible_key_blocks(i, qb, kb, t_c, causal)
         local = local_key_block(i, qb, kb, t_c)
         if variant == "fa":

@@ -1,0 +1,21 @@
+"""B200-native (sm_100a) VFA / VSA attention forward — drop-in for the reference's
+`vfa_lab` attention entry points (arXiv 2604.12798).
+
+Compute runs in libvfa_b200.so (hand-written tcgen05/TMEM/TMA kernels, C ABI in
+include/vfa_b200.h). This package is the host-side mirror of the reference API.
+"""
+
+from ._lib import KEY_REPRS, QUERY_REPRS, LibraryNotBuilt
+from .api import (AttentionProblem, BlockSpec, ForwardResult, FullyMaskedRowError, KernelError,
+                  NormalizerUnderflowError, OpCounters, OverflowMonitor, SkipConfig, SkipStats,
+                  attention_forward, check_status, fa_forward, precompute_kreprs, stats_dict,
+                  tile_schedule, vfa_forward, vsa_forward)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AttentionProblem", "BlockSpec", "ForwardResult", "FullyMaskedRowError", "KEY_REPRS",
+    "KernelError", "LibraryNotBuilt", "NormalizerUnderflowError", "OpCounters", "OverflowMonitor",
+    "QUERY_REPRS", "SkipConfig", "SkipStats", "attention_forward", "check_status", "fa_forward",
+    "precompute_kreprs", "stats_dict", "tile_schedule", "vfa_forward", "vsa_forward",
+]

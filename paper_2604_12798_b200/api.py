@@ -1,0 +1,497 @@
+"""Drop-in host API mirroring the reference's attention entry points.
+
+Reference (src/X.py = /root/reference/pkg/src/vfa_lab/X.py):
+  BlockSpec                      src/tensor.py:19-52
+  AttentionProblem               src/reference.py:20-54
+  SkipConfig / SkipStats         src/sparse.py:41-96
+  OpCounters charges             src/counters.py:59-100
+  fa_forward                     src/fa.py:28-61
+  vfa_forward                    src/vfa.py:156-223
+  vsa_forward                    src/sparse.py:256-329
+  precompute_kreprs              src/vfa.py:79-88
+  FullyMaskedRowError / NormalizerUnderflowError   src/errors.py:4-17
+
+Same names, keyword arguments, validation errors and numerical exceptions; the
+compute runs in libvfa_b200.so (hand-written sm_100a kernels) on bf16 CUDA
+tensors. Differences that follow from running on the GPU: O is returned as a bf16
+torch tensor on the device (shape of q), the LSE is returned as well (`.lse`),
+`trace` is None (no per-visit m snapshots), and the OverflowMonitor counts come
+from device counters when monitor=True (exp_arg_max is not tracked).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, fields
+
+import numpy as np
+import torch
+
+from . import _lib
+
+NEG_INF = float("-inf")
+
+
+# ----------------------------------------------------------------------------- errors
+class FullyMaskedRowError(ValueError):
+    """A query row has every score masked; its softmax is undefined (src/errors.py:4-9)."""
+
+    def __init__(self, row: int):
+        self.row = row
+        super().__init__(f"query row {row} is fully masked; cannot normalize")
+
+
+class NormalizerUnderflowError(ArithmeticError):
+    """A softmax normalizer underflowed to zero at finalization (src/errors.py:12-17)."""
+
+    def __init__(self, row: int):
+        self.row = row
+        super().__init__(f"normalizer underflow at query row {row}")
+
+
+class KernelError(RuntimeError):
+    """CUDA launch/runtime failure inside libvfa_b200 (C-ABI code 5)."""
+
+
+# ----------------------------------------------------------------------------- problem
+@dataclass(frozen=True)
+class BlockSpec:
+    """Tile geometry (src/tensor.py:19-52): lengths must divide by the block sizes."""
+
+    seq_len_q: int
+    seq_len_k: int
+    head_dim: int
+    q_block: int = 128
+    k_block: int = 128
+
+    def __post_init__(self):
+        for name in ("seq_len_q", "seq_len_k", "head_dim", "q_block", "k_block"):
+            if getattr(self, name) < 1:
+                raise ValueError(f"{name} must be >= 1")
+        if self.seq_len_q % self.q_block != 0:
+            raise ValueError(f"seq_len_q={self.seq_len_q} not divisible by q_block={self.q_block}")
+        if self.seq_len_k % self.k_block != 0:
+            raise ValueError(f"seq_len_k={self.seq_len_k} not divisible by k_block={self.k_block}")
+
+    @property
+    def t_r(self) -> int:
+        return self.seq_len_q // self.q_block
+
+    @property
+    def t_c(self) -> int:
+        return self.seq_len_k // self.k_block
+
+
+def _as_device_bf16(x, device):
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if not isinstance(x, torch.Tensor):
+        raise TypeError("q, k, v must be torch tensors or numpy arrays")
+    if x.dtype != torch.bfloat16 or x.device.type != "cuda":
+        x = x.to(device=device, dtype=torch.bfloat16)
+    return x
+
+
+@dataclass
+class AttentionProblem:
+    """One attention invocation (src/reference.py:20-54).
+
+    q: [Nq, d] or [B, Hq, Nq, d]; k, v: [Nk, d] or [B, Hkv, Nk, d] (Hq % Hkv == 0, GQA).
+    Tensors are moved to the GPU as bf16 if they are not already.
+    """
+
+    q: object
+    k: object
+    v: object
+    blocks: BlockSpec | None = None
+    scale: float | None = None
+    causal: bool = False
+
+    def __post_init__(self):
+        # validate shapes first (src/reference.py:31-46), then move to the GPU
+        qs, ks, vs = (tuple(np.shape(x)) if not isinstance(x, torch.Tensor) else tuple(x.shape)
+                      for x in (self.q, self.k, self.v))
+        if len(qs) not in (2, 4) or len(ks) != len(qs) or len(vs) != len(qs):
+            raise ValueError("q, k, v must all be 2-D [N, d] or all 4-D [B, H, N, d]")
+        n_q, d = qs[-2], qs[-1]
+        if ks[-1] != d or vs[-1] != d:
+            raise ValueError("Q, K, V must share the head dimension")
+        if ks != vs:
+            raise ValueError("K and V must have the same number of rows")
+        if len(qs) == 4:
+            if qs[0] != ks[0]:
+                raise ValueError("Q and K/V batch sizes differ")
+            if qs[1] % ks[1]:
+                raise ValueError("query heads must be a multiple of key/value heads")
+        n_k = ks[-2]
+        if self.blocks is None:
+            self.blocks = BlockSpec(n_q, n_k, d, 128, 128)
+        if (n_q, n_k, d) != (self.blocks.seq_len_q, self.blocks.seq_len_k, self.blocks.head_dim):
+            raise ValueError("tensor shapes do not match the block spec")
+        if self.causal and n_q != n_k:
+            raise ValueError("causal masking requires N_q == N_k")
+        if self.scale is None:
+            self.scale = 1.0 / math.sqrt(d)
+        dev = None
+        for x in (self.q, self.k, self.v):
+            if isinstance(x, torch.Tensor) and x.device.type == "cuda":
+                dev = x.device
+        dev = dev or torch.device("cuda", torch.cuda.current_device() if torch.cuda.is_available() else 0)
+        self.q = _as_device_bf16(self.q, dev)
+        self.k = _as_device_bf16(self.k, dev)
+        self.v = _as_device_bf16(self.v, dev)
+
+    @property
+    def t_r(self) -> int:
+        return self.blocks.t_r
+
+    @property
+    def t_c(self) -> int:
+        return self.blocks.t_c
+
+
+# ----------------------------------------------------------------------------- skip config / stats
+@dataclass(frozen=True)
+class SkipConfig:
+    """Skip thresholds (src/sparse.py:41-59). lam=None disables skipping."""
+
+    lam: float | None
+    tau: float = 0.0
+    granularity: str = "block"
+
+    def __post_init__(self):
+        if self.lam is not None and not (0.0 < self.lam <= 1.0):
+            raise ValueError(f"lambda must be in (0, 1], got {self.lam}")
+        if self.tau < 0:
+            raise ValueError(f"tau must be >= 0, got {self.tau}")
+        if self.granularity not in ("block", "row"):
+            raise ValueError(f"granularity must be 'block' or 'row', got {self.granularity!r}")
+
+    @property
+    def ln_lambda(self) -> float:
+        return NEG_INF if self.lam is None else math.log(self.lam)
+
+
+@dataclass
+class SkipStats:
+    """src/sparse.py:62-96 (the fields the block-granular VSA pass fills)."""
+
+    blocks_visited: int = 0
+    blocks_skipped: int = 0
+    rows_masked: int = 0
+    row_slots: int = 0
+    rescales_elided: int = 0
+    blocks_processed: int = 0
+    processed_special: int = 0
+    processed_frozen: int = 0
+
+    @property
+    def block_sparsity(self) -> float:
+        return self.blocks_skipped / self.blocks_visited if self.blocks_visited else 0.0
+
+    def as_dict(self) -> dict:
+        d = {f.name: getattr(self, f.name) for f in fields(self)}
+        d["block_sparsity"] = self.block_sparsity
+        return d
+
+
+@dataclass
+class OpCounters:
+    """Element-level op accounting (src/counters.py:14-43), charged per block class
+    from the device's per-class block counts, so it is integer-equal to the
+    reference's instrumented counters whenever the visit statistics agree."""
+
+    mul_scale: int = 0
+    max_rowreduce: int = 0
+    max_running: int = 0
+    sub_broadcast: int = 0
+    exp_evals: int = 0
+    sum_rowreduce: int = 0
+    mad_l: int = 0
+    rescale_mul_l: int = 0
+    rescale_mul_O: int = 0
+    tensor_macs: int = 0
+    rowmax_reductions: int = 0
+    rescale_events: int = 0
+    blocks_processed: int = 0
+    blocks_skipped: int = 0
+    rescales_elided: int = 0
+    rows_masked: int = 0
+
+    def as_dict(self) -> dict:
+        return {f.name: getattr(self, f.name) for f in fields(self)}
+
+    def charge(self, full: int, frozen: int, skipped: int, q: int, k: int, d: int, frozen_rowmax: bool):
+        """n * charge_full_block + m * charge_frozen_block + s * charge_skipped_block."""
+        qk = q * k
+        self.mul_scale += (full + frozen + skipped) * qk
+        self.max_rowreduce += (full + skipped + (frozen if frozen_rowmax else 0)) * qk
+        self.max_running += (full + skipped + (frozen if frozen_rowmax else 0)) * q
+        self.sub_broadcast += (full + frozen) * qk
+        self.exp_evals += full * (qk + q) + frozen * qk
+        self.sum_rowreduce += (full + frozen) * qk
+        self.mad_l += (full + frozen) * q
+        self.rescale_mul_l += full * q
+        self.rescale_mul_O += full * q * d
+        self.tensor_macs += (full + frozen) * 2 * qk * d + skipped * qk * d
+        self.rowmax_reductions += full + skipped + (frozen if frozen_rowmax else 0)
+        self.rescale_events += full
+        self.blocks_processed += full + frozen
+        self.blocks_skipped += skipped
+
+
+@dataclass
+class OverflowMonitor:
+    """src/vfa.py:109-135; GPU counts exp arguments > ln 65504 and > 88.7228."""
+
+    exp_arg_max: float = float("nan")
+    count_over_f16: int = 0
+    count_over_f32: int = 0
+    calibration_gap: dict | None = None
+
+
+class ForwardResult(tuple):
+    """Tuple with the reference's arity plus `.lse` (fp32, [..., Nq]) and `.stats`."""
+
+    lse: torch.Tensor
+    stats: dict
+
+    def __new__(cls, items, lse, stats):
+        obj = super().__new__(cls, items)
+        obj.lse = lse
+        obj.stats = stats
+        return obj
+
+
+# ----------------------------------------------------------------------------- core launcher
+def _strides(x):
+    s = x.stride()
+    if x.stride(-1) != 1:
+        raise ValueError("the head dimension must be contiguous")
+    return (s[0], s[1], s[2])
+
+
+def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind, reorder,
+            use_m_init, tc1, n_sink, n_local, lam, monitor):
+    if kind not in _lib.KEY_REPRS:
+        raise ValueError(f"unknown key representation {kind!r}")
+    if qkind not in _lib.QUERY_REPRS:
+        raise ValueError(f"unknown query representation {qkind!r}")
+    p = _lib.VfaParams()
+    p.batch, p.heads_q, p.seq_q, p.head_dim = q.shape
+    p.heads_kv, p.seq_k = k.shape[1], k.shape[2]
+    p.q_stride[:] = _strides(q)
+    p.k_stride[:] = _strides(k)
+    p.v_stride[:] = _strides(v)
+    p.o_stride[:] = _strides(o)
+    p.scale = float(scale) if scale is not None else 0.0
+    p.causal = int(bool(causal))
+    p.q_block, p.k_block = int(q_block), int(k_block)
+    p.variant = _lib.VARIANTS[variant]
+    p.kind = _lib.KEY_REPRS.index(kind)
+    p.qkind = _lib.QUERY_REPRS.index(qkind)
+    p.reorder = int(bool(reorder))
+    p.use_m_init = int(bool(use_m_init))
+    p.tc1 = 0 if tc1 is None else int(tc1)
+    p.n_sink, p.n_local = int(n_sink), int(n_local)
+    p.monitor = int(bool(monitor))
+    p.lam = float(lam) if lam is not None else 0.0
+    return p
+
+
+def _raise_for(rc):
+    msg = _lib.last_error()
+    if rc in (_lib.VFA_ERR_CONFIG, _lib.VFA_ERR_DATA):
+        raise ValueError(msg)
+    raise KernelError(f"libvfa_b200 error {rc}: {msg}")
+
+
+def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128, scale=None,
+                      kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
+                      n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
+                      check=True, skip_trace=False, stream=None, workspace=None,
+                      krepr_precomputed=False):
+    """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
+
+    Returns (out, lse, info) with info = {"stats": int64 device tensor | dict,
+    "status": uint32 device tensor, "skip_trace": uint8 device tensor | None}.
+    With check=True the status word is read back (one device sync) and
+    FullyMaskedRowError / NormalizerUnderflowError raised like src/core.py:101-109.
+    workspace: optional uint8 device buffer (>= vfa_workspace_bytes) holding the key-block
+    representations; with krepr_precomputed=True they are reused instead of recomputed.
+    """
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
+        raise ValueError(f"lambda must be in (0, 1], got {lam}")
+    lib = _lib.load()
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(x, torch.Tensor) or x.dtype != torch.bfloat16 or x.device.type != "cuda":
+            raise TypeError(f"{name} must be a bf16 CUDA tensor")
+        if x.dim() != 4:
+            raise ValueError(f"{name} must be 4-D [B, H, N, d]")
+    dev = q.device
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.bfloat16, device=dev)
+    if lse is None:
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
+    p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
+                scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
+                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor)
+    rc = lib.vfa_check_params(ctypes.byref(p))
+    if rc:
+        _raise_for(rc)
+    p.krepr_precomputed = int(bool(krepr_precomputed))
+    ws_bytes = int(lib.vfa_workspace_bytes(ctypes.byref(p)))
+    if workspace is None:
+        if krepr_precomputed:
+            raise ValueError("krepr_precomputed needs the workspace that holds the representations")
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    else:
+        if workspace.numel() < ws_bytes:
+            raise ValueError(f"workspace too small: {workspace.numel()} < {ws_bytes}")
+        ws = workspace
+    stats = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+    status = torch.empty(_lib.STATUS_COUNT, dtype=torch.int32, device=dev)
+    trace = None
+    if skip_trace:
+        trace = torch.empty((q.shape[0], q.shape[1], q.shape[2] // 128, k.shape[2] // k_block),
+                            dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        rc = lib.vfa_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                         lse.data_ptr(), ws.data_ptr(), ws_bytes, stats.data_ptr(), status.data_ptr(),
+                         trace.data_ptr() if trace is not None else None, ctypes.c_void_p(st))
+    if rc:
+        _raise_for(rc)
+    info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws}
+    if check:
+        check_status(status)
+    return out, lse, info
+
+
+def check_status(status: torch.Tensor):
+    """Raise the reference's finalize errors from a device status word (src/core.py:101-109)."""
+    s = status.cpu().numpy().view(np.uint32)
+    flags = int(s[_lib.STATUS_FLAGS])
+    if flags & 1:
+        raise FullyMaskedRowError(int(s[_lib.STATUS_MASKED_ROW]))
+    if flags & 2:
+        raise NormalizerUnderflowError(int(s[_lib.STATUS_UNDERFLOW_ROW]))
+    return flags
+
+
+def stats_dict(info) -> dict:
+    s = info["stats"].cpu().tolist()
+    return {"visited": s[_lib.STAT_VISITED], "skipped": s[_lib.STAT_SKIPPED],
+            "special": s[_lib.STAT_SPECIAL], "frozen": s[_lib.STAT_FROZEN],
+            "count_over_f32": s[_lib.STAT_OVER_F32], "count_over_f16": s[_lib.STAT_OVER_F16],
+            "nonfinite_rows": int(info["status"].cpu()[_lib.STATUS_NONFINITE_ROWS])}
+
+
+# ----------------------------------------------------------------------------- reference-shaped entry points
+def _run(p: AttentionProblem, variant, **kw):
+    q, k, v = p.q, p.k, p.v
+    two_d = q.dim() == 2
+    if two_d:
+        q, k, v = (x.view(1, 1, *x.shape) for x in (q, k, v))
+    out, lse, info = attention_forward(q, k, v, variant=variant, causal=p.causal,
+                                       q_block=p.blocks.q_block, k_block=p.blocks.k_block,
+                                       scale=p.scale, **kw)
+    st = stats_dict(info)
+    if two_d:
+        out, lse = out.view(*p.q.shape), lse.view(p.q.shape[0])
+    return out, lse, st
+
+
+def _counters(st, p: AttentionProblem, frozen_rowmax: bool) -> OpCounters:
+    c = OpCounters()
+    c.charge(st["special"], st["frozen"], st["skipped"], p.blocks.q_block, p.blocks.k_block,
+             p.blocks.head_dim, frozen_rowmax)
+    return c
+
+
+def _monitor(st, monitor: bool) -> OverflowMonitor:
+    m = OverflowMonitor()
+    if monitor:
+        m.count_over_f16 = st["count_over_f16"]
+        m.count_over_f32 = st["count_over_f32"]
+    return m
+
+
+def fa_forward(p: AttentionProblem, order_hook=None):
+    """Baseline online softmax, rescale on every block (src/fa.py:28-61).
+
+    Returns (O, counters, trace=None) with `.lse`. order_hook (a test-only
+    permutation hook in the reference) is not supported on the GPU path.
+    """
+    if order_hook is not None:
+        raise ValueError("order_hook is not supported by the GPU fa_forward")
+    out, lse, st = _run(p, "fa")
+    return ForwardResult((out, _counters(st, p, False), None), lse, st)
+
+
+def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True,
+                use_m_init: bool = True, qkind: str = "row_wise", tc1: int | None = None,
+                monitor: bool = False, *, n_sink: int = 1, n_local: int = 1):
+    """Frozen-max pass with m-initialisation (src/vfa.py:156-223).
+
+    Returns (O, counters, trace=None, overflow_monitor) with `.lse`.
+    """
+    if kind not in _lib.KEY_REPRS:
+        raise ValueError(f"unknown key representation {kind!r}")
+    if qkind not in _lib.QUERY_REPRS:
+        raise ValueError(f"unknown query representation {qkind!r}")
+    if tc1 is not None and not (1 <= tc1 <= p.t_c):
+        raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
+    out, lse, st = _run(p, "vfa", kind=kind, reorder=reorder, use_m_init=use_m_init, qkind=qkind,
+                        tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor)
+    return ForwardResult((out, _counters(st, p, False), None, _monitor(st, monitor)), lse, st)
+
+
+def vsa_forward(p: AttentionProblem, cfg: SkipConfig, kind: str = "sabsmax", qkind: str = "row_wise",
+                tc1: int | None = None, monitor: bool = False, *, n_sink: int = 1, n_local: int = 1):
+    """Frozen max + BLASST block skipping (src/sparse.py:256-329).
+
+    Returns (O, counters, SkipStats, overflow_monitor) with `.lse`.
+    """
+    if cfg.granularity != "block":
+        raise ValueError("vsa_forward requires block granularity")
+    if kind not in _lib.KEY_REPRS:
+        raise ValueError(f"unknown key representation {kind!r}")
+    if tc1 is not None and not (1 <= tc1 <= p.t_c):
+        raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
+    out, lse, st = _run(p, "vsa", kind=kind, qkind=qkind, tc1=tc1, n_sink=n_sink, n_local=n_local,
+                        lam=cfg.lam, monitor=monitor)
+    stats = SkipStats(blocks_visited=st["visited"], blocks_skipped=st["skipped"],
+                      blocks_processed=st["special"] + st["frozen"],
+                      processed_special=st["special"], processed_frozen=st["frozen"])
+    return ForwardResult((out, _counters(st, p, True), stats, _monitor(st, monitor)), lse, st)
+
+
+def precompute_kreprs(p: AttentionProblem, kind: str, tc1: int | None = None) -> torch.Tensor:
+    """Key-block representations on the GPU (src/vfa.py:79-88): bf16 [..., n_blocks, d]."""
+    if kind not in _lib.KEY_REPRS:
+        raise ValueError(f"unknown key representation {kind!r}")
+    tc1 = p.t_c if tc1 is None else tc1
+    if not (1 <= tc1 <= p.t_c):
+        raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
+    k = p.k if p.k.dim() == 4 else p.k.view(1, 1, *p.k.shape)
+    q = p.q if p.q.dim() == 4 else p.q.view(1, 1, *p.q.shape)
+    prm = _params(q, k, k, q, variant="vfa", causal=p.causal, q_block=p.blocks.q_block,
+                  k_block=p.blocks.k_block, scale=p.scale, kind=kind, qkind="row_wise", reorder=True,
+                  use_m_init=True, tc1=tc1, n_sink=1, n_local=1, lam=None, monitor=False)
+    out = torch.empty((k.shape[0], k.shape[1], tc1, k.shape[3]), dtype=torch.bfloat16, device=k.device)
+    lib = _lib.load()
+    with torch.cuda.device(k.device):
+        rc = lib.vfa_krepr(ctypes.byref(prm), k.data_ptr(), out.data_ptr(),
+                           ctypes.c_void_p(torch.cuda.current_stream(k.device).cuda_stream))
+    if rc:
+        _raise_for(rc)
+    return out if p.k.dim() == 4 else out[0, 0]
+
+
+def tile_schedule(i, q_block, k_block, t_c, causal, n_sink=1, n_local=1, reorder=True, variant="vfa"):
+    """The device tile scheduler's visit order and exact-update set for query block i."""
+    return _lib.schedule(i, q_block, k_block, t_c, causal, n_sink, n_local, reorder, variant)

@@ -1,0 +1,938 @@
+// B200 (sm_100a) VFA / VSA / FA attention forward.
+//
+// One CTA = one work unit = (batch b, KV head, NQ query heads of that KV head's
+// GQA group, one 128-row query tile). The NQ query tiles share every K/V tile
+// loaded into shared memory and share the tile schedule (same rows => same
+// causal extent, same sink/local blocks).
+//
+// Warp roles (16 warps):
+//   warps 0-3   softmax WG for query tile 0   (thread r owns row r, TMEM lane r)
+//   warps 4-7   softmax WG for query tile 1
+//   warps 8-11  correction WG: O rescale in TMEM on exact-update blocks only
+//   warp 12     MMA issuer (one thread), TMEM allocator
+//   warp 13     TMA producer (one thread)
+//   warps 14-15 idle
+// TMEM (512 columns): S_t at t*128 (P_t bf16 aliased over its first BC/2 columns),
+// O_t at 256 + t*D.
+//
+// Reference algorithm (src/X.py = /root/reference/pkg/src/vfa_lab/X.py):
+//   precompute_kreprs / block_repr / sabsmax   src/vfa.py:47-88     -> krepr_kernel
+//   m_init (row_wise)                          src/vfa.py:91-106    -> m-init prologue (tcgen05 Q.Krepr^T)
+//   build_schedule / visible / local blocks    src/vfa.py:146-153, src/core.py:112-122 -> schedule.h
+//   special-block update (rowmax + rescale)    src/vfa.py:202-208, src/core.py:76-92
+//   frozen-block update (no rowmax/rescale)    src/vfa.py:209-215, src/core.py:95-98
+//   BLASST skip (all rows m~ - m_new < ln l)   src/sparse.py:99-109, 296-304
+//   fa_forward (rescale every block)           src/fa.py:28-61
+//   finalize (O / l, l == 0 errors)            src/core.py:101-109
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/vfa_b200.h"
+#include "ptx.cuh"
+#include "schedule.h"
+
+namespace vfa {
+
+constexpr int kBR = 128;          // query rows per tile (tcgen05 M)
+constexpr int kThreads = 512;
+constexpr int kMaxSmem = 227 * 1024;
+constexpr float kLn2 = 0.6931471805599453f;
+
+enum Mode { kFA = 0, kVFA = 1, kVSA = 2 };
+
+struct FwdArgs {
+  int B, Hq, Hkv, Lq, Lk, group, Tr, Tc;
+  int units_per_kvh, heads_per_unit;
+  float c_scale;      // softmax scale * log2(e)
+  float log2_lambda;  // skip threshold in log2 units (-inf: no skipping)
+  int causal, reorder, use_m_init, nrep_cap, n_sink, n_local, monitor;
+  __nv_bfloat16* o;
+  long long o_sb, o_sh, o_sr;
+  float* lse;
+  unsigned long long* stats;
+  unsigned int* status;
+  unsigned char* skip_trace;
+};
+
+template <int D, int BC, int NQ>
+struct Cfg {
+  static constexpr int kQBytes = kBR * D * 2;
+  static constexpr int kKVBytes = BC * D * 2;
+  static constexpr int kDCh = D / 64;  // 64-column (128-byte) swizzle chunks
+  static constexpr int kCtlBytes = 4096;
+  static constexpr int kAvail = kMaxSmem - 1024 - kCtlBytes - NQ * kQBytes;
+  static constexpr int kStagesRaw = kAvail / kKVBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kSmem = 1024 + NQ * kQBytes + kStages * kKVBytes + kCtlBytes;
+  static __host__ __device__ constexpr uint32_t s_off(int t) { return static_cast<uint32_t>(t) * 128u; }
+  static constexpr int kOBase = NQ == 2 ? 256 : 128;
+  static constexpr uint32_t kTmemCols = NQ == 2 ? 512 : 256;
+  static_assert(kStages >= 2, "not enough shared memory for a K/V ring");
+};
+
+template <int NS, int NQ>
+struct __align__(16) Ctl {
+  uint64_t q_full[NQ];
+  uint64_t kv_full[NS];
+  uint64_t kv_empty[NS];
+  uint64_t s_full[NQ];
+  uint64_t s_free[NQ];
+  uint64_t p_full[NQ];
+  uint64_t o_full[NQ];
+  uint64_t o_ready[NQ];
+  uint64_t o_final[NQ];
+  uint64_t sc_full[NQ];
+  uint32_t tmem_base;
+  uint32_t skip[NQ];
+  float fbuf[NQ][kBR];
+};
+
+struct Unit {
+  int b, kvh, h0, qt;
+};
+
+__device__ __forceinline__ Unit decode_unit(const FwdArgs& a, int u) {
+  Unit w;
+  int bk = u / a.units_per_kvh;
+  int r = u - bk * a.units_per_kvh;
+  int pairs = a.group / a.heads_per_unit;
+  w.qt = a.Tr - 1 - r / pairs;  // longest causal tiles first within each KV head
+  int pair = r - (r / pairs) * pairs;
+  w.b = bk / a.Hkv;
+  w.kvh = bk - w.b * a.Hkv;
+  w.h0 = w.kvh * a.group + pair * a.heads_per_unit;
+  return w;
+}
+
+template <int MODE>
+__device__ __forceinline__ TileSchedule unit_schedule(const FwdArgs& a, int qt, int BC) {
+  return make_schedule(qt + 1, kBR, BC, a.Tc, a.causal != 0, a.n_sink, a.n_local,
+                       MODE == kFA ? false : (a.reorder != 0), MODE == kFA);
+}
+
+// number of m-init chunks (BC representations per chunk)
+template <int MODE>
+__device__ __forceinline__ int minit_chunks(const FwdArgs& a, const TileSchedule& s, int BC, int* nrep) {
+  if (MODE == kFA || !a.use_m_init) {
+    *nrep = 0;
+    return 0;
+  }
+  int n = s.vmax < a.nrep_cap ? s.vmax : a.nrep_cap;
+  *nrep = n;
+  return (n + BC - 1) / BC;
+}
+
+__device__ __forceinline__ bool needs_corr(const TileSchedule& s, int pos, bool* special_out = nullptr) {
+  int j = sched_block(s, pos);
+  bool sp = sched_is_special(s, j);
+  if (special_out) *special_out = sp;
+  return sp && pos > 0;
+}
+
+// ------------------------------------------------------------------------------------
+template <int D, int BC, int NQ, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
+                   const FwdArgs a) {
+  using C = Cfg<D, BC, NQ>;
+  constexpr int NS = C::kStages;
+  using CtlT = Ctl<NS, NQ>;
+  static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + NQ * C::kQBytes;
+  CtlT* ctl = reinterpret_cast<CtlT*>(sKV + NS * C::kKVBytes);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  const Unit unit = decode_unit(a, blockIdx.x);
+  const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);
+  const int N = sched.vmax;
+  int nrep = 0;
+  const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);
+
+  if (tid == 0) {
+    for (int t = 0; t < NQ; ++t) {
+      mbar_init(&ctl->q_full[t], 1);
+      mbar_init(&ctl->s_full[t], 1);
+      mbar_init(&ctl->s_free[t], 4);
+      mbar_init(&ctl->p_full[t], 4);
+      mbar_init(&ctl->o_full[t], 1);
+      mbar_init(&ctl->o_ready[t], 4);
+      mbar_init(&ctl->o_final[t], 1);
+      mbar_init(&ctl->sc_full[t], kBR);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&ctl->kv_full[s], 1);
+      mbar_init(&ctl->kv_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 13 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmR);
+  }
+  if (warp == 12) tmem_alloc<C::kTmemCols>(&ctl->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = ctl->tmem_base;
+
+  if (warp == 13) {
+    // ============================ TMA producer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      for (int t = 0; t < NQ; ++t) {
+        mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
+#pragma unroll
+        for (int c = 0; c < C::kDCh; ++c)
+          tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+                      unit.h0 + t, unit.b, pol_q);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      auto load_tile = [&](const CUtensorMap* map, int row) {
+        mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
+        uint8_t* dst = sKV + stage * C::kKVBytes;
+#pragma unroll
+        for (int c = 0; c < C::kDCh; ++c)
+          tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
+        if (++stage == NS) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      for (int ch = 0; ch < nchunks; ++ch) load_tile(&tmR, ch * BC);
+      for (int pos = 0; pos < N; ++pos) {
+        const int j = sched_block(sched, pos);
+        load_tile(&tmK, (j - 1) * BC);
+        load_tile(&tmV, (j - 1) * BC);
+      }
+    }
+  } else if (warp == 12) {
+    // ============================ MMA issuer ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+    if (lane == 0) {
+      constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
+      constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      for (int t = 0; t < NQ; ++t) mbar_wait(&ctl->q_full[t], 0);
+      tc_fence_after();
+      int stage = 0;
+      uint32_t phase = 0;
+      auto acquire = [&]() -> int {
+        mbar_wait(&ctl->kv_full[stage], phase);
+        tc_fence_after();
+        int s = stage;
+        if (++stage == NS) {
+          stage = 0;
+          phase ^= 1;
+        }
+        return s;
+      };
+      auto issue_qk = [&](int t, int s) {
+        const uint32_t qa = smem_u32(sQ + t * C::kQBytes);
+        const uint32_t kb = smem_u32(sKV + s * C::kKVBytes);
+        const uint32_t dS = tbase + C::s_off(t);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oq = (kk >> 2) * (kBR * 128) + (kk & 3) * 32;
+          const uint32_t ok = (kk >> 2) * (BC * 128) + (kk & 3) * 32;
+          mma_ss(dS, make_sw128_desc(qa + oq, 16, 1024), make_sw128_desc(kb + ok, 16, 1024), kIdescQK,
+                 kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, int s, bool acc) {
+        const uint32_t vb = smem_u32(sKV + s * C::kKVBytes);
+        const uint32_t dO = tbase + C::kOBase + t * D;
+        const uint32_t aP = tbase + C::s_off(t);
+#pragma unroll
+        for (int kk = 0; kk < BC / 16; ++kk)
+          mma_ts(dO, aP + kk * 8, make_sw128_desc(vb + kk * 2048, BC * 128, 1024), kIdescPV,
+                 (acc || kk > 0) ? 1u : 0u);
+      };
+      uint32_t sfree_ph[NQ], p_ph[NQ], ordy_ph[NQ];
+      bool o_init[NQ];
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        sfree_ph[t] = 0;
+        p_ph[t] = 0;
+        ordy_ph[t] = 0;
+        o_init[t] = false;
+      }
+      // m-init prologue: S_t = Q_t . Krepr_chunk^T
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int s = acquire();
+        for (int t = 0; t < NQ; ++t) {
+          if (ch > 0) {
+            mbar_wait(&ctl->s_free[t], sfree_ph[t]);
+            sfree_ph[t] ^= 1;
+            tc_fence_after();
+          }
+          issue_qk(t, s);
+          mma_commit(&ctl->s_full[t]);
+        }
+        mma_commit(&ctl->kv_empty[s]);
+      }
+      // first QK
+      {
+        const int s = acquire();
+        for (int t = 0; t < NQ; ++t) {
+          if (nchunks > 0) {
+            mbar_wait(&ctl->s_free[t], sfree_ph[t]);
+            sfree_ph[t] ^= 1;
+            tc_fence_after();
+          }
+          issue_qk(t, s);
+          mma_commit(&ctl->s_full[t]);
+        }
+        mma_commit(&ctl->kv_empty[s]);
+      }
+      for (int pos = 0; pos < N; ++pos) {
+        const bool corr = needs_corr(sched, pos);
+        const bool corr_next = (pos + 1 < N) && needs_corr(sched, pos + 1);
+        const int vs = acquire();
+        int ks = -1;
+        for (int t = 0; t < NQ; ++t) {
+          mbar_wait(&ctl->p_full[t], p_ph[t]);
+          p_ph[t] ^= 1;
+          tc_fence_after();
+          const bool skip = (MODE == kVSA) && (ctl->skip[t] != 0);
+          if (corr) {
+            mbar_wait(&ctl->o_ready[t], ordy_ph[t]);
+            ordy_ph[t] ^= 1;
+            tc_fence_after();
+          }
+          if (!skip) {
+            issue_pv(t, vs, o_init[t]);
+            o_init[t] = true;
+          }
+          if (corr_next) mma_commit(&ctl->o_full[t]);
+          if (t == NQ - 1) mma_commit(&ctl->kv_empty[vs]);
+          if (pos + 1 < N) {
+            if (t == 0) ks = acquire();
+            issue_qk(t, ks);
+            mma_commit(&ctl->s_full[t]);
+          }
+        }
+        if (ks >= 0) mma_commit(&ctl->kv_empty[ks]);
+      }
+      for (int t = 0; t < NQ; ++t) mma_commit(&ctl->o_final[t]);
+    }
+  } else if (warp >= 14) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+  } else if (warp >= 8) {
+    // ============================ correction WG ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+    const int r = tid - 256;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    uint32_t sc_ph[NQ], of_ph[NQ];
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) sc_ph[t] = of_ph[t] = 0;
+    for (int pos = 1; pos < N; ++pos) {
+      if (!needs_corr(sched, pos)) continue;
+      for (int t = 0; t < NQ; ++t) {
+        mbar_wait(&ctl->sc_full[t], sc_ph[t]);
+        sc_ph[t] ^= 1;
+        const float f = ctl->fbuf[t][r];
+        mbar_wait(&ctl->o_full[t], of_ph[t]);
+        of_ph[t] ^= 1;
+        tc_fence_after();
+        const bool work = (MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f);
+        if (work) {
+          const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float v[32];
+            tmem_ld32(tO + c * 32, v);
+            tmem_wait_ld();
+            reg_fence32(v);
+            uint32_t u[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(v[e] * f);
+            tmem_st32(tO + c * 32, u);
+          }
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->o_ready[t]);
+      }
+    }
+  } else {
+    // ============================ softmax WGs ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
+    const int t = warp >> 2;
+    const int r = tid & 127;
+    if (t < NQ) {
+      const int h = unit.h0 + t;
+      const int R = unit.qt * kBR + r;  // absolute query row
+      const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t tS = tbase + C::s_off(t) + lane_off;
+      const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
+      const float cs = a.c_scale;
+      float m2 = -INFINITY;  // running max, log2 units of scaled scores
+      float l = 0.f;
+      uint32_t s_ph = 0;
+      long long n_special = 0, n_frozen = 0, n_skipped = 0;
+      unsigned long long over32 = 0, over16 = 0;
+
+      // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
+      if (nchunks > 0) {
+        float mx = -INFINITY;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          mbar_wait(&ctl->s_full[t], s_ph);
+          s_ph ^= 1;
+          tc_fence_after();
+          const int valid = nrep - ch * BC;
+#pragma unroll
+          for (int c = 0; c < BC / 32; ++c) {
+            float v[32];
+            tmem_ld32(tS + c * 32, v);
+            tmem_wait_ld();
+            reg_fence32(v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e < valid) mx = fmaxf(mx, v[e]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->s_free[t]);
+        }
+        m2 = mx * cs;
+      }
+
+      for (int pos = 0; pos < N; ++pos) {
+        const int j = sched_block(sched, pos);
+        const bool special = (MODE == kFA) || sched_is_special(sched, j);
+        const bool corr = special && pos > 0;
+        const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
+        const int lim = R - (j - 1) * BC;  // columns > lim are causally masked
+        mbar_wait(&ctl->s_full[t], s_ph);
+        s_ph ^= 1;
+        tc_fence_after();
+        bool skipped = false;
+        if (MODE == kFA || MODE == kVSA || special) {
+          // ---- full row in registers: rowmax (+ skip test) (+ rescale)
+          float v[BC];
+#pragma unroll
+          for (int c = 0; c < BC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < BC / 32; ++c) reg_fence32(v + c * 32);
+          if (mask) {
+#pragma unroll
+            for (int e = 0; e < BC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+          }
+          float mt = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < BC; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
+          const float mt2 = mt * cs;
+          const float m2n = fmaxf(m2, mt2);
+          if (MODE == kVSA) {
+            const bool below = (mt2 - m2n < a.log2_lambda) ||
+                               (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
+            skipped = named_bar_and(1 + t, kBR, below);
+          }
+          if (skipped) {
+            ++n_skipped;
+            if (corr) {
+              ctl->fbuf[t][r] = 1.0f;
+              mbar_arrive(&ctl->sc_full[t]);
+            }
+          } else {
+            float mu;
+            if (special) {
+              const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
+              m2 = m2n;
+              l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
+              if (corr) {
+                ctl->fbuf[t][r] = f;
+                mbar_arrive(&ctl->sc_full[t]);
+              }
+              ++n_special;
+            } else {
+              ++n_frozen;
+            }
+            mu = (m2 == -INFINITY) ? 0.f : m2;
+            float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < BC / 32; ++c) {
+              uint32_t u[16];
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float x0 = fmaf(v[c * 32 + e], cs, -mu);
+                const float x1 = fmaf(v[c * 32 + e + 1], cs, -mu);
+                if (a.monitor) {
+                  over32 += (x0 > 128.0f) + (x1 > 128.0f);
+                  over16 += (x0 > 15.999295f) + (x1 > 15.999295f);
+                }
+                const float p0 = ex2_approx(x0);
+                const float p1 = ex2_approx(x1);
+                ls0 += p0;
+                ls1 += p1;
+                u[e >> 1] = pack_bf16x2(p0, p1);
+              }
+              tmem_st16(tS + c * 16, u);
+            }
+            l = __fadd_rn(l, __fadd_rn(ls0, ls1));
+          }
+        } else {
+          // ---- frozen block (VFA): no rowmax, no rescale; streamed in 32-column chunks
+          const float mu = (m2 == -INFINITY) ? 0.f : m2;
+          float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+          for (int c = 0; c < BC / 32; ++c) {
+            float v[32];
+            tmem_ld32(tS + c * 32, v);
+            tmem_wait_ld();
+            reg_fence32(v);
+            if (mask) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e > lim) ? -INFINITY : v[e];
+            }
+            uint32_t u[16];
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float x0 = fmaf(v[e], cs, -mu);
+              const float x1 = fmaf(v[e + 1], cs, -mu);
+              if (a.monitor) {
+                over32 += (x0 > 128.0f) + (x1 > 128.0f);
+                over16 += (x0 > 15.999295f) + (x1 > 15.999295f);
+              }
+              const float p0 = ex2_approx(x0);
+              const float p1 = ex2_approx(x1);
+              ls0 += p0;
+              ls1 += p1;
+              u[e >> 1] = pack_bf16x2(p0, p1);
+            }
+            tmem_st16(tS + c * 16, u);
+          }
+          l = __fadd_rn(l, __fadd_rn(ls0, ls1));
+          ++n_frozen;
+        }
+        if (r == 0) {
+          if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
+          if (a.skip_trace) {
+            const size_t idx = ((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos;
+            a.skip_trace[idx] = skipped ? 2 : 1;
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->p_full[t]);
+      }
+
+      // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l
+      mbar_wait(&ctl->o_final[t], 0);
+      tc_fence_after();
+      const float inv = 1.0f / l;
+      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr;
+      bool finite = true;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float v[32];
+        tmem_ld32(tO + c * 32, v);
+        tmem_wait_ld();
+        reg_fence32(v);
+        uint32_t u[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
+          finite = finite && isfinite(o0) && isfinite(o1);
+          u[e >> 1] = pack_bf16x2(o0, o1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(u[4 * q4], u[4 * q4 + 1], u[4 * q4 + 2], u[4 * q4 + 3]);
+      }
+      const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
+      if (a.lse) a.lse[lrow] = (m2 + __log2f(l)) * kLn2;
+      if (a.status) {
+        if (l == 0.f) {
+          if (m2 == -INFINITY) {
+            atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
+            atomicMin(&a.status[VFA_STATUS_MASKED_ROW], static_cast<unsigned>(lrow));
+          } else {
+            atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
+            atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], static_cast<unsigned>(lrow));
+          }
+        }
+        if (!finite) {
+          atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
+          atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+        }
+      }
+      if (a.stats) {
+        if (a.monitor) {
+          atomicAdd(&a.stats[VFA_STAT_OVER_F32], over32);
+          atomicAdd(&a.stats[VFA_STAT_OVER_F16], over16);
+        }
+        if (r == 0) {
+          atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
+          atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
+          atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_special));
+          atomicAdd(&a.stats[VFA_STAT_FROZEN], static_cast<unsigned long long>(n_frozen));
+        }
+      }
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tbase);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Key-block representations (src/vfa.py:47-88): one warp per key block, lane owns
+// D/32 consecutive columns; sabsmax keeps the first row on ties (strict >).
+template <int D>
+__global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restrict__ k, long long sb, long long sh,
+                                                    long long sr, int Hkv, int BC, int nblk, int kind,
+                                                    __nv_bfloat16* __restrict__ out) {
+  constexpr int CPL = D / 32;  // columns per lane (2 or 4)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jb = blockIdx.x * 4 + warp;
+  const int kvh = blockIdx.y, b = blockIdx.z;
+  if (jb >= nblk) return;
+  const __nv_bfloat16* base = k + b * sb + kvh * sh + static_cast<long long>(jb) * BC * sr + lane * CPL;
+  float best[CPL], val[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    best[c] = kind == VFA_KREPR_K_MEAN ? 0.f : -INFINITY;
+    val[c] = 0.f;
+  }
+  for (int row = 0; row < BC; ++row) {
+    float x[CPL];
+    if constexpr (CPL == 4) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(base + row * sr);
+      const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+      const __nv_bfloat162 p1 = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+      x[0] = __low2float(p0);
+      x[1] = __high2float(p0);
+      x[2] = __low2float(p1);
+      x[3] = __high2float(p1);
+    } else {
+      const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(base + row * sr);
+      x[0] = __low2float(p0);
+      x[1] = __high2float(p0);
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      switch (kind) {
+        case VFA_KREPR_SABSMAX:
+          if (fabsf(x[c]) > best[c]) {
+            best[c] = fabsf(x[c]);
+            val[c] = x[c];
+          }
+          break;
+        case VFA_KREPR_K_MAX:
+          best[c] = fmaxf(best[c], x[c]);
+          break;
+        case VFA_KREPR_K_MEAN:
+          best[c] += x[c];
+          break;
+        default:
+          best[c] = fmaxf(best[c], fabsf(x[c]));
+          break;
+      }
+    }
+  }
+  __nv_bfloat16* dst = out + ((static_cast<long long>(b) * Hkv + kvh) * nblk + jb) * D + lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    float r = kind == VFA_KREPR_SABSMAX ? val[c] : (kind == VFA_KREPR_K_MEAN ? best[c] / BC : best[c]);
+    dst[c] = __float2bfloat16_rn(r);
+  }
+}
+
+}  // namespace vfa
+
+// ====================================================================================
+// Host side
+// ====================================================================================
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 4-D bf16 tensor [B, H, L, D] (innermost D) with element strides; box {64, box_rows, 1, 1}.
+bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t L, int64_t D, int64_t sb,
+              int64_t sh, int64_t sr, int box_rows) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(B)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(sr * 2), static_cast<cuuint64_t>(sh * 2),
+                           static_cast<cuuint64_t>(sb * 2)};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int64_t n_key_blocks(const VfaParams* p) { return p->seq_k / p->k_block; }
+int64_t n_reprs(const VfaParams* p) {
+  int64_t tc = n_key_blocks(p);
+  return (p->tc1 > 0 && p->tc1 < tc) ? p->tc1 : tc;
+}
+
+template <int D, int BC, int NQ, int MODE>
+int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+               const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
+  using C = vfa::Cfg<D, BC, NQ>;
+  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    attr_set = true;
+  }
+  const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
+  if (units <= 0) return VFA_OK;
+  kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return VFA_OK;
+}
+
+template <int D, int BC, int NQ>
+int dispatch_mode(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                  const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
+  switch (p->variant) {
+    case VFA_VARIANT_FA:
+      return launch_fwd<D, BC, NQ, vfa::kFA>(p, mq, mk, mv, mr, args, st);
+    case VFA_VARIANT_VFA:
+      return launch_fwd<D, BC, NQ, vfa::kVFA>(p, mq, mk, mv, mr, args, st);
+    default:
+      return launch_fwd<D, BC, NQ, vfa::kVSA>(p, mq, mk, mv, mr, args, st);
+  }
+}
+
+template <int D, int BC>
+int dispatch_nq(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
+  return nq == 2 ? dispatch_mode<D, BC, 2>(p, mq, mk, mv, mr, args, st)
+                 : dispatch_mode<D, BC, 1>(p, mq, mk, mv, mr, args, st);
+}
+
+int launch_krepr(const VfaParams* p, const void* k, void* out, cudaStream_t st) {
+  const int nblk = static_cast<int>(n_reprs(p));
+  dim3 grid((nblk + 3) / 4, static_cast<unsigned>(p->heads_kv), static_cast<unsigned>(p->batch));
+  if (p->head_dim == 128)
+    vfa::krepr_kernel<128><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
+                                                p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
+                                                p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
+  else
+    vfa::krepr_kernel<64><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
+                                               p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
+                                               p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("krepr launch: ") + cudaGetErrorString(e));
+  return VFA_OK;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int vfa_check_params(const VfaParams* p) {
+  if (!p) return fail(VFA_ERR_CONFIG, "params is NULL");
+  if (p->variant < VFA_VARIANT_FA || p->variant > VFA_VARIANT_VSA)
+    return fail(VFA_ERR_CONFIG, "variant must be 0 (fa), 1 (vfa) or 2 (vsa)");
+  if (p->kind < VFA_KREPR_SABSMAX || p->kind > VFA_KREPR_K_ABSMAX_UNSIGNED)
+    return fail(VFA_ERR_CONFIG, "unknown key representation");
+  if (p->qkind != 0) return fail(VFA_ERR_CONFIG, "only the row_wise query representation runs on the GPU path");
+  if (p->q_block != 128) return fail(VFA_ERR_CONFIG, "q_block must be 128 (tcgen05 M = 128)");
+  if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
+  if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
+  if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
+  if (p->variant == VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
+  if (p->batch < 1 || p->heads_q < 1 || p->heads_kv < 1 || p->seq_q < 1 || p->seq_k < 1)
+    return fail(VFA_ERR_DATA, "all dimensions must be >= 1");
+  if (p->heads_q % p->heads_kv) return fail(VFA_ERR_DATA, "heads_q must be a multiple of heads_kv");
+  if (p->seq_q % p->q_block)
+    return fail(VFA_ERR_DATA, "seq_len_q=" + std::to_string(p->seq_q) + " not divisible by q_block=" +
+                                  std::to_string(p->q_block));
+  if (p->seq_k % p->k_block)
+    return fail(VFA_ERR_DATA, "seq_len_k=" + std::to_string(p->seq_k) + " not divisible by k_block=" +
+                                  std::to_string(p->k_block));
+  if (p->causal && p->seq_q != p->seq_k) return fail(VFA_ERR_DATA, "causal masking requires N_q == N_k");
+  if (p->tc1 < 0 || p->tc1 > n_key_blocks(p))
+    return fail(VFA_ERR_CONFIG, "tc1 must be in 1..T_c (0 = all)");
+  const int64_t* strides[4] = {p->q_stride, p->k_stride, p->v_stride, p->o_stride};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (strides[i][j] % 8 != 0 || strides[i][j] < 0)
+        return fail(VFA_ERR_DATA, "strides must be non-negative multiples of 8 elements (16 bytes)");
+  if (p->seq_q * p->heads_q * p->batch >= 0xffffffffLL) return fail(VFA_ERR_DATA, "too many rows");
+  return VFA_OK;
+}
+
+size_t vfa_workspace_bytes(const VfaParams* p) {
+  if (!p || vfa_check_params(p) != VFA_OK) return 0;
+  return static_cast<size_t>(p->batch * p->heads_kv * n_reprs(p) * p->head_dim * 2) + 256;
+}
+
+int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!k || !out) return fail(VFA_ERR_DATA, "NULL pointer");
+  return launch_krepr(p, k, out, static_cast<cudaStream_t>(stream));
+}
+
+int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+            void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+            unsigned char* skip_trace, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!q || !k || !v || !o) return fail(VFA_ERR_DATA, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool minit = p->variant != VFA_VARIANT_FA && p->use_m_init;
+  const int64_t nrep = n_reprs(p);
+  if (minit) {
+    if (!workspace || workspace_bytes < vfa_workspace_bytes(p) || !aligned16(workspace))
+      return fail(VFA_ERR_DATA, "workspace too small or misaligned");
+  }
+  const int D = static_cast<int>(p->head_dim), BC = p->k_block;
+  const int group = static_cast<int>(p->heads_q / p->heads_kv);
+  const int nq = (group % 2 == 0) ? 2 : 1;
+
+  CUtensorMap mq, mk, mv, mr;
+  if (!make_map(&mq, q, p->batch, p->heads_q, p->seq_q, D, p->q_stride[0], p->q_stride[1], p->q_stride[2], 128) ||
+      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2], BC) ||
+      !make_map(&mv, v, p->batch, p->heads_kv, p->seq_k, D, p->v_stride[0], p->v_stride[1], p->v_stride[2], BC))
+    return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  if (minit) {
+    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, BC))
+      return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed (krepr)");
+    if (!p->krepr_precomputed) {
+      rc = launch_krepr(p, k, workspace, st);
+      if (rc) return rc;
+    }
+  } else {
+    mr = mk;
+  }
+  if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * VFA_STAT_COUNT, st);
+  if (status) {
+    cudaMemsetAsync(status, 0, sizeof(unsigned) * VFA_STATUS_COUNT, st);
+    cudaMemsetAsync(status + VFA_STATUS_UNDERFLOW_ROW, 0xff, sizeof(unsigned) * 2, st);
+  }
+  if (skip_trace)
+    cudaMemsetAsync(skip_trace, 0,
+                    static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * n_key_blocks(p)), st);
+
+  vfa::FwdArgs a;
+  a.B = static_cast<int>(p->batch);
+  a.Hq = static_cast<int>(p->heads_q);
+  a.Hkv = static_cast<int>(p->heads_kv);
+  a.Lq = static_cast<int>(p->seq_q);
+  a.Lk = static_cast<int>(p->seq_k);
+  a.group = group;
+  a.Tr = static_cast<int>(p->seq_q / 128);
+  a.Tc = static_cast<int>(n_key_blocks(p));
+  a.heads_per_unit = nq;
+  a.units_per_kvh = a.Tr * (group / nq);
+  const double scale = p->scale > 0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(D));
+  a.c_scale = static_cast<float>(scale * 1.4426950408889634);
+  a.log2_lambda = (p->variant == VFA_VARIANT_VSA && p->lam > 0) ? static_cast<float>(std::log2(p->lam)) : -INFINITY;
+  a.causal = p->causal ? 1 : 0;
+  a.reorder = p->reorder ? 1 : 0;
+  a.use_m_init = minit ? 1 : 0;
+  a.nrep_cap = static_cast<int>(nrep);
+  a.n_sink = p->n_sink;
+  a.n_local = p->n_local;
+  a.monitor = p->monitor ? 1 : 0;
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.o_sb = p->o_stride[0];
+  a.o_sh = p->o_stride[1];
+  a.o_sr = p->o_stride[2];
+  a.lse = lse;
+  a.stats = reinterpret_cast<unsigned long long*>(stats);
+  a.status = status;
+  a.skip_trace = skip_trace;
+
+  if (D == 128 && BC == 128) return dispatch_nq<128, 128>(p, nq, mq, mk, mv, mr, a, st);
+  if (D == 128 && BC == 64) return dispatch_nq<128, 64>(p, nq, mq, mk, mv, mr, a, st);
+  if (D == 64 && BC == 128) return dispatch_nq<64, 128>(p, nq, mq, mk, mv, mr, a, st);
+  return dispatch_nq<64, 64>(p, nq, mq, mk, mv, mr, a, st);
+}
+
+int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local, int reorder,
+                 int variant, int* order_out, unsigned char* special_out, int cap) {
+  if (i < 1 || q_block < 1 || k_block < 1 || t_c < 1) return -VFA_ERR_CONFIG;
+  vfa::TileSchedule s = vfa::make_schedule(i, q_block, k_block, t_c, causal != 0, n_sink, n_local,
+                                           variant != VFA_VARIANT_FA && reorder != 0, variant == VFA_VARIANT_FA);
+  for (int pos = 0; pos < s.vmax && pos < cap; ++pos) {
+    int j = vfa::sched_block(s, pos);
+    if (order_out) order_out[pos] = j;
+    if (special_out) special_out[pos] = vfa::sched_is_special(s, j) ? 1 : 0;
+  }
+  return s.vmax;
+}
+
+int vfa_status_code(const unsigned int* status_host) {
+  if (!status_host) return fail(VFA_ERR_CONFIG, "status is NULL");
+  if (status_host[VFA_STATUS_FLAGS] & 3u) {
+    if (status_host[VFA_STATUS_FLAGS] & 1u)
+      return fail(VFA_ERR_NUMERICAL, "query row " + std::to_string(status_host[VFA_STATUS_MASKED_ROW]) +
+                                         " is fully masked; cannot normalize");
+    return fail(VFA_ERR_NUMERICAL,
+                "normalizer underflow at query row " + std::to_string(status_host[VFA_STATUS_UNDERFLOW_ROW]));
+  }
+  return VFA_OK;
+}
+
+const char* vfa_last_error(void) { return g_last_error.c_str(); }
+
+const char* vfa_version(void) { return "vfa_b200 0.1.0 (sm_100a, tcgen05/TMEM/TMA)"; }
+
+}  // extern "C"

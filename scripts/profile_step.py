@@ -1,0 +1,32 @@
+"""One C2 forward of a chosen variant, for ncu captures (numbers printed under ncu are not bench values).
+
+    ncu --set full -k regex:vfa_fwd_kernel -s 1 -c 1 -o prof python scripts/profile_step.py --variant vfa
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import CONFIGS, Runner, make_inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--variant", default="vfa", choices=("fa", "vfa", "vsa"))
+ap.add_argument("--config", default="c2", choices=tuple(CONFIGS))
+ap.add_argument("--lam", type=float, default=1e-2)
+ap.add_argument("--k-block", type=int, default=128)
+ap.add_argument("--head-dim", type=int, default=128)
+ap.add_argument("--iters", type=int, default=2)
+a = ap.parse_args()
+cfg = dict(CONFIGS[a.config])
+cfg["d"] = a.head_dim
+dev = torch.device("cuda", 0)
+q, k, v = make_inputs(cfg, dev)
+r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block)
+sh = torch.cuda.current_stream().cuda_stream
+for _ in range(a.iters):
+    r.krepr(sh)
+    r.attn(sh)
+torch.cuda.synchronize()
+print(a.variant, r.stats_dict())

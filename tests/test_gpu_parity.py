@@ -1,0 +1,294 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Inputs are bf16; the oracle computes in float64 on the identical (upcast) values.
+Tolerances (bf16 inputs, fp32 S / l / O accumulation, bf16 P and bf16 O):
+  O   : max |O_gpu - O_ref| <= 2e-2 and max_rel_err (tests/conftest.py:42-46 metric) <= 2e-2
+  LSE : max |LSE_gpu - LSE_ref| <= 1e-3
+  visit statistics (visited / special / frozen / skipped): exact
+  VSA skip decisions: exact wherever the oracle's decision margin exceeds 1e-3
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import case, case_bits, case_names
+from oracle import vfa_oracle as vo
+
+pytestmark = pytest.mark.gpu
+
+O_ABS, O_REL, LSE_ABS = 2e-2, 2e-2, 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2604_12798_b200 import build
+    build.build()
+
+
+def _rand(shape, seed, dev="cuda"):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+
+
+def _f64(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _run_gpu(q, k, v, **kw):
+    from paper_2604_12798_b200 import attention_forward, stats_dict
+    out, lse, info = attention_forward(q, k, v, check=False, **kw)
+    torch.cuda.synchronize()
+    return out, lse, info, stats_dict(info)
+
+
+def _compare(out, lse, ref_o, ref_lse, tag=""):
+    o = _f64(out)
+    l = lse.double().cpu().numpy()
+    assert np.isfinite(o).all(), f"{tag}: non-finite output"
+    err = np.abs(o - ref_o).max()
+    rel = vo.max_rel_err(o, ref_o)
+    lerr = np.abs(l - ref_lse).max()
+    assert err <= O_ABS, f"{tag}: O max abs err {err}"
+    assert rel <= O_REL, f"{tag}: O max_rel_err {rel}"
+    assert lerr <= LSE_ABS, f"{tag}: LSE max abs err {lerr}"
+    return err, rel, lerr
+
+
+CONFIGS = []
+for variant in ("fa", "vfa", "vsa"):
+    for d in (64, 128):
+        for bc in (64, 128):
+            for causal in (True, False):
+                CONFIGS.append((variant, d, bc, causal))
+
+
+@pytest.mark.parametrize("variant,d,bc,causal", CONFIGS)
+def test_parity_matrix(variant, d, bc, causal):
+    B, Hq, Hkv, L = 1, 2, 1, 512
+    seed = hash((variant, d, bc, causal)) % 1000
+    q, k, v = _rand((B, Hq, L, d), seed), _rand((B, Hkv, L, d), seed + 1), _rand((B, Hkv, L, d), seed + 2)
+    kw = dict(variant=variant, causal=causal, q_block=128, k_block=bc)
+    if variant == "vsa":
+        kw["lam"] = 1e-2
+    out, lse, info, st = _run_gpu(q, k, v, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    for key in ("visited", "special", "frozen"):
+        if variant != "vsa":
+            assert st[key] == ref_st[key], (key, st, ref_st)
+    assert st["visited"] == ref_st["visited"]
+
+
+@pytest.mark.parametrize("hq,hkv,b", [(1, 1, 1), (3, 1, 1), (8, 2, 2), (4, 4, 1)])
+def test_gqa_and_single_tile_paths(hq, hkv, b):
+    L, d = 384, 128
+    q, k, v = _rand((b, hq, L, d), 11), _rand((b, hkv, L, d), 12), _rand((b, hkv, L, d), 13)
+    for variant in ("fa", "vfa"):
+        kw = dict(variant=variant, causal=True, q_block=128, k_block=128)
+        out, lse, _, st = _run_gpu(q, k, v, **kw)
+        ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+        _compare(out, lse, ref_o, ref_lse, f"{variant} hq={hq} hkv={hkv} b={b}")
+        assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
+
+
+@pytest.mark.parametrize("kind", ["sabsmax", "k_max", "k_mean", "k_absmax_unsigned"])
+@pytest.mark.parametrize("opts", [dict(), dict(reorder=False), dict(use_m_init=False), dict(tc1=2),
+                                  dict(n_sink=2, n_local=2), dict(n_sink=1, n_local=2, k_block=64),
+                                  dict(n_sink=0, n_local=1)])
+def test_vfa_options(kind, opts):
+    L, d = 640, 128
+    q, k, v = _rand((1, 2, L, d), 21), _rand((1, 1, L, d), 22), _rand((1, 1, L, d), 23)
+    kw = dict(variant="vfa", causal=True, q_block=128, k_block=128, kind=kind)
+    kw.update(opts)
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
+
+
+@pytest.mark.parametrize("name", [n for n in case_names()])
+def test_golden_vectors(name):
+    m, q, k, v, out32, lse = case(name)
+    if m["q_block"] != 128:
+        pytest.skip("q_block 64 runs on the CPU oracle only (tcgen05 M = 128)")
+    from paper_2604_12798_b200 import attention_forward, stats_dict
+    from paper_2604_12798_b200.api import NormalizerUnderflowError
+    qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda()[None, None]
+                  for x in case_bits(name))
+    kw = dict(variant=m["variant"], causal=m["causal"], q_block=128, k_block=m["k_block"],
+              n_sink=m["n_sink"], n_local=m["n_local"])
+    for key in ("kind", "reorder", "use_m_init", "tc1", "lam"):
+        if key in m:
+            kw[key] = m[key]
+    if m["error"]:
+        with pytest.raises(NormalizerUnderflowError) as ei:
+            attention_forward(qb, kb, vb, **kw)
+        assert ei.value.row == int(m["error"].split(":")[1])
+        return
+    out, lse_g, info = attention_forward(qb, kb, vb, check=False, monitor=True, **kw)
+    st = stats_dict(info)
+    if m.get("mon.count_over_f32", 0) > 0:
+        # frozen-max overflow: float64 stays finite, fp32 exp2 may not; must be reported
+        assert st["count_over_f32"] > 0
+        o = _f64(out[0, 0])
+        if not np.isfinite(o).all():
+            assert st["nonfinite_rows"] > 0
+        return
+    _compare(out[0, 0], lse_g[0, 0], out32.astype(np.float64), lse, name)
+    if "stats.blocks_visited" in m:
+        assert st["visited"] == m["stats.blocks_visited"]
+        assert st["skipped"] == m["stats.blocks_skipped"]
+        assert st["special"] == m["stats.processed_special"]
+        assert st["frozen"] == m["stats.processed_frozen"]
+    if "counters.rescale_events" in m and m["variant"] != "vsa":
+        assert st["special"] == m["counters.rescale_events"]
+        assert st["special"] + st["frozen"] == m["counters.blocks_processed"]
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("bc", [64, 128])
+@pytest.mark.parametrize("kind", ["sabsmax", "k_max", "k_mean", "k_absmax_unsigned"])
+def test_krepr_kernel(d, bc, kind):
+    from paper_2604_12798_b200 import AttentionProblem, BlockSpec, precompute_kreprs
+    L = 1024
+    k = _rand((2, 3, L, d), 31)
+    k[0, 0, 5, 3] = -k[0, 0, 7, 3].abs() - 1  # planted ties / signs
+    q = _rand((2, 3, L, d), 32)
+    p = AttentionProblem(q, k, k, blocks=BlockSpec(L, L, d, 128, bc))
+    got = _f64(precompute_kreprs(p, kind))
+    kk = _f64(k)
+    for b in range(2):
+        for h in range(3):
+            ref = np.stack(vo.precompute_kreprs(kk[b, h], bc, kind))
+            if kind == "k_mean":
+                assert np.abs(got[b, h] - ref).max() <= 2e-2 * np.abs(ref).max() + 1e-3
+            else:
+                assert np.array_equal(got[b, h], ref)  # selected elements: exact in bf16
+
+
+def _planted_sink(L, d, boost, seed, hq=2):
+    q, k, v = _rand((1, hq, L, d), seed), _rand((1, 1, L, d), seed + 1), _rand((1, 1, L, d), seed + 2)
+    amp = float(np.sqrt(boost * np.sqrt(d)))
+    q[..., 0] = amp
+    k[..., 0] = 0
+    k[:, :, :128, 0] = amp
+    return q, k, v
+
+
+@pytest.mark.parametrize("lam", [1e-4, 1e-3, 3e-3, 1e-2, 1e-1])
+def test_vsa_skip_decisions(lam):
+    L, d = 2048, 128
+    q, k, v = _planted_sink(L, d, 8.0, 41)
+    kw = dict(variant="vsa", causal=True, q_block=128, k_block=128, lam=lam)
+    from paper_2604_12798_b200 import attention_forward
+    out, lse, info = attention_forward(q, k, v, check=False, skip_trace=True, **kw)
+    trace = info["skip_trace"].cpu().numpy()
+    qq, kk, vv = _f64(q), _f64(k), _f64(v)
+    ref_o = np.empty(qq.shape)
+    flips = 0
+    for h in range(2):
+        r = vo.forward_head(qq[0, h], kk[0, 0], vv[0, 0], record_decisions=True, **kw)
+        ref_o[0, h] = r.out
+        for i, dec in enumerate(r.decisions):
+            for pos, (j, skip, margin) in enumerate(dec):
+                g = trace[0, h, i, pos]
+                assert g in (1, 2)
+                if margin > 1e-3:
+                    assert (g == 2) == skip, (h, i, pos, j, margin)
+                elif (g == 2) != skip:
+                    flips += 1
+    assert flips <= 2
+    if flips == 0:
+        assert np.abs(_f64(out) - ref_o).max() <= O_ABS
+
+
+def test_vsa_tiny_lambda_bitwise_equals_vfa():
+    # reference tests/test_sparse.py:148-153 on the device path
+    q, k, v = _rand((1, 4, 1024, 128), 51), _rand((1, 2, 1024, 128), 52), _rand((1, 2, 1024, 128), 53)
+    base = dict(causal=True, q_block=128, k_block=128)
+    o1, l1, _, _ = _run_gpu(q, k, v, variant="vfa", **base)
+    o2, l2, _, st = _run_gpu(q, k, v, variant="vsa", lam=1e-9, **base)
+    assert st["skipped"] == 0
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_single_key_block_vfa_equals_fa():
+    # reference tests/test_vfa.py:115-125: T_c = 1 -> the one block is special
+    q, k, v = _rand((1, 2, 128, 64), 61), _rand((1, 1, 128, 64), 62), _rand((1, 1, 128, 64), 63)
+    o1, l1, _, _ = _run_gpu(q, k, v, variant="fa", causal=True)
+    o2, l2, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True, use_m_init=False)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_deterministic_and_head_sharding_invariant():
+    q, k, v = _rand((1, 8, 1024, 128), 71), _rand((1, 2, 1024, 128), 72), _rand((1, 2, 1024, 128), 73)
+    o1, l1, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True)
+    o2, l2, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True)
+    assert torch.equal(o1, o2)
+    # shard by KV-head group exactly as bench.py does for multi-GPU runs
+    o3, l3, _, _ = _run_gpu(q[:, 4:].contiguous(), k[:, 1:].contiguous(), v[:, 1:].contiguous(),
+                            variant="vfa", causal=True)
+    assert torch.equal(o1[:, 4:], o3) and torch.equal(l1[:, 4:], l3)
+
+
+def test_strided_inputs():
+    base = _rand((1, 1024, 4, 128), 81)  # [B, L, H, d] layout viewed as [B, H, L, d]
+    q = base.permute(0, 2, 1, 3)
+    kv = _rand((1, 1024, 2, 128), 82).permute(0, 2, 1, 3)
+    out, lse, _, _ = _run_gpu(q, kv, kv, variant="vfa", causal=True)
+    ref_o, ref_lse, _ = vo.forward(_f64(q), _f64(kv), _f64(kv), variant="vfa", causal=True,
+                                   q_block=128, k_block=128)
+    _compare(out, lse, ref_o, ref_lse, "strided")
+
+
+def test_large_context_sampled_head():
+    # C2 geometry per head (d=128, Bc=128) at L=8192: one head checked against the oracle
+    L = 8192
+    q, k, v = _rand((1, 4, L, 128), 91), _rand((1, 1, L, 128), 92), _rand((1, 1, L, 128), 93)
+    out, lse, _, st = _run_gpu(q, k, v, variant="vfa", causal=True)
+    r = vo.forward_head(_f64(q[0, 3]), _f64(k[0, 0]), _f64(v[0, 0]), variant="vfa", causal=True,
+                        q_block=128, k_block=128)
+    _compare(out[0, 3], lse[0, 3], r.out, r.lse, "L=8192")
+    t_r = L // 128
+    assert st["special"] == 4 * sum(min(2, i) for i in range(1, t_r + 1))
+
+
+def test_validation_errors_raise_like_reference():
+    from paper_2604_12798_b200 import attention_forward
+    q = _rand((1, 1, 200, 128), 1)
+    with pytest.raises(ValueError):
+        attention_forward(q, q, q, variant="vfa")  # 200 % 128 != 0 (src/tensor.py:37-44)
+    q = _rand((1, 1, 256, 128), 1)
+    with pytest.raises(ValueError):
+        attention_forward(q, q, q, variant="vsa", lam=1.5)
+    with pytest.raises(ValueError):
+        attention_forward(q, q, q, variant="vfa", kind="median")
+    with pytest.raises(ValueError):
+        attention_forward(q, q, q, variant="vfa", q_block=64)
+    k = _rand((1, 1, 128, 128), 2)
+    with pytest.raises(ValueError):
+        attention_forward(q, k, k, variant="fa", causal=True)  # causal needs Nq == Nk
+
+
+def test_dropin_api_mirrors_reference():
+    # reference-shaped call: 2-D single head, numpy inputs, tuple results
+    from paper_2604_12798_b200 import (AttentionProblem, BlockSpec, SkipConfig, fa_forward,
+                                       vfa_forward, vsa_forward)
+    rng = np.random.default_rng(5)
+    L, d = 512, 64
+    q, k, v = (torch.from_numpy(rng.normal(size=(L, d))).to(torch.bfloat16) for _ in range(3))
+    qf, kf, vf = (x.double().numpy() for x in (q, k, v))
+    p = AttentionProblem(q, k, v, blocks=BlockSpec(L, L, d, 128, 128), causal=True)
+    out, counters, trace, mon = vfa_forward(p)
+    r = vo.forward_head(qf, kf, vf, variant="vfa", causal=True, q_block=128, k_block=128)
+    assert out.shape == (L, d) and trace is None
+    assert vo.max_rel_err(_f64(out), r.out) <= O_REL
+    t_r = L // 128
+    assert counters.rowmax_reductions == sum(min(2, i) for i in range(1, t_r + 1))
+    assert counters.blocks_processed == sum(range(1, t_r + 1))
+    o2, c2, _ = fa_forward(p)
+    assert c2.rescale_events == sum(range(1, t_r + 1))
+    o3, c3, stats, _ = vsa_forward(p, SkipConfig(lam=1e-9))
+    assert stats.blocks_skipped == 0 and torch.equal(o3, out)
+    assert c3.rowmax_reductions == stats.blocks_visited
