@@ -13,6 +13,8 @@ import threading
 
 LIB_NAME = "libvfa_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# experiments only (e.g. tuning-knob sweeps): load an alternative in-tree build
+LIB_PATH = os.environ.get("VFA_B200_LIB", LIB_PATH)
 
 VFA_OK = 0
 VFA_ERR_CONFIG = 2

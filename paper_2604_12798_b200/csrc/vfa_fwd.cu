@@ -137,6 +137,100 @@ __device__ __forceinline__ bool needs_corr(const TileSchedule& s, int pos, bool*
 }
 
 // ------------------------------------------------------------------------------------
+// Softmax element math. x = s * (scale*log2 e) - m2 in packed pairs (FFMA2); P = exp2(x)
+// on MUFU.EX2 for most pairs and on the FMA pipe (degree-4 polynomial, |rel err| < 3e-6)
+// for kPoly of every 8 pairs, so that neither the XU nor the FMA pipe limits the
+// tensor core; row sums accumulate in packed FADD2; P is packed to bf16 pairs.
+#ifndef VFA_POLY_PAIRS
+#define VFA_POLY_PAIRS 3
+#endif
+constexpr int kPolyPairs = VFA_POLY_PAIRS;  // of every 8 element pairs (tuning knob)
+
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  // clamp to [-127, 128]: x <= -127 (incl. masked -inf) gives exactly +0 (the exponent add
+  // wraps 1.0 * 2^-127 to 0x00000000, matching MUFU.EX2.FTZ), x >= 128 gives +inf like MUFU
+  x.x = fminf(fmaxf(x.x, -127.f), 128.f);
+  x.y = fminf(fmaxf(x.y, -127.f), 128.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: round to integer
+  const float2 r = __fadd2_rn(x, magic);
+  const float2 jf = __fadd2_rn(r, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-jf.x, -jf.y));  // f in [-0.5, 0.5]
+  float2 p = __ffma2_rn(make_float2(0.009582853876054287f, 0.009582853876054287f), f,
+                        make_float2(0.05590642988681793f, 0.05590642988681793f));
+  p = __ffma2_rn(p, f, make_float2(0.24024099111557007f, 0.24024099111557007f));
+  p = __ffma2_rn(p, f, make_float2(0.6931241750717163f, 0.6931241750717163f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  // scale by 2^j: add j to the exponent field (the low bits of r hold j)
+  float2 y;
+  y.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(r.x) << 23));
+  y.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(r.y) << 23));
+  return y;
+}
+
+template <bool MON>
+__device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o16) {
+  if (MON) {
+    // OverflowMonitor (src/vfa.py:122-128) thresholds, in log2 units
+    o32 += (x.x > 128.0f) + (x.y > 128.0f);
+    o16 += (x.x > 15.999295f) + (x.y > 15.999295f);
+  }
+}
+
+// 32 consecutive columns: P = exp2(s*cs - m2) -> 16 packed bf16x2 words, row sum into acc.
+template <bool MON, bool MASK, int kPoly>
+__device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu2, int lim, uint32_t* u,
+                                          float2& acc, uint32_t& o32, uint32_t& o16) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    float2 s = make_float2(v[e], v[e + 1]);
+    if (MASK) {
+      s.x = (e > lim) ? -INFINITY : s.x;
+      s.y = (e + 1 > lim) ? -INFINITY : s.y;
+    }
+    const float2 x = __ffma2_rn(s, cs2, nmu2);
+    count_over<MON>(x, o32, o16);
+    float2 p;
+    if (((e >> 1) & 7) < kPoly) {
+      p = ex2_poly2(x);
+    } else {
+      p.x = ex2_approx(x.x);
+      p.y = ex2_approx(x.y);
+    }
+    acc = __fadd2_rn(acc, p);
+    u[e >> 1] = pack_bf16x2(p.x, p.y);
+  }
+}
+
+// Frozen block: stream S from TMEM in 32-column chunks, write P (bf16) back over the
+// already-read columns. One chunk body in the instruction stream (unroll 1).
+template <int BC, bool MON, bool MASK, int kPoly>
+__device__ __forceinline__ void p_frozen(uint32_t tS, float2 cs2, float2 nmu2, int lim, float2& acc,
+                                         uint32_t& o32, uint32_t& o16) {
+#pragma unroll 1
+  for (int c = 0; c < BC / 32; ++c) {
+    float v[32];
+    tmem_ld32(tS + c * 32, v);
+    tmem_wait_ld();
+    reg_fence32(v);
+    uint32_t u[16];
+    p_chunk32<MON, MASK, kPoly>(v, cs2, nmu2, lim - c * 32, u, acc, o32, o16);
+    tmem_st16(tS + c * 16, u);
+  }
+}
+
+// Exact-update block: the row is already in registers (masked entries -inf).
+template <int BC, bool MON, int kPoly>
+__device__ __forceinline__ void p_row(const float* v, uint32_t tS, float2 cs2, float2 nmu2, float2& acc,
+                                      uint32_t& o32, uint32_t& o16) {
+#pragma unroll
+  for (int c = 0; c < BC / 32; ++c) {
+    uint32_t u[16];
+    p_chunk32<MON, false, kPoly>(v + c * 32, cs2, nmu2, BC, u, acc, o32, o16);
+    tmem_st16(tS + c * 16, u);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 template <int D, int BC, int NQ, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -156,12 +250,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
-
-  const Unit unit = decode_unit(a, blockIdx.x);
-  const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);
-  const int N = sched.vmax;
-  int nrep = 0;
-  const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);
 
   if (tid == 0) {
     for (int t = 0; t < NQ; ++t) {
@@ -190,12 +278,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = ctl->tmem_base;
+  // Each role re-derives its work description after its setmaxnreg so that nothing
+  // computed before the role split has to stay live (or spill) across it.
+#define VFA_ROLE_SETUP()                                                       \
+  const uint32_t tbase = ctl->tmem_base;                                       \
+  const Unit unit = decode_unit(a, blockIdx.x);                                \
+  const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);              \
+  const int N = sched.vmax;                                                    \
+  int nrep = 0;                                                                \
+  const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);                 \
+  (void)tbase; (void)nrep; (void)nchunks; (void)N
 
   if (warp == 13) {
     // ============================ TMA producer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
     if (lane == 0) {
+      VFA_ROLE_SETUP();
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       for (int t = 0; t < NQ; ++t) {
@@ -230,8 +328,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ============================ MMA issuer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
     if (lane == 0) {
+      VFA_ROLE_SETUP();
       constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
       constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      // UMMA smem descriptors: hi word constant (SBO = 1024 B, version 1, SWIZZLE_128B),
+      // lo word = (address >> 4) | LBO << 16. Addresses < 256 KiB so the start field never carries.
+      constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+      constexpr uint32_t kLboK = 1u << 16;                       // K-major: LBO unused
+      constexpr uint32_t kLboV = static_cast<uint32_t>((BC * 128) >> 4) << 16;  // V: next 64-col chunk
+      const uint32_t q_lo = smem_u32(sQ) >> 4;
+      const uint32_t kv_lo = smem_u32(sKV) >> 4;
       for (int t = 0; t < NQ; ++t) mbar_wait(&ctl->q_full[t], 0);
       tc_fence_after();
       int stage = 0;
@@ -239,32 +345,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto acquire = [&]() -> int {
         mbar_wait(&ctl->kv_full[stage], phase);
         tc_fence_after();
-        int s = stage;
+        int st = stage;
         if (++stage == NS) {
           stage = 0;
           phase ^= 1;
         }
-        return s;
+        return st;
       };
-      auto issue_qk = [&](int t, int s) {
-        const uint32_t qa = smem_u32(sQ + t * C::kQBytes);
-        const uint32_t kb = smem_u32(sKV + s * C::kKVBytes);
-        const uint32_t dS = tbase + C::s_off(t);
+      auto issue_qk = [&](int t, int st) {
+        const uint32_t a_lo = q_lo + t * (C::kQBytes >> 4) + kLboK;
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oq = (kk >> 2) * (kBR * 128) + (kk & 3) * 32;
-          const uint32_t ok = (kk >> 2) * (BC * 128) + (kk & 3) * 32;
-          mma_ss(dS, make_sw128_desc(qa + oq, 16, 1024), make_sw128_desc(kb + ok, 16, 1024), kIdescQK,
-                 kk > 0 ? 1u : 0u);
+          const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+          const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
+          mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
+                 (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
         }
       };
-      auto issue_pv = [&](int t, int s, bool acc) {
-        const uint32_t vb = smem_u32(sKV + s * C::kKVBytes);
-        const uint32_t dO = tbase + C::kOBase + t * D;
-        const uint32_t aP = tbase + C::s_off(t);
+      auto issue_pv = [&](int t, int st, bool acc) {
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
         for (int kk = 0; kk < BC / 16; ++kk)
-          mma_ts(dO, aP + kk * 8, make_sw128_desc(vb + kk * 2048, BC * 128, 1024), kIdescPV,
+          mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + kk * 8,
+                 (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
                  (acc || kk > 0) ? 1u : 0u);
       };
       uint32_t sfree_ph[NQ], p_ph[NQ], ordy_ph[NQ];
@@ -339,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
   } else if (warp >= 8) {
     // ============================ correction WG ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+    VFA_ROLE_SETUP();
     const int r = tid - 256;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     uint32_t sc_ph[NQ], of_ph[NQ];
@@ -357,16 +462,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool work = (MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f);
         if (work) {
           const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float v[32];
-            tmem_ld32(tO + c * 32, v);
+          const float2 f2 = make_float2(f, f);
+#pragma unroll 1
+          for (int c = 0; c < D / 16; ++c) {
+            float v[16];
+            tmem_ld16(tO + c * 16, v);
             tmem_wait_ld();
-            reg_fence32(v);
-            uint32_t u[32];
+            reg_fence16(v);
+            uint32_t u[16];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(v[e] * f);
-            tmem_st32(tO + c * 32, u);
+            for (int e = 0; e < 16; e += 2) {
+              const float2 o = __fmul2_rn(make_float2(v[e], v[e + 1]), f2);
+              u[e] = __float_as_uint(o.x);
+              u[e + 1] = __float_as_uint(o.y);
+            }
+            tmem_st16(tO + c * 16, u);
           }
           tmem_wait_st();
         }
@@ -377,10 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ============================ softmax WGs ============================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
     const int t = warp >> 2;
     const int r = tid & 127;
     if (t < NQ) {
+      VFA_ROLE_SETUP();
       const int h = unit.h0 + t;
       const int R = unit.qt * kBR + r;  // absolute query row
       const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -390,8 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m2 = -INFINITY;  // running max, log2 units of scaled scores
       float l = 0.f;
       uint32_t s_ph = 0;
-      long long n_special = 0, n_frozen = 0, n_skipped = 0;
-      unsigned long long over32 = 0, over16 = 0;
+      int n_special = 0, n_frozen = 0, n_skipped = 0;
+      uint32_t over32 = 0, over16 = 0;
 
       // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
       if (nchunks > 0) {
@@ -418,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         m2 = mx * cs;
       }
 
+      const float2 cs2 = make_float2(cs, cs);
       for (int pos = 0; pos < N; ++pos) {
         const int j = sched_block(sched, pos);
         const bool special = (MODE == kFA) || sched_is_special(sched, j);
@@ -428,8 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_ph ^= 1;
         tc_fence_after();
         bool skipped = false;
+        float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this tile's P (pairs)
         if (MODE == kFA || MODE == kVSA || special) {
-          // ---- full row in registers: rowmax (+ skip test) (+ rescale)
+          // ---- exact-update / skip-test block: rowmax over the full row (src/vfa.py:202-208,
+          //      src/sparse.py:296-300), then rescale and exponentiate
           float v[BC];
 #pragma unroll
           for (int c = 0; c < BC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
@@ -457,7 +571,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_arrive(&ctl->sc_full[t]);
             }
           } else {
-            float mu;
             if (special) {
               const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
               m2 = m2n;
@@ -470,63 +583,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               ++n_frozen;
             }
-            mu = (m2 == -INFINITY) ? 0.f : m2;
-            float ls0 = 0.f, ls1 = 0.f;
-#pragma unroll
-            for (int c = 0; c < BC / 32; ++c) {
-              uint32_t u[16];
-#pragma unroll
-              for (int e = 0; e < 32; e += 2) {
-                const float x0 = fmaf(v[c * 32 + e], cs, -mu);
-                const float x1 = fmaf(v[c * 32 + e + 1], cs, -mu);
-                if (a.monitor) {
-                  over32 += (x0 > 128.0f) + (x1 > 128.0f);
-                  over16 += (x0 > 15.999295f) + (x1 > 15.999295f);
-                }
-                const float p0 = ex2_approx(x0);
-                const float p1 = ex2_approx(x1);
-                ls0 += p0;
-                ls1 += p1;
-                u[e >> 1] = pack_bf16x2(p0, p1);
-              }
-              tmem_st16(tS + c * 16, u);
-            }
-            l = __fadd_rn(l, __fadd_rn(ls0, ls1));
+            const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
+            // masked entries are -inf in v and exponentiate to exact zeros on both paths
+            if (a.monitor)
+              p_row<BC, true, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
+            else
+              p_row<BC, false, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
           }
         } else {
-          // ---- frozen block (VFA): no rowmax, no rescale; streamed in 32-column chunks
-          const float mu = (m2 == -INFINITY) ? 0.f : m2;
-          float ls0 = 0.f, ls1 = 0.f;
-#pragma unroll
-          for (int c = 0; c < BC / 32; ++c) {
-            float v[32];
-            tmem_ld32(tS + c * 32, v);
-            tmem_wait_ld();
-            reg_fence32(v);
-            if (mask) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) v[e] = (c * 32 + e > lim) ? -INFINITY : v[e];
-            }
-            uint32_t u[16];
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float x0 = fmaf(v[e], cs, -mu);
-              const float x1 = fmaf(v[e + 1], cs, -mu);
-              if (a.monitor) {
-                over32 += (x0 > 128.0f) + (x1 > 128.0f);
-                over16 += (x0 > 15.999295f) + (x1 > 15.999295f);
-              }
-              const float p0 = ex2_approx(x0);
-              const float p1 = ex2_approx(x1);
-              ls0 += p0;
-              ls1 += p1;
-              u[e >> 1] = pack_bf16x2(p0, p1);
-            }
-            tmem_st16(tS + c * 16, u);
+          // ---- frozen block (VFA, src/vfa.py:209-215): no rowmax, no rescale, streamed chunks
+          const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
+          if (a.monitor) {
+            if (mask) p_frozen<BC, true, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            else p_frozen<BC, true, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+          } else {
+            if (mask) p_frozen<BC, false, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            else p_frozen<BC, false, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
           }
-          l = __fadd_rn(l, __fadd_rn(ls0, ls1));
           ++n_frozen;
         }
+        if (!skipped) l = __fadd_rn(l, __fadd_rn(acc.x, acc.y));
         if (r == 0) {
           if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
           if (a.skip_trace) {
@@ -582,8 +658,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (a.stats) {
         if (a.monitor) {
-          atomicAdd(&a.stats[VFA_STAT_OVER_F32], over32);
-          atomicAdd(&a.stats[VFA_STAT_OVER_F16], over16);
+          atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
+          atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
         }
         if (r == 0) {
           atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
@@ -600,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 12) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tbase);
+    tmem_dealloc<C::kTmemCols>(ctl->tmem_base);
   }
 }
 
