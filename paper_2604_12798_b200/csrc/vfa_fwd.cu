@@ -136,6 +136,12 @@ __device__ __forceinline__ bool needs_corr(const TileSchedule& s, int pos, bool*
   return sp && pos > 0;
 }
 
+// tcgen05.commit from one elected lane of the (converged) MMA warp.
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  if (elect_one()) mma_commit(bar);
+  __syncwarp();
+}
+
 // ------------------------------------------------------------------------------------
 // Softmax element math. x = s * (scale*log2 e) - m2 in packed pairs (FFMA2); P = exp2(x)
 // on MUFU.EX2 for most pairs and on the FMA pipe (degree-4 polynomial, |rel err| < 3e-6)
@@ -327,7 +333,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 12) {
     // ============================ MMA issuer ============================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-    if (lane == 0) {
+    {
+      // the whole warp runs the issue loop (warp-uniform state in uniform registers);
+      // one elected lane issues each tcgen05 instruction
       VFA_ROLE_SETUP();
       constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
       constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
@@ -359,17 +367,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
           const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
-          mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
-                 (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
+          if (elect_one())
+            mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
+                   (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
+          __syncwarp();
         }
       };
       auto issue_pv = [&](int t, int st, bool acc) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
-        for (int kk = 0; kk < BC / 16; ++kk)
-          mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + kk * 8,
-                 (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
-                 (acc || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BC / 16; ++kk) {
+          if (elect_one())
+            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + kk * 8,
+                   (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
+                   (acc || kk > 0) ? 1u : 0u);
+          __syncwarp();
+        }
       };
       uint32_t sfree_ph[NQ], p_ph[NQ], ordy_ph[NQ];
       bool o_init[NQ];
@@ -390,9 +403,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           issue_qk(t, s);
-          mma_commit(&ctl->s_full[t]);
+          commit_elect(&ctl->s_full[t]);
         }
-        mma_commit(&ctl->kv_empty[s]);
+        commit_elect(&ctl->kv_empty[s]);
       }
       // first QK
       {
@@ -404,9 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           issue_qk(t, s);
-          mma_commit(&ctl->s_full[t]);
+          commit_elect(&ctl->s_full[t]);
         }
-        mma_commit(&ctl->kv_empty[s]);
+        commit_elect(&ctl->kv_empty[s]);
       }
       for (int pos = 0; pos < N; ++pos) {
         const bool corr = needs_corr(sched, pos);
@@ -427,17 +440,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_pv(t, vs, o_init[t]);
             o_init[t] = true;
           }
-          if (corr_next) mma_commit(&ctl->o_full[t]);
-          if (t == NQ - 1) mma_commit(&ctl->kv_empty[vs]);
+          if (corr_next) commit_elect(&ctl->o_full[t]);
+          if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
           if (pos + 1 < N) {
             if (t == 0) ks = acquire();
             issue_qk(t, ks);
-            mma_commit(&ctl->s_full[t]);
+            commit_elect(&ctl->s_full[t]);
           }
         }
-        if (ks >= 0) mma_commit(&ctl->kv_empty[ks]);
+        if (ks >= 0) commit_elect(&ctl->kv_empty[ks]);
       }
-      for (int t = 0; t < NQ; ++t) mma_commit(&ctl->o_final[t]);
+      for (int t = 0; t < NQ; ++t) commit_elect(&ctl->o_final[t]);
     }
   } else if (warp >= 14) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
