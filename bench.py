@@ -239,27 +239,35 @@ class Runner:
         return {"visited": s[0], "skipped": s[1], "special": s[2], "frozen": s[3]}
 
 
-def time_steps(runner, steps, flush, barrier):
-    """Per-step CUDA-event timing on the launching stream; L2 flushed between steps."""
-    torch = runner.torch
+def time_interleaved(runners, steps, flush, barrier):
+    """Per-step CUDA-event timing on the launching stream, variants interleaved step by step
+    (so every variant sees the same clock / power state); L2 flushed before every step.
+    Returns {name: (total_ms, mean attention-kernel ms, mean step ms, min step ms)}."""
+    import torch
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    ev = {name: [] for name in runners}
     barrier()
     torch.cuda.synchronize()
-    for e0, e1, e2 in ev:
-        flush.zero_()
-        e0.record(stream)
-        runner.krepr(sh)
-        e1.record(stream)
-        runner.attn(sh)
-        e2.record(stream)
+    for _ in range(steps):
+        for name, r in runners.items():
+            e = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
+            flush.zero_()
+            e[0].record(stream)
+            r.krepr(sh)
+            e[1].record(stream)
+            r.attn(sh)
+            e[2].record(stream)
+            ev[name].append(e)
     torch.cuda.synchronize()
     barrier()
-    step_ms = [a.elapsed_time(c) for a, _, c in ev]
-    attn_ms = [b.elapsed_time(c) for _, b, c in ev]
-    return float(np.sum(step_ms)), float(np.mean(attn_ms)), float(np.mean(step_ms)), float(np.min(step_ms))
+    out = {}
+    for name, lst in ev.items():
+        step_ms = [a.elapsed_time(c) for a, _, c in lst]
+        attn_ms = [b.elapsed_time(c) for _, b, c in lst]
+        out[name] = (float(np.sum(step_ms)), float(np.mean(attn_ms)), float(np.mean(step_ms)),
+                     float(np.min(step_ms)))
+    return out
 
 
 def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam):
@@ -311,38 +319,33 @@ def main_ours(args):
 
     cfg = CONFIGS[args.config]
     B, Hq, Hkv, L, d = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["L"], cfg["d"]
-    if Hkv % world:
-        raise SystemExit(f"--gpus {world} must divide Hkv={Hkv}")
-    grp = Hq // Hkv
-    kv_per = Hkv // world
+    from paper_2604_12798_b200.sharding import gather_heads, kv_head_shard, shard_inputs
+    shard = kv_head_shard(rank, world, Hq, Hkv)
     q_full, k_full, v_full = make_inputs(cfg, dev)
-    kv0 = rank * kv_per
-    q = q_full[:, kv0 * grp:(kv0 + kv_per) * grp].contiguous()
-    k = k_full[:, kv0:kv0 + kv_per].contiguous()
-    v = v_full[:, kv0:kv0 + kv_per].contiguous()
+    q, k, v = shard_inputs(q_full, k_full, v_full, shard)
     if world > 1:
         del q_full, k_full, v_full
     flops_total = causal_flops(B, Hq, L, d)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2
 
-    runners = {"vfa": Runner(q, k, v, "vfa"), "fa": Runner(q, k, v, "fa"),
-               "vsa": Runner(q, k, v, "vsa", lam=args.lam)}
+    tile = dict(k_block=args.k_block, n_sink=args.n_sink, n_local=args.n_local)
+    runners = {"vfa": Runner(q, k, v, "vfa", **tile), "fa": Runner(q, k, v, "fa", **tile),
+               "vsa": Runner(q, k, v, "vsa", lam=args.lam, **tile)}
     order = ["vfa"] if args.no_ablation else ["vfa", "fa", "vsa"]
+    runners = {name: runners[name] for name in order}
     res = {}
     clocks = ClockSampler(dev.index)
-    for name in order:
-        r = runners[name]
-        sh = torch.cuda.current_stream().cuda_stream
+    sh = torch.cuda.current_stream().cuda_stream
+    for r in runners.values():
         for _ in range(args.warmup):
             flush.zero_()
             r.krepr(sh)
             r.attn(sh)
-        torch.cuda.synchronize()
-        if name == "vfa":
-            with clocks:
-                total_ms, attn_ms, mean_ms, min_ms = time_steps(r, args.steps, flush, barrier)
-        else:
-            total_ms, attn_ms, mean_ms, min_ms = time_steps(r, args.steps, flush, barrier)
+    torch.cuda.synchronize()
+    with clocks:
+        timed = time_interleaved(runners, args.steps, flush, barrier)
+    for name, r in runners.items():
+        total_ms, attn_ms, mean_ms, min_ms = timed[name]
         t = torch.tensor([total_ms, attn_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -361,17 +364,15 @@ def main_ours(args):
     verified = None
     if world > 1:
         r = runners["vfa"]
-        o_parts = [torch.empty_like(r.o) for _ in range(world)]
-        l_parts = [torch.empty_like(r.lse) for _ in range(world)]
-        dist.all_gather(o_parts, r.o)
-        dist.all_gather(l_parts, r.lse)
+        o_all = gather_heads(r.o, world)  # NCCL all_gather over NVLink, verification only
+        l_all = gather_heads(r.lse, world)
         if rank == 0:
-            full = Runner(q_full, k_full, v_full, "vfa")
+            full = Runner(q_full, k_full, v_full, "vfa", **tile)
             sh = torch.cuda.current_stream().cuda_stream
             full.krepr(sh)
             full.attn(sh)
             torch.cuda.synchronize()
-            verified = bool(torch.equal(torch.cat(o_parts, 1), full.o) and torch.equal(torch.cat(l_parts, 1), full.lse))
+            verified = bool(torch.equal(o_all, full.o) and torch.equal(l_all, full.lse))
             del full
 
     # ---- end-to-end through the public API with host buffers (N GPUs, per-rank shard)
@@ -416,21 +417,22 @@ def main_ours(args):
             "dtype": "bf16",
             "data": "synthetic N(0,1) bf16 Q/K/V (seeded torch generator); no checkpoint needed",
             "config": {"workload": cfg["workload"], "batch": B, "heads_q": Hq, "heads_kv": Hkv,
-                       "seq_len": L, "head_dim": d, "q_block": 128, "k_block": 128, "causal": True,
-                       "variant": "vfa", "key_repr": "sabsmax", "n_sink": 1, "n_local": 1,
+                       "seq_len": L, "head_dim": d, "q_block": 128, "k_block": args.k_block, "causal": True,
+                       "variant": "vfa", "key_repr": "sabsmax", "n_sink": args.n_sink, "n_local": args.n_local,
                        "parallelism": f"kv-head sharding x{world}" if world > 1 else "single GPU",
                        "flops_per_step": flops_total,
-                       "l2": "inputs 384 MiB > 126 MB L2, and L2 flushed (256 MiB write) between timed steps"},
+                       "l2": "inputs 384 MiB > 126 MB L2, and L2 flushed (256 MiB write) between timed steps",
+                       "timing": "variants fa/vfa/vsa interleaved step by step; value = the vfa steps"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(),
-                         "kernel": "vfa_fwd_kernel<128,128,2,VFA> (per rank)",
+                         "kernel": f"vfa_fwd_kernel<{d},{args.k_block},2,VFA> (per rank)",
                          "peak_source": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
                          "frac_of_sustained": round(achieved / peak_sus, 4) if peak_sus else None},
             "ablation": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
                          for k2, v2 in res.items()},
             "clocks": clocks.summary(),
-            "gpu_launches": args.steps * runners["vfa"].launches_per_step,
+            "gpu_launches": args.steps * sum(r.launches_per_step for r in runners.values()),
             "status_flags": int(status[0]),
         }
         if "fa" in res:
@@ -518,6 +520,9 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--lam", type=float, default=1e-2, help="VSA lambda for the ablation line")
+    ap.add_argument("--k-block", type=int, default=128, choices=(64, 128))
+    ap.add_argument("--n-sink", type=int, default=1)
+    ap.add_argument("--n-local", type=int, default=1)
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

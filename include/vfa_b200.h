@@ -127,6 +127,11 @@ int vfa_status_code(const unsigned int* status_host);
 /* Message for the last non-zero return on this thread. */
 const char* vfa_last_error(void);
 
+/* Debug only: when non-NULL, subsequent vfa_fwd calls record clock64() timestamps of the
+ * first CTA into device_buffer (long long[Lk/k_block * 8]: per visited block, softmax tile
+ * 0/1 "S ready"/"P done", MMA tile 0/1 "P observed"/"next QK issued"). NULL disables. */
+int vfa_debug_trace(long long* device_buffer);
+
 /* Library version string. */
 const char* vfa_version(void);
 

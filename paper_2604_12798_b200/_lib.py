@@ -33,7 +33,7 @@ STATUS_COUNT = 4
 
 # every symbol include/vfa_b200.h declares
 EXPORTS = ("vfa_check_params", "vfa_workspace_bytes", "vfa_fwd", "vfa_krepr", "vfa_schedule",
-           "vfa_status_code", "vfa_last_error", "vfa_version")
+           "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace")
 
 
 class VfaParams(ctypes.Structure):
@@ -89,6 +89,8 @@ def load():
         lib.vfa_status_code.restype = ctypes.c_int
         lib.vfa_last_error.argtypes = []
         lib.vfa_last_error.restype = ctypes.c_char_p
+        lib.vfa_debug_trace.argtypes = [vp]
+        lib.vfa_debug_trace.restype = ctypes.c_int
         lib.vfa_version.argtypes = []
         lib.vfa_version.restype = ctypes.c_char_p
         _lib = lib

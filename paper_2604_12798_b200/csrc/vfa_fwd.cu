@@ -59,7 +59,15 @@ struct FwdArgs {
   unsigned long long* stats;
   unsigned int* status;
   unsigned char* skip_trace;
+  long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
+
+// debug timeline slots per visited block (CTA 0 only): softmax t: S ready, P done;
+// MMA t: P observed, next QK issued
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ void trace_event(const FwdArgs& a, int pos, int slot) {
+  if (a.trace != nullptr && blockIdx.x == 0) a.trace[pos * kTraceSlots + slot] = clock64();
+}
 
 template <int D, int BC, int NQ>
 struct Cfg {
@@ -71,27 +79,35 @@ struct Cfg {
   static constexpr int kStagesRaw = kAvail / kKVBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = 1024 + NQ * kQBytes + kStages * kKVBytes + kCtlBytes;
-  static __host__ __device__ constexpr uint32_t s_off(int t) { return static_cast<uint32_t>(t) * 128u; }
-  static constexpr int kOBase = NQ == 2 ? 256 : 128;
-  static constexpr uint32_t kTmemCols = NQ == 2 ? 512 : 256;
-  static_assert(kStages >= 2, "not enough shared memory for a K/V ring");
+  // S buffers per query tile: 2 (S of the next block computed while the softmax works on
+  // this one) whenever NQ*2*BC + NQ*D TMEM columns fit in 512, else 1.
+  static constexpr int kSB = (NQ * 2 * BC + NQ * D <= 512) ? 2 : 1;
+  static constexpr int kSCols = kSB == 2 ? BC : 128;
+  static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
+    return static_cast<uint32_t>((t * kSB + b) * kSCols);
+  }
+  static constexpr int kOBase = NQ * kSB * kSCols;
+  static constexpr int kColsUsed = kOBase + NQ * D;
+  static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
+  static_assert(kColsUsed <= 512, "TMEM over-subscribed");
+  static_assert(kStages >= 3, "not enough shared memory for a K/V ring");
 };
 
-template <int NS, int NQ>
+template <int NS, int NQ, int SB>
 struct __align__(16) Ctl {
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
-  uint64_t s_full[NQ];
-  uint64_t s_free[NQ];
-  uint64_t p_full[NQ];
-  uint64_t o_full[NQ];
-  uint64_t o_ready[NQ];
-  uint64_t o_final[NQ];
-  uint64_t sc_full[NQ];
+  uint64_t s_full[NQ][SB];   // MMA -> softmax: S of sequence element g ready (buffer g % SB)
+  uint64_t s_free[NQ][SB];   // softmax -> MMA: m-init chunk read, buffer reusable
+  uint64_t p_full[NQ][SB];   // softmax -> MMA: P (bf16, aliased over S) ready / skip decided
+  uint64_t sc_full[NQ][SB];  // softmax -> correction: per-row rescale factor published
+  uint64_t o_full[NQ];       // MMA -> correction: every PV before this block has completed
+  uint64_t o_ready[NQ];      // correction -> MMA: O rescaled in TMEM
+  uint64_t o_final[NQ];      // MMA -> epilogue: last PV completed
   uint32_t tmem_base;
-  uint32_t skip[NQ];
-  float fbuf[NQ][kBR];
+  uint32_t skip[NQ][SB];
+  float fbuf[NQ][SB][kBR];
 };
 
 struct Unit {
@@ -244,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const FwdArgs a) {
   using C = Cfg<D, BC, NQ>;
   constexpr int NS = C::kStages;
-  using CtlT = Ctl<NS, NQ>;
+  constexpr int SB = C::kSB;
+  using CtlT = Ctl<NS, NQ, SB>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
 
   extern __shared__ uint8_t smem_raw[];
@@ -260,13 +277,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&ctl->q_full[t], 1);
-      mbar_init(&ctl->s_full[t], 1);
-      mbar_init(&ctl->s_free[t], 4);
-      mbar_init(&ctl->p_full[t], 4);
+      for (int b = 0; b < SB; ++b) {
+        mbar_init(&ctl->s_full[t][b], 1);
+        mbar_init(&ctl->s_free[t][b], 4);
+        mbar_init(&ctl->p_full[t][b], 4);
+        mbar_init(&ctl->sc_full[t][b], kBR);
+      }
       mbar_init(&ctl->o_full[t], 1);
       mbar_init(&ctl->o_ready[t], 4);
       mbar_init(&ctl->o_final[t], 1);
-      mbar_init(&ctl->sc_full[t], kBR);
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&ctl->kv_full[s], 1);
@@ -286,6 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   // Each role re-derives its work description after its setmaxnreg so that nothing
   // computed before the role split has to stay live (or spill) across it.
+  // Sequence g = 0 .. G-1: nchunks m-init chunks (S = Q . Krepr^T), then the N visited
+  // key blocks in schedule order (S = Q . K^T); element g uses S buffer g % SB.
 #define VFA_ROLE_SETUP()                                                       \
   const uint32_t tbase = ctl->tmem_base;                                       \
   const Unit unit = decode_unit(a, blockIdx.x);                                \
@@ -293,7 +314,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int N = sched.vmax;                                                    \
   int nrep = 0;                                                                \
   const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);                 \
-  (void)tbase; (void)nrep; (void)nchunks; (void)N
+  const int G = nchunks + N;                                                   \
+  (void)tbase; (void)nrep; (void)nchunks; (void)N; (void)G
 
   if (warp == 13) {
     // ============================ TMA producer ============================
@@ -323,11 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       };
-      for (int ch = 0; ch < nchunks; ++ch) load_tile(&tmR, ch * BC);
-      for (int pos = 0; pos < N; ++pos) {
-        const int j = sched_block(sched, pos);
-        load_tile(&tmK, (j - 1) * BC);
-        load_tile(&tmV, (j - 1) * BC);
+      // S-operand of sequence element g: a Krepr chunk or a K block
+      auto load_s_operand = [&](int g) {
+        if (g < nchunks)
+          load_tile(&tmR, g * BC);
+        else
+          load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
+      };
+      // same order as the MMA warp consumes: op(0..SB-1), then per g: [V(g)], op(g+SB)
+      for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
+      for (int g = 0; g < G; ++g) {
+        if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+        if (g + SB < G) load_s_operand(g + SB);
       }
     }
   } else if (warp == 12) {
@@ -342,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // UMMA smem descriptors: hi word constant (SBO = 1024 B, version 1, SWIZZLE_128B),
       // lo word = (address >> 4) | LBO << 16. Addresses < 256 KiB so the start field never carries.
       constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
-      constexpr uint32_t kLboK = 1u << 16;                       // K-major: LBO unused
+      constexpr uint32_t kLboK = 1u << 16;                                      // K-major: LBO unused
       constexpr uint32_t kLboV = static_cast<uint32_t>((BC * 128) >> 4) << 16;  // V: next 64-col chunk
       const uint32_t q_lo = smem_u32(sQ) >> 4;
       const uint32_t kv_lo = smem_u32(sKV) >> 4;
@@ -360,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return st;
       };
-      auto issue_qk = [&](int t, int st) {
+      auto issue_qk = [&](int t, int b, int st) {
         const uint32_t a_lo = q_lo + t * (C::kQBytes >> 4) + kLboK;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
 #pragma unroll
@@ -368,84 +397,79 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
           const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
           if (elect_one())
-            mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
+            mma_ss(tbase + C::s_off(t, b), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
                    (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
           __syncwarp();
         }
       };
-      auto issue_pv = [&](int t, int st, bool acc) {
+      auto issue_pv = [&](int t, int b, int st, bool acc) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
         for (int kk = 0; kk < BC / 16; ++kk) {
           if (elect_one())
-            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + kk * 8,
+            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + kk * 8,
                    (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
                    (acc || kk > 0) ? 1u : 0u);
           __syncwarp();
         }
       };
-      uint32_t sfree_ph[NQ], p_ph[NQ], ordy_ph[NQ];
-      bool o_init[NQ];
-#pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        sfree_ph[t] = 0;
-        p_ph[t] = 0;
-        ordy_ph[t] = 0;
-        o_init[t] = false;
-      }
-      // m-init prologue: S_t = Q_t . Krepr_chunk^T
-      for (int ch = 0; ch < nchunks; ++ch) {
-        const int s = acquire();
-        for (int t = 0; t < NQ; ++t) {
-          if (ch > 0) {
-            mbar_wait(&ctl->s_free[t], sfree_ph[t]);
-            sfree_ph[t] ^= 1;
-            tc_fence_after();
-          }
-          issue_qk(t, s);
-          commit_elect(&ctl->s_full[t]);
+      // S = Q_t . op^T for sequence element g into buffer g % SB (op = Krepr chunk or K block)
+      uint32_t sfree_ph = 0;  // bit (t * SB + b)
+      auto issue_s_tile = [&](int g, int t, int st) {
+        const int b = g % SB;
+        // the buffer's previous occupant g - SB: an m-init chunk must have been read
+        // (s_free); a visited block's P was consumed by its PV, issued before this QK
+        if (g >= SB && g - SB < nchunks) {
+          const int bit = t * SB + b;
+          mbar_wait(&ctl->s_free[t][b], (sfree_ph >> bit) & 1u);
+          sfree_ph ^= 1u << bit;
+          tc_fence_after();
         }
-        commit_elect(&ctl->kv_empty[s]);
+        issue_qk(t, b, st);
+        commit_elect(&ctl->s_full[t][b]);
+      };
+      uint32_t p_ph = 0, ordy_ph = 0;
+      uint32_t o_init = 0;  // bit t: O_t holds an accumulation
+      for (int g = 0; g < SB && g < G; ++g) {
+        const int st = acquire();
+        for (int t = 0; t < NQ; ++t) issue_s_tile(g, t, st);
+        commit_elect(&ctl->kv_empty[st]);
       }
-      // first QK
-      {
-        const int s = acquire();
-        for (int t = 0; t < NQ; ++t) {
-          if (nchunks > 0) {
-            mbar_wait(&ctl->s_free[t], sfree_ph[t]);
-            sfree_ph[t] ^= 1;
-            tc_fence_after();
-          }
-          issue_qk(t, s);
-          commit_elect(&ctl->s_full[t]);
-        }
-        commit_elect(&ctl->kv_empty[s]);
-      }
-      for (int pos = 0; pos < N; ++pos) {
-        const bool corr = needs_corr(sched, pos);
-        const bool corr_next = (pos + 1 < N) && needs_corr(sched, pos + 1);
-        const int vs = acquire();
+      // Per element g and query tile t: PV_t(g) then QK_t(g + SB), so each query tile's next
+      // S is issued as soon as its own P is consumed (the two tiles ping-pong on the tensor pipe).
+      for (int g = 0; g < G; ++g) {
+        const bool main_blk = g >= nchunks;
+        const int pos = g - nchunks;
+        const int b = g % SB;
+        const bool corr = main_blk && needs_corr(sched, pos);
+        const bool corr_next = main_blk && (pos + 1 < N) && needs_corr(sched, pos + 1);
+        const bool next_s = g + SB < G;
+        const int vs = main_blk ? acquire() : -1;
         int ks = -1;
         for (int t = 0; t < NQ; ++t) {
-          mbar_wait(&ctl->p_full[t], p_ph[t]);
-          p_ph[t] ^= 1;
-          tc_fence_after();
-          const bool skip = (MODE == kVSA) && (ctl->skip[t] != 0);
-          if (corr) {
-            mbar_wait(&ctl->o_ready[t], ordy_ph[t]);
-            ordy_ph[t] ^= 1;
+          if (main_blk) {
+            const int bit = t * SB + b;
+            mbar_wait(&ctl->p_full[t][b], (p_ph >> bit) & 1u);
+            p_ph ^= 1u << bit;
             tc_fence_after();
+            if (lane == 0) trace_event(a, pos, 4 + 2 * t);
+            const bool skip = (MODE == kVSA) && (ctl->skip[t][b] != 0);
+            if (corr) {
+              mbar_wait(&ctl->o_ready[t], (ordy_ph >> t) & 1u);
+              ordy_ph ^= 1u << t;
+              tc_fence_after();
+            }
+            if (!skip) {
+              issue_pv(t, b, vs, (o_init >> t) & 1u);
+              o_init |= 1u << t;
+            }
+            if (corr_next) commit_elect(&ctl->o_full[t]);
+            if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
           }
-          if (!skip) {
-            issue_pv(t, vs, o_init[t]);
-            o_init[t] = true;
-          }
-          if (corr_next) commit_elect(&ctl->o_full[t]);
-          if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
-          if (pos + 1 < N) {
+          if (next_s) {
             if (t == 0) ks = acquire();
-            issue_qk(t, ks);
-            commit_elect(&ctl->s_full[t]);
+            issue_s_tile(g + SB, t, ks);
+            if (main_blk && lane == 0) trace_event(a, pos, 5 + 2 * t);
           }
         }
         if (ks >= 0) commit_elect(&ctl->kv_empty[ks]);
@@ -460,17 +484,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     VFA_ROLE_SETUP();
     const int r = tid - 256;
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint32_t sc_ph[NQ], of_ph[NQ];
-#pragma unroll
-    for (int t = 0; t < NQ; ++t) sc_ph[t] = of_ph[t] = 0;
+    uint32_t sc_ph = 0, of_ph = 0;
     for (int pos = 1; pos < N; ++pos) {
       if (!needs_corr(sched, pos)) continue;
+      const int b = (nchunks + pos) % SB;
       for (int t = 0; t < NQ; ++t) {
-        mbar_wait(&ctl->sc_full[t], sc_ph[t]);
-        sc_ph[t] ^= 1;
-        const float f = ctl->fbuf[t][r];
-        mbar_wait(&ctl->o_full[t], of_ph[t]);
-        of_ph[t] ^= 1;
+        const int bit = t * SB + b;
+        mbar_wait(&ctl->sc_full[t][b], (sc_ph >> bit) & 1u);
+        sc_ph ^= 1u << bit;
+        const float f = ctl->fbuf[t][b][r];
+        mbar_wait(&ctl->o_full[t], (of_ph >> t) & 1u);
+        of_ph ^= 1u << t;
         tc_fence_after();
         const bool work = (MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f);
         if (work) {
@@ -508,12 +532,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int h = unit.h0 + t;
       const int R = unit.qt * kBR + r;  // absolute query row
       const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t tS = tbase + C::s_off(t) + lane_off;
       const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
       const float cs = a.c_scale;
       float m2 = -INFINITY;  // running max, log2 units of scaled scores
       float l = 0.f;
-      uint32_t s_ph = 0;
+      uint32_t s_ph = 0;  // bit b: phase of s_full[t][b]
       int n_special = 0, n_frozen = 0, n_skipped = 0;
       uint32_t over32 = 0, over16 = 0;
 
@@ -521,8 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (nchunks > 0) {
         float mx = -INFINITY;
         for (int ch = 0; ch < nchunks; ++ch) {
-          mbar_wait(&ctl->s_full[t], s_ph);
-          s_ph ^= 1;
+          const int b = ch % SB;
+          const uint32_t tS = tbase + C::s_off(t, b) + lane_off;
+          mbar_wait(&ctl->s_full[t][b], (s_ph >> b) & 1u);
+          s_ph ^= 1u << b;
           tc_fence_after();
           const int valid = nrep - ch * BC;
 #pragma unroll
@@ -537,21 +562,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->s_free[t]);
+          if (lane == 0) mbar_arrive(&ctl->s_free[t][b]);
         }
         m2 = mx * cs;
       }
 
       const float2 cs2 = make_float2(cs, cs);
       for (int pos = 0; pos < N; ++pos) {
+        const int b = (nchunks + pos) % SB;
+        const uint32_t tS = tbase + C::s_off(t, b) + lane_off;
         const int j = sched_block(sched, pos);
         const bool special = (MODE == kFA) || sched_is_special(sched, j);
         const bool corr = special && pos > 0;
         const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
         const int lim = R - (j - 1) * BC;  // columns > lim are causally masked
-        mbar_wait(&ctl->s_full[t], s_ph);
-        s_ph ^= 1;
+        mbar_wait(&ctl->s_full[t][b], (s_ph >> b) & 1u);
+        s_ph ^= 1u << b;
         tc_fence_after();
+        if (r == 0) trace_event(a, pos, 2 * t);
         bool skipped = false;
         float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this tile's P (pairs)
         if (MODE == kFA || MODE == kVSA || special) {
@@ -580,8 +608,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (skipped) {
             ++n_skipped;
             if (corr) {
-              ctl->fbuf[t][r] = 1.0f;
-              mbar_arrive(&ctl->sc_full[t]);
+              ctl->fbuf[t][b][r] = 1.0f;
+              mbar_arrive(&ctl->sc_full[t][b]);
             }
           } else {
             if (special) {
@@ -589,8 +617,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               m2 = m2n;
               l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
               if (corr) {
-                ctl->fbuf[t][r] = f;
-                mbar_arrive(&ctl->sc_full[t]);
+                ctl->fbuf[t][b][r] = f;
+                mbar_arrive(&ctl->sc_full[t][b]);
               }
               ++n_special;
             } else {
@@ -617,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!skipped) l = __fadd_rn(l, __fadd_rn(acc.x, acc.y));
         if (r == 0) {
-          if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
+          if (MODE == kVSA) ctl->skip[t][b] = skipped ? 1u : 0u;
           if (a.skip_trace) {
             const size_t idx = ((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos;
             a.skip_trace[idx] = skipped ? 2 : 1;
@@ -626,7 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctl->p_full[t]);
+        if (r == 0) trace_event(a, pos, 2 * t + 1);
+        if (lane == 0) mbar_arrive(&ctl->p_full[t][b]);
       }
 
       // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l
@@ -764,6 +793,7 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
 namespace {
 
 thread_local std::string g_last_error;
+long long* g_debug_trace = nullptr;  // debug only: set by vfa_debug_trace()
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -988,6 +1018,7 @@ int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, voi
   a.stats = reinterpret_cast<unsigned long long*>(stats);
   a.status = status;
   a.skip_trace = skip_trace;
+  a.trace = g_debug_trace;
 
   if (D == 128 && BC == 128) return dispatch_nq<128, 128>(p, nq, mq, mk, mv, mr, a, st);
   if (D == 128 && BC == 64) return dispatch_nq<128, 64>(p, nq, mq, mk, mv, mr, a, st);
@@ -1021,6 +1052,11 @@ int vfa_status_code(const unsigned int* status_host) {
 }
 
 const char* vfa_last_error(void) { return g_last_error.c_str(); }
+
+int vfa_debug_trace(long long* device_buffer) {
+  g_debug_trace = device_buffer;
+  return VFA_OK;
+}
 
 const char* vfa_version(void) { return "vfa_b200 0.1.0 (sm_100a, tcgen05/TMEM/TMA)"; }
 

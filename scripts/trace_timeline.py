@@ -1,0 +1,56 @@
+"""Per-visit timeline of CTA 0 (the longest causal unit) from the debug trace.
+
+    python scripts/trace_timeline.py [--variant vfa|fa|vsa] [--k-block 128]
+Prints, per query tile, the softmax busy time per block (S ready -> P done), the gap the
+softmax waits for the next S, the MMA's latency to observe P, and the per-block period.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import CONFIGS, Runner, make_inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--variant", default="vfa")
+ap.add_argument("--k-block", type=int, default=128)
+ap.add_argument("--n-local", type=int, default=1)
+a = ap.parse_args()
+cfg = CONFIGS["c2"]
+dev = torch.device("cuda", 0)
+q, k, v = make_inputs(cfg, dev)
+r = Runner(q, k, v, a.variant, lam=1e-2 if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
+T = cfg["L"] // a.k_block
+buf = torch.zeros(T * 8, dtype=torch.int64, device=dev)
+sh = torch.cuda.current_stream().cuda_stream
+r.krepr(sh)
+r.attn(sh)  # warm-up
+r.lib.vfa_debug_trace(buf.data_ptr())
+r.krepr(sh)
+r.attn(sh)
+torch.cuda.synchronize()
+r.lib.vfa_debug_trace(None)
+tr = buf.cpu().numpy().reshape(T, 8).astype(np.float64)
+n = int((tr[:, 1] > 0).sum())
+tr = tr[:n]
+t0 = tr[tr > 0].min()
+tr = np.where(tr > 0, tr - t0, np.nan)
+print(f"variant={a.variant} k_block={a.k_block} visited={n} total={np.nanmax(tr):.0f} cycles "
+      f"-> {np.nanmax(tr) / n:.0f} cycles per block (both query tiles)")
+for t in (0, 1):
+    s_ready, p_done, p_seen, qk_iss = tr[:, 2 * t], tr[:, 2 * t + 1], tr[:, 4 + 2 * t], tr[:, 5 + 2 * t]
+    busy = p_done - s_ready
+    wait_s = s_ready[1:] - p_done[:-1]
+    seen = p_seen - p_done
+    qk_to_s = s_ready[1:] - qk_iss[:-1]
+    sl = slice(4, n - 4)
+    print(f" tile {t}: softmax busy median {np.nanmedian(busy[sl]):.0f} (p10 {np.nanpercentile(busy[sl], 10):.0f}"
+          f" p90 {np.nanpercentile(busy[sl], 90):.0f}); softmax waits for S {np.nanmedian(wait_s[sl]):.0f};"
+          f" MMA sees P after {np.nanmedian(seen[sl]):.0f}; S ready {np.nanmedian(qk_to_s[sl]):.0f} after QK issue;"
+          f" period {np.nanmedian(np.diff(s_ready)[sl]):.0f}")
+print("first 6 blocks (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK]")
+for i in range(min(6, n)):
+    print(" ", np.round(tr[i]).astype(int).tolist())
