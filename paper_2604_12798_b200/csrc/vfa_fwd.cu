@@ -41,7 +41,20 @@
 namespace vfa {
 
 constexpr int kBR = 128;          // query rows per tile (tcgen05 M)
-constexpr int kThreads = 512;
+// warps 0-15: four softmax warpgroups (2 query tiles x 2 column halves); warp 16: MMA
+// issuer (both query tiles, strictly alternating) + TMEM allocator; warp 17: TMA producer;
+// warps 18-19 complete the last warpgroup. (One issuer per tile was measured slower: the
+// tiles drift into phase and contend for the softmax issue slots.)
+constexpr int kSoftmaxWarps = 16;
+constexpr int kMmaWarp = 16;
+constexpr int kLoadWarp = 17;
+constexpr int kThreads = 640;
+// setmaxnreg budgets. The CTA's register pool is what the launch allocated
+// (threads x compiled registers/thread, 640 x 96 = 61440); asking for more than the pool
+// blocks setmaxnreg.inc forever, so the host checks this budget before launching.
+constexpr int kRegsSoftmax = 104;
+constexpr int kRegsOther = 56;
+constexpr int kRegBudget = kSoftmaxWarps * 32 * kRegsSoftmax + (kThreads - kSoftmaxWarps * 32) * kRegsOther;
 constexpr int kMaxSmem = 227 * 1024;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -74,40 +87,37 @@ struct Cfg {
   static constexpr int kQBytes = kBR * D * 2;
   static constexpr int kKVBytes = BC * D * 2;
   static constexpr int kDCh = D / 64;  // 64-column (128-byte) swizzle chunks
-  static constexpr int kCtlBytes = 4096;
+  static constexpr int kHC = BC / 2;   // S columns per softmax half (column split of each row)
+  static constexpr int kHD = D / 2;    // O columns rescaled / stored by each half
+  static constexpr int kCtlBytes = 12288;
   static constexpr int kAvail = kMaxSmem - 1024 - kCtlBytes - NQ * kQBytes;
   static constexpr int kStagesRaw = kAvail / kKVBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = 1024 + NQ * kQBytes + kStages * kKVBytes + kCtlBytes;
-  // S buffers per query tile: 2 (S of the next block computed while the softmax works on
-  // this one) whenever NQ*2*BC + NQ*D TMEM columns fit in 512, else 1.
-  static constexpr int kSB = (NQ * 2 * BC + NQ * D <= 512) ? 2 : 1;
-  static constexpr int kSCols = kSB == 2 ? BC : 128;
-  static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
-    return static_cast<uint32_t>((t * kSB + b) * kSCols);
-  }
-  static constexpr int kOBase = NQ * kSB * kSCols;
+  // TMEM: S_t (BC fp32 columns; P_t aliased as packed bf16 inside each half's region), O_t.
+  static __host__ __device__ constexpr uint32_t s_off(int t) { return static_cast<uint32_t>(t * 128); }
+  static constexpr int kOBase = NQ * 128;
   static constexpr int kColsUsed = kOBase + NQ * D;
-  static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
+  static constexpr uint32_t kTmemCols = kColsUsed <= 256 ? 256 : 512;
   static_assert(kColsUsed <= 512, "TMEM over-subscribed");
   static_assert(kStages >= 3, "not enough shared memory for a K/V ring");
+  static_assert(kHC % 32 == 0, "half row must be whole 32-column chunks");
 };
 
-template <int NS, int NQ, int SB>
+template <int NS, int NQ>
 struct __align__(16) Ctl {
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
-  uint64_t s_full[NQ][SB];   // MMA -> softmax: S of sequence element g ready (buffer g % SB)
-  uint64_t s_free[NQ][SB];   // softmax -> MMA: m-init chunk read, buffer reusable
-  uint64_t p_full[NQ][SB];   // softmax -> MMA: P (bf16, aliased over S) ready / skip decided
-  uint64_t sc_full[NQ][SB];  // softmax -> correction: per-row rescale factor published
-  uint64_t o_full[NQ];       // MMA -> correction: every PV before this block has completed
-  uint64_t o_ready[NQ];      // correction -> MMA: O rescaled in TMEM
-  uint64_t o_final[NQ];      // MMA -> epilogue: last PV completed
+  uint64_t s_full[NQ];  // MMA -> softmax halves: S of sequence element g ready
+  uint64_t s_free[NQ];  // softmax halves -> MMA: m-init chunk read (8 warps)
+  uint64_t p_full[NQ];  // softmax halves -> MMA: P ready / skip decided (8 warps)
+  uint64_t o_final[NQ];  // MMA -> epilogue: last PV completed
   uint32_t tmem_base;
-  uint32_t skip[NQ][SB];
-  float fbuf[NQ][SB][kBR];
+  uint32_t skip[NQ];
+  float xmax[NQ][2][2][kBR];  // [tile][parity][half][row]: half-row maxima exchange
+  float xl[NQ][2][kBR];       // [tile][half][row]: final half-row sums
+  uint32_t xfin[NQ][2][kBR];  // [tile][half][row]: output finite flags
 };
 
 struct Unit {
@@ -145,12 +155,6 @@ __device__ __forceinline__ int minit_chunks(const FwdArgs& a, const TileSchedule
   return (n + BC - 1) / BC;
 }
 
-__device__ __forceinline__ bool needs_corr(const TileSchedule& s, int pos, bool* special_out = nullptr) {
-  int j = sched_block(s, pos);
-  bool sp = sched_is_special(s, j);
-  if (special_out) *special_out = sp;
-  return sp && pos > 0;
-}
 
 // tcgen05.commit from one elected lane of the (converged) MMA warp.
 __device__ __forceinline__ void commit_elect(uint64_t* bar) {
@@ -260,8 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const FwdArgs a) {
   using C = Cfg<D, BC, NQ>;
   constexpr int NS = C::kStages;
-  constexpr int SB = C::kSB;
-  using CtlT = Ctl<NS, NQ, SB>;
+  constexpr int HC = C::kHC;
+  constexpr int HD = C::kHD;
+  using CtlT = Ctl<NS, NQ>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
 
   extern __shared__ uint8_t smem_raw[];
@@ -277,14 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&ctl->q_full[t], 1);
-      for (int b = 0; b < SB; ++b) {
-        mbar_init(&ctl->s_full[t][b], 1);
-        mbar_init(&ctl->s_free[t][b], 4);
-        mbar_init(&ctl->p_full[t][b], 4);
-        mbar_init(&ctl->sc_full[t][b], kBR);
-      }
-      mbar_init(&ctl->o_full[t], 1);
-      mbar_init(&ctl->o_ready[t], 4);
+      mbar_init(&ctl->s_full[t], 1);
+      mbar_init(&ctl->s_free[t], 8);
+      mbar_init(&ctl->p_full[t], 8);
       mbar_init(&ctl->o_final[t], 1);
     }
     for (int s = 0; s < NS; ++s) {
@@ -293,20 +293,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 13 && lane == 0) {
+  if (warp == kLoadWarp && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmR);
   }
-  if (warp == 12) tmem_alloc<C::kTmemCols>(&ctl->tmem_base);
+  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(&ctl->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   // Each role re-derives its work description after its setmaxnreg so that nothing
   // computed before the role split has to stay live (or spill) across it.
   // Sequence g = 0 .. G-1: nchunks m-init chunks (S = Q . Krepr^T), then the N visited
-  // key blocks in schedule order (S = Q . K^T); element g uses S buffer g % SB.
+  // key blocks in schedule order (S = Q . K^T).
 #define VFA_ROLE_SETUP()                                                       \
   const uint32_t tbase = ctl->tmem_base;                                       \
   const Unit unit = decode_unit(a, blockIdx.x);                                \
@@ -317,54 +317,54 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G = nchunks + N;                                                   \
   (void)tbase; (void)nrep; (void)nchunks; (void)N; (void)G
 
-  if (warp == 13) {
-    // ============================ TMA producer ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-    if (lane == 0) {
-      VFA_ROLE_SETUP();
-      const uint64_t pol_q = policy_evict_first();
-      const uint64_t pol_kv = policy_evict_last();
-      for (int t = 0; t < NQ; ++t) {
-        mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
+  if (warp >= kSoftmaxWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
+    if (warp == kLoadWarp) {
+      // ============================ TMA producer ============================
+      if (lane == 0) {
+        VFA_ROLE_SETUP();
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        for (int t = 0; t < NQ; ++t) {
+          mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
 #pragma unroll
-        for (int c = 0; c < C::kDCh; ++c)
-          tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
-                      unit.h0 + t, unit.b, pol_q);
-      }
-      int stage = 0;
-      uint32_t phase = 0;
-      auto load_tile = [&](const CUtensorMap* map, int row) {
-        mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
-        uint8_t* dst = sKV + stage * C::kKVBytes;
-#pragma unroll
-        for (int c = 0; c < C::kDCh; ++c)
-          tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
-        if (++stage == NS) {
-          stage = 0;
-          phase ^= 1;
+          for (int c = 0; c < C::kDCh; ++c)
+            tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+                        unit.h0 + t, unit.b, pol_q);
         }
-      };
-      // S-operand of sequence element g: a Krepr chunk or a K block
-      auto load_s_operand = [&](int g) {
-        if (g < nchunks)
-          load_tile(&tmR, g * BC);
-        else
-          load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
-      };
-      // same order as the MMA warp consumes: op(0..SB-1), then per g: [V(g)], op(g+SB)
-      for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
-      for (int g = 0; g < G; ++g) {
-        if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
-        if (g + SB < G) load_s_operand(g + SB);
+        int stage = 0;
+        uint32_t phase = 0;
+        auto load_tile = [&](const CUtensorMap* map, int row) {
+          mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
+          uint8_t* dst = sKV + stage * C::kKVBytes;
+#pragma unroll
+          for (int c = 0; c < C::kDCh; ++c)
+            tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+        };
+        // the MMA warp's consumption order: op(0); per g: [V(g)], op(g+1)
+        auto load_s_operand = [&](int g) {
+          if (g < nchunks)
+            load_tile(&tmR, g * BC);
+          else
+            load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
+        };
+        load_s_operand(0);
+        for (int g = 0; g < G; ++g) {
+          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+          if (g + 1 < G) load_s_operand(g + 1);
+        }
       }
-    }
-  } else if (warp == 12) {
-    // ============================ MMA issuer ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-    {
-      // the whole warp runs the issue loop (warp-uniform state in uniform registers);
-      // one elected lane issues each tcgen05 instruction
+    } else if (warp == kMmaWarp) {
+      // ============================ MMA issuer ============================
+      // The whole warp runs the issue loop (warp-uniform state in uniform registers); one
+      // elected lane issues each tcgen05 instruction. Per element g and query tile t:
+      // PV_t(g) then QK_t(g+1), so each tile's next S is issued as soon as its own P is
+      // consumed and the two query tiles ping-pong (anti-phase) on the tensor pipe.
       VFA_ROLE_SETUP();
       constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
       constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return st;
       };
-      auto issue_qk = [&](int t, int b, int st) {
+      auto issue_qk = [&](int t, int st) {
         const uint32_t a_lo = q_lo + t * (C::kQBytes >> 4) + kLboK;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
 #pragma unroll
@@ -397,78 +397,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
           const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
           if (elect_one())
-            mma_ss(tbase + C::s_off(t, b), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
+            mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
                    (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
           __syncwarp();
         }
       };
-      auto issue_pv = [&](int t, int b, int st, bool acc) {
+      // P of half h occupies TMEM columns [h*HC, h*HC + HC/2) of S_t (packed bf16 pairs)
+      auto issue_pv = [&](int t, int st, bool acc) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
         for (int kk = 0; kk < BC / 16; ++kk) {
+          const uint32_t pcol = (kk * 16 / HC) * HC + (kk * 16 % HC) / 2;
           if (elect_one())
-            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + kk * 8,
+            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + pcol,
                    (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
                    (acc || kk > 0) ? 1u : 0u);
           __syncwarp();
         }
       };
-      // S = Q_t . op^T for sequence element g into buffer g % SB (op = Krepr chunk or K block)
-      uint32_t sfree_ph = 0;  // bit (t * SB + b)
+      uint32_t sfree_ph = 0, p_ph = 0, o_init = 0;
       auto issue_s_tile = [&](int g, int t, int st) {
-        const int b = g % SB;
-        // the buffer's previous occupant g - SB: an m-init chunk must have been read
-        // (s_free); a visited block's P was consumed by its PV, issued before this QK
-        if (g >= SB && g - SB < nchunks) {
-          const int bit = t * SB + b;
-          mbar_wait(&ctl->s_free[t][b], (sfree_ph >> bit) & 1u);
-          sfree_ph ^= 1u << bit;
+        // S_t's previous occupant g - 1: an m-init chunk must have been read (s_free);
+        // a visited block's P was consumed by its PV, issued before this QK
+        if (g >= 1 && g - 1 < nchunks) {
+          mbar_wait(&ctl->s_free[t], (sfree_ph >> t) & 1u);
+          sfree_ph ^= 1u << t;
           tc_fence_after();
         }
-        issue_qk(t, b, st);
-        commit_elect(&ctl->s_full[t][b]);
+        issue_qk(t, st);
+        commit_elect(&ctl->s_full[t]);
       };
-      uint32_t p_ph = 0, ordy_ph = 0;
-      uint32_t o_init = 0;  // bit t: O_t holds an accumulation
-      for (int g = 0; g < SB && g < G; ++g) {
+      {
         const int st = acquire();
-        for (int t = 0; t < NQ; ++t) issue_s_tile(g, t, st);
+        for (int t = 0; t < NQ; ++t) issue_s_tile(0, t, st);
         commit_elect(&ctl->kv_empty[st]);
       }
-      // Per element g and query tile t: PV_t(g) then QK_t(g + SB), so each query tile's next
-      // S is issued as soon as its own P is consumed (the two tiles ping-pong on the tensor pipe).
       for (int g = 0; g < G; ++g) {
         const bool main_blk = g >= nchunks;
         const int pos = g - nchunks;
-        const int b = g % SB;
-        const bool corr = main_blk && needs_corr(sched, pos);
-        const bool corr_next = main_blk && (pos + 1 < N) && needs_corr(sched, pos + 1);
-        const bool next_s = g + SB < G;
+        const bool next_s = g + 1 < G;
         const int vs = main_blk ? acquire() : -1;
         int ks = -1;
         for (int t = 0; t < NQ; ++t) {
           if (main_blk) {
-            const int bit = t * SB + b;
-            mbar_wait(&ctl->p_full[t][b], (p_ph >> bit) & 1u);
-            p_ph ^= 1u << bit;
+            mbar_wait(&ctl->p_full[t], (p_ph >> t) & 1u);
+            p_ph ^= 1u << t;
             tc_fence_after();
             if (lane == 0) trace_event(a, pos, 4 + 2 * t);
-            const bool skip = (MODE == kVSA) && (ctl->skip[t][b] != 0);
-            if (corr) {
-              mbar_wait(&ctl->o_ready[t], (ordy_ph >> t) & 1u);
-              ordy_ph ^= 1u << t;
-              tc_fence_after();
-            }
+            const bool skip = (MODE == kVSA) && (ctl->skip[t] != 0);
             if (!skip) {
-              issue_pv(t, b, vs, (o_init >> t) & 1u);
+              issue_pv(t, vs, (o_init >> t) & 1u);
               o_init |= 1u << t;
             }
-            if (corr_next) commit_elect(&ctl->o_full[t]);
             if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
           }
           if (next_s) {
             if (t == 0) ks = acquire();
-            issue_s_tile(g + SB, t, ks);
+            issue_s_tile(g + 1, t, ks);
             if (main_blk && lane == 0) trace_event(a, pos, 5 + 2 * t);
           }
         }
@@ -476,82 +461,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int t = 0; t < NQ; ++t) commit_elect(&ctl->o_final[t]);
     }
-  } else if (warp >= 14) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-  } else if (warp >= 8) {
-    // ============================ correction WG ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-    VFA_ROLE_SETUP();
-    const int r = tid - 256;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint32_t sc_ph = 0, of_ph = 0;
-    for (int pos = 1; pos < N; ++pos) {
-      if (!needs_corr(sched, pos)) continue;
-      const int b = (nchunks + pos) % SB;
-      for (int t = 0; t < NQ; ++t) {
-        const int bit = t * SB + b;
-        mbar_wait(&ctl->sc_full[t][b], (sc_ph >> bit) & 1u);
-        sc_ph ^= 1u << bit;
-        const float f = ctl->fbuf[t][b][r];
-        mbar_wait(&ctl->o_full[t], (of_ph >> t) & 1u);
-        of_ph ^= 1u << t;
-        tc_fence_after();
-        const bool work = (MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f);
-        if (work) {
-          const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
-          const float2 f2 = make_float2(f, f);
-#pragma unroll 1
-          for (int c = 0; c < D / 16; ++c) {
-            float v[16];
-            tmem_ld16(tO + c * 16, v);
-            tmem_wait_ld();
-            reg_fence16(v);
-            uint32_t u[16];
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const float2 o = __fmul2_rn(make_float2(v[e], v[e + 1]), f2);
-              u[e] = __float_as_uint(o.x);
-              u[e + 1] = __float_as_uint(o.y);
-            }
-            tmem_st16(tO + c * 16, u);
-          }
-          tmem_wait_st();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ctl->o_ready[t]);
-      }
-    }
   } else {
     // ============================ softmax WGs ============================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
-    const int t = warp >> 2;
+    // WG w = warp/4: query tile t = w/2, column half hf = w%2. Each thread owns row r of
+    // its tile (TMEM lane r) and HC = BC/2 columns of every S tile and D/2 columns of O.
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    const int t = warp >> 3;
+    const int hf = (warp >> 2) & 1;
     const int r = tid & 127;
     if (t < NQ) {
       VFA_ROLE_SETUP();
       const int h = unit.h0 + t;
       const int R = unit.qt * kBR + r;  // absolute query row
       const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t tO = tbase + C::kOBase + t * D + lane_off;
+      const uint32_t tS = tbase + C::s_off(t) + hf * HC + lane_off;  // this half's S columns
+      const uint32_t tO = tbase + C::kOBase + t * D + hf * HD + lane_off;
+      const uint32_t pair_bar = 1 + t;  // named barrier of the tile's two halves (256 threads)
       const float cs = a.c_scale;
-      float m2 = -INFINITY;  // running max, log2 units of scaled scores
-      float l = 0.f;
-      uint32_t s_ph = 0;  // bit b: phase of s_full[t][b]
+      float m2 = -INFINITY;  // running max, log2 units of scaled scores (identical in both halves)
+      float l = 0.f;         // this half's share of the normalizer
+      uint32_t s_ph = 0, xpar = 0;
       int n_special = 0, n_frozen = 0, n_skipped = 0;
       uint32_t over32 = 0, over16 = 0;
+      // half-row max exchange: returns max(mine, other half's) for this row
+      auto exchange_max = [&](float mine) -> float {
+        ctl->xmax[t][xpar][hf][r] = mine;
+        named_bar_sync(pair_bar, 2 * kBR);
+        const float other = ctl->xmax[t][xpar][hf ^ 1][r];
+        xpar ^= 1;
+        return fmaxf(mine, other);
+      };
 
       // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
       if (nchunks > 0) {
         float mx = -INFINITY;
         for (int ch = 0; ch < nchunks; ++ch) {
-          const int b = ch % SB;
-          const uint32_t tS = tbase + C::s_off(t, b) + lane_off;
-          mbar_wait(&ctl->s_full[t][b], (s_ph >> b) & 1u);
-          s_ph ^= 1u << b;
+          mbar_wait(&ctl->s_full[t], s_ph);
+          s_ph ^= 1;
           tc_fence_after();
-          const int valid = nrep - ch * BC;
+          const int valid = nrep - ch * BC - hf * HC;
 #pragma unroll
-          for (int c = 0; c < BC / 32; ++c) {
+          for (int c = 0; c < HC / 32; ++c) {
             float v[32];
             tmem_ld32(tS + c * 32, v);
             tmem_wait_ld();
@@ -562,63 +512,74 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->s_free[t][b]);
+          if (lane == 0) mbar_arrive(&ctl->s_free[t]);
         }
-        m2 = mx * cs;
+        m2 = exchange_max(mx) * cs;
       }
 
       const float2 cs2 = make_float2(cs, cs);
       for (int pos = 0; pos < N; ++pos) {
-        const int b = (nchunks + pos) % SB;
-        const uint32_t tS = tbase + C::s_off(t, b) + lane_off;
         const int j = sched_block(sched, pos);
         const bool special = (MODE == kFA) || sched_is_special(sched, j);
-        const bool corr = special && pos > 0;
         const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
-        const int lim = R - (j - 1) * BC;  // columns > lim are causally masked
-        mbar_wait(&ctl->s_full[t][b], (s_ph >> b) & 1u);
-        s_ph ^= 1u << b;
+        const int lim = R - (j - 1) * BC - hf * HC;  // this half's columns > lim are masked
+        mbar_wait(&ctl->s_full[t], s_ph);
+        s_ph ^= 1;
         tc_fence_after();
-        if (r == 0) trace_event(a, pos, 2 * t);
+        if (r == 0 && hf == 0) trace_event(a, pos, 2 * t);
         bool skipped = false;
-        float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this tile's P (pairs)
+        float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this half's P (pairs)
         if (MODE == kFA || MODE == kVSA || special) {
-          // ---- exact-update / skip-test block: rowmax over the full row (src/vfa.py:202-208,
-          //      src/sparse.py:296-300), then rescale and exponentiate
-          float v[BC];
+          // ---- exact-update / skip-test block: rowmax over the full row (two halves,
+          //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale and exponentiate
+          float v[HC];
 #pragma unroll
-          for (int c = 0; c < BC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+          for (int c = 0; c < HC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < BC / 32; ++c) reg_fence32(v + c * 32);
+          for (int c = 0; c < HC / 32; ++c) reg_fence32(v + c * 32);
           if (mask) {
 #pragma unroll
-            for (int e = 0; e < BC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+            for (int e = 0; e < HC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
           }
           float mt = -INFINITY;
 #pragma unroll
-          for (int e = 0; e < BC; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
+          for (int e = 0; e < HC; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
+          mt = exchange_max(mt);
           const float mt2 = mt * cs;
           const float m2n = fmaxf(m2, mt2);
           if (MODE == kVSA) {
             const bool below = (mt2 - m2n < a.log2_lambda) ||
                                (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
-            skipped = named_bar_and(1 + t, kBR, below);
+            skipped = named_bar_and(pair_bar, 2 * kBR, below);
           }
           if (skipped) {
             ++n_skipped;
-            if (corr) {
-              ctl->fbuf[t][b][r] = 1.0f;
-              mbar_arrive(&ctl->sc_full[t][b]);
-            }
           } else {
             if (special) {
               const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
               m2 = m2n;
               l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
-              if (corr) {
-                ctl->fbuf[t][b][r] = f;
-                mbar_arrive(&ctl->sc_full[t][b]);
+              // rescale this half of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
+              // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
+              const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
+              if (work) {
+                const float2 f2 = make_float2(f, f);
+#pragma unroll 1
+                for (int c = 0; c < HD / 16; ++c) {
+                  float o[16];
+                  tmem_ld16(tO + c * 16, o);
+                  tmem_wait_ld();
+                  reg_fence16(o);
+                  uint32_t u[16];
+#pragma unroll
+                  for (int e = 0; e < 16; e += 2) {
+                    const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+                    u[e] = __float_as_uint(x.x);
+                    u[e + 1] = __float_as_uint(x.y);
+                  }
+                  tmem_st16(tO + c * 16, u);
+                }
               }
               ++n_special;
             } else {
@@ -627,25 +588,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
             // masked entries are -inf in v and exponentiate to exact zeros on both paths
             if (a.monitor)
-              p_row<BC, true, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
+              p_row<HC, true, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
             else
-              p_row<BC, false, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
+              p_row<HC, false, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
           }
         } else {
           // ---- frozen block (VFA, src/vfa.py:209-215): no rowmax, no rescale, streamed chunks
           const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
           if (a.monitor) {
-            if (mask) p_frozen<BC, true, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-            else p_frozen<BC, true, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            if (mask) p_frozen<HC, true, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            else p_frozen<HC, true, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
           } else {
-            if (mask) p_frozen<BC, false, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-            else p_frozen<BC, false, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            if (mask) p_frozen<HC, false, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
+            else p_frozen<HC, false, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
           }
           ++n_frozen;
         }
         if (!skipped) l = __fadd_rn(l, __fadd_rn(acc.x, acc.y));
-        if (r == 0) {
-          if (MODE == kVSA) ctl->skip[t][b] = skipped ? 1u : 0u;
+        if (r == 0 && hf == 0) {
+          if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
           if (a.skip_trace) {
             const size_t idx = ((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos;
             a.skip_trace[idx] = skipped ? 2 : 1;
@@ -654,18 +615,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (r == 0) trace_event(a, pos, 2 * t + 1);
-        if (lane == 0) mbar_arrive(&ctl->p_full[t][b]);
+        if (r == 0 && hf == 0) trace_event(a, pos, 2 * t + 1);
+        if (lane == 0) mbar_arrive(&ctl->p_full[t]);
       }
 
-      // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l
+      // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l; l = l_lo + l_hi
+      ctl->xl[t][hf][r] = l;
+      named_bar_sync(pair_bar, 2 * kBR);
+      const float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
       mbar_wait(&ctl->o_final[t], 0);
       tc_fence_after();
-      const float inv = 1.0f / l;
-      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr;
+      const float inv = 1.0f / lsum;
+      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr + hf * HD;
       bool finite = true;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < HD / 32; ++c) {
         float v[32];
         tmem_ld32(tO + c * 32, v);
         tmem_wait_ld();
@@ -682,9 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(u[4 * q4], u[4 * q4 + 1], u[4 * q4 + 2], u[4 * q4 + 3]);
       }
       const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
-      if (a.lse) a.lse[lrow] = (m2 + __log2f(l)) * kLn2;
+      if (hf == 0 && a.lse) a.lse[lrow] = (m2 + __log2f(lsum)) * kLn2;
       if (a.status) {
-        if (l == 0.f) {
+        if (hf == 0 && lsum == 0.f) {
           if (m2 == -INFINITY) {
             atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
             atomicMin(&a.status[VFA_STATUS_MASKED_ROW], static_cast<unsigned>(lrow));
@@ -693,7 +657,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], static_cast<unsigned>(lrow));
           }
         }
-        if (!finite) {
+        // a row is non-finite if either half is: combine through smem, count it once
+        ctl->xfin[t][hf][r] = finite ? 1u : 0u;
+        named_bar_sync(pair_bar, 2 * kBR);
+        if (hf == 0 && !(ctl->xfin[t][0][r] && ctl->xfin[t][1][r])) {
           atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
           atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
         }
@@ -703,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
           atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
         }
-        if (r == 0) {
+        if (r == 0 && hf == 0) {
           atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
           atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
           atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_special));
@@ -716,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(ctl->tmem_base);
   }
@@ -849,6 +816,12 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncGetAttributes: ") + cudaGetErrorString(e));
+    if (vfa::kRegBudget > fa.numRegs * vfa::kThreads)
+      return fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(vfa::kRegBudget) + " exceeds the launch allocation " +
+                                    std::to_string(fa.numRegs * vfa::kThreads) + " (would deadlock)");
     attr_set = true;
   }
   const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
