@@ -77,10 +77,24 @@ struct FwdArgs {
 
 // debug timeline slots per visited block (CTA 0 only): softmax t: S ready, P done;
 // MMA t: P observed, next QK issued
-constexpr int kTraceSlots = 8;
+constexpr int kTraceSlots = 16;
 __device__ __forceinline__ void trace_event(const FwdArgs& a, int pos, int slot) {
   if (a.trace != nullptr && blockIdx.x == 0) a.trace[pos * kTraceSlots + slot] = clock64();
 }
+// fine-grained softmax events (tile 0, half 0, row 0), compiled in only with -DVFA_TRACE_INNER
+#ifdef VFA_TRACE_INNER
+__device__ long long* g_inner_trace;
+__device__ int g_inner_pos;
+#define VFA_INNER(slot)                                                                    \
+  do {                                                                                     \
+    if (g_inner_trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0)                   \
+      g_inner_trace[g_inner_pos * kTraceSlots + (slot)] = clock64();                       \
+  } while (0)
+#else
+#define VFA_INNER(slot) \
+  do {                  \
+  } while (0)
+#endif
 
 template <int D, int BC, int NQ>
 struct Cfg {
@@ -238,9 +252,11 @@ __device__ __forceinline__ void p_frozen(uint32_t tS, float2 cs2, float2 nmu2, i
     tmem_ld32(tS + c * 32, v);
     tmem_wait_ld();
     reg_fence32(v);
+    VFA_INNER(8 + 2 * c);
     uint32_t u[16];
     p_chunk32<MON, MASK, kPoly>(v, cs2, nmu2, lim - c * 32, u, acc, o32, o16);
     tmem_st16(tS + c * 16, u);
+    VFA_INNER(9 + 2 * c);
   }
 }
 
@@ -527,6 +543,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_ph ^= 1;
         tc_fence_after();
         if (r == 0 && hf == 0) trace_event(a, pos, 2 * t);
+#ifdef VFA_TRACE_INNER
+        if (tid == 0) g_inner_pos = pos;
+#endif
         bool skipped = false;
         float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this half's P (pairs)
         if (MODE == kFA || MODE == kVSA || special) {
@@ -612,7 +631,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             a.skip_trace[idx] = skipped ? 2 : 1;
           }
         }
+        VFA_INNER(13);
         tmem_wait_st();
+        VFA_INNER(14);
         tc_fence_before();
         __syncwarp();
         if (r == 0 && hf == 0) trace_event(a, pos, 2 * t + 1);
@@ -1028,6 +1049,9 @@ const char* vfa_last_error(void) { return g_last_error.c_str(); }
 
 int vfa_debug_trace(long long* device_buffer) {
   g_debug_trace = device_buffer;
+#ifdef VFA_TRACE_INNER
+  cudaMemcpyToSymbol(vfa::g_inner_trace, &device_buffer, sizeof(device_buffer));
+#endif
   return VFA_OK;
 }
 

@@ -24,7 +24,7 @@ dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
 r = Runner(q, k, v, a.variant, lam=1e-2 if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
 T = cfg["L"] // a.k_block
-buf = torch.zeros(T * 8, dtype=torch.int64, device=dev)
+buf = torch.zeros(T * 16, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)
 r.attn(sh)  # warm-up
@@ -33,7 +33,7 @@ r.krepr(sh)
 r.attn(sh)
 torch.cuda.synchronize()
 r.lib.vfa_debug_trace(None)
-tr = buf.cpu().numpy().reshape(T, 8).astype(np.float64)
+tr = buf.cpu().numpy().reshape(T, 16).astype(np.float64)
 n = int((tr[:, 1] > 0).sum())
 tr = tr[:n]
 t0 = tr[tr > 0].min()
@@ -51,6 +51,11 @@ for t in (0, 1):
           f" p90 {np.nanpercentile(busy[sl], 90):.0f}); softmax waits for S {np.nanmedian(wait_s[sl]):.0f};"
           f" MMA sees P after {np.nanmedian(seen[sl]):.0f}; S ready {np.nanmedian(qk_to_s[sl]):.0f} after QK issue;"
           f" period {np.nanmedian(np.diff(s_ready)[sl]):.0f}")
-print("first 6 blocks (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK]")
-for i in range(min(6, n)):
-    print(" ", np.round(tr[i]).astype(int).tolist())
+print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK]")
+for i in range(20, min(26, n)):
+    print(" ", np.round(tr[i, :8]).astype(int).tolist())
+if np.isfinite(tr[:, 8]).any():
+    inner = tr[:, 8:15] - tr[:, [0]]
+    print("tile0/half0 inner (rel. S ready): chunk0 ld done, chunk0 st issued, chunk1 ld done, chunk1 st issued,"
+          " ..., before wait::st, after wait::st")
+    print("  median:", [int(x) for x in np.nanmedian(inner[8:n - 4], axis=0)])
