@@ -270,26 +270,24 @@ def time_interleaved(runners, steps, flush, barrier):
     return out
 
 
-def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam):
-    """End-to-end through the public API: pinned H2D of q/k/v, forward, D2H of O + LSE."""
+def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam, chunk=1):
+    """End-to-end through the public API on HOST tensors: attention_forward(q_h, k_h, v_h)
+    with page-locked inputs runs the library's pipelined path (chunked H2D copy, kernels,
+    D2H copy of O + LSE on overlapping streams); timed with CUDA events on the caller's
+    stream, which the library makes wait for the last device->host copy."""
     import torch
-    from paper_2604_12798_b200 import attention_forward
+    from paper_2604_12798_b200 import attention_forward_host
     stream = torch.cuda.current_stream()
     total = 0.0
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(stream)
-        q = q_h.to(dev, non_blocking=True)
-        k = k_h.to(dev, non_blocking=True)
-        v = v_h.to(dev, non_blocking=True)
-        out, lse, _ = attention_forward(q, k, v, variant=variant, causal=True, lam=lam, check=False)
-        o_h.copy_(out, non_blocking=True)
-        lse_h.copy_(lse, non_blocking=True)
+        attention_forward_host(q_h, k_h, v_h, variant=variant, causal=True, lam=lam, out=o_h, lse=lse_h,
+                               check=False, chunk_kv_heads=chunk)
         e1.record(stream)
         torch.cuda.synchronize()
         total += e0.elapsed_time(e1)
-        del q, k, v, out, lse
     h2d = q_h.numel() * 2 + k_h.numel() * 2 + v_h.numel() * 2
     d2h = o_h.numel() * 2 + lse_h.numel() * 4
     return total / steps, h2d, d2h
@@ -376,15 +374,17 @@ def main_ours(args):
             del full
 
     # ---- end-to-end through the public API with host buffers (N GPUs, per-rank shard)
-    e2e_ms, h2d, d2h = None, 0, 0
+    e2e_ms, h2d, d2h, e2e_equal = None, 0, 0, None
     if not args.no_e2e:
         q_h = q.cpu().pin_memory()
         k_h = k.cpu().pin_memory()
         v_h = v.cpu().pin_memory()
         o_h = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
         lse_h = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
-        e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, 1, "vfa", None)  # warm-up
-        e2e_ms, h2d, d2h = e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, args.e2e_steps, "vfa", None)
+        e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, 1, "vfa", None, args.e2e_chunk)  # warm-up
+        e2e_ms, h2d, d2h = e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, args.e2e_steps, "vfa", None,
+                                     args.e2e_chunk)
+        e2e_equal = bool(torch.equal(o_h, runners["vfa"].o.cpu()) and torch.equal(lse_h, runners["vfa"].lse.cpu()))
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -442,8 +442,9 @@ def main_ours(args):
         if e2e_ms is not None:
             line["e2e"] = {"value": round(flops_total / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                            "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
-                           "d2h_bytes_per_step": d2h,
-                           "api": "paper_2604_12798_b200.attention_forward on pinned-host-copied inputs"}
+                           "d2h_bytes_per_step": d2h, "bitwise_equal_to_device_run": e2e_equal,
+                           "api": "paper_2604_12798_b200.attention_forward on page-locked host tensors (library-pipelined H2D / kernels / D2H)",
+                           "chunk_kv_heads": args.e2e_chunk}
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -527,6 +528,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=1, help="KV heads per pipelined host chunk")
     ap.add_argument("--cpu-core-seconds", type=float, default=24.0)
     ap.add_argument("--cpu-core-seconds-ref", type=float, default=2.5,
                     help="per-step wall seconds of the reference arm (x cores)")

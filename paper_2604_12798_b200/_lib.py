@@ -33,7 +33,8 @@ STATUS_COUNT = 4
 
 # every symbol include/vfa_b200.h declares
 EXPORTS = ("vfa_check_params", "vfa_workspace_bytes", "vfa_fwd", "vfa_krepr", "vfa_schedule",
-           "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace")
+           "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace",
+           "vfa_host_scratch_bytes", "vfa_fwd_host")
 
 
 class VfaParams(ctypes.Structure):
@@ -80,6 +81,10 @@ def load():
         lib.vfa_workspace_bytes.restype = ctypes.c_size_t
         lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
         lib.vfa_fwd.restype = ctypes.c_int
+        lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int]
+        lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
+        lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, vp]
+        lib.vfa_fwd_host.restype = ctypes.c_int
         lib.vfa_krepr.argtypes = [P, vp, vp, vp]
         lib.vfa_krepr.restype = ctypes.c_int
         lib.vfa_schedule.argtypes = [ctypes.c_int] * 9 + [ctypes.POINTER(ctypes.c_int),

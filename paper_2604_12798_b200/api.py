@@ -325,6 +325,14 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
         raise ValueError(f"unknown variant {variant!r}")
     if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
         raise ValueError(f"lambda must be in (0, 1], got {lam}")
+    if all(isinstance(x, torch.Tensor) and x.device.type == "cpu" for x in (q, k, v)):
+        if skip_trace or krepr_precomputed or workspace is not None:
+            raise ValueError("skip_trace / krepr_precomputed / workspace need device-resident inputs")
+        return attention_forward_host(q, k, v, variant=variant, causal=causal, q_block=q_block,
+                                      k_block=k_block, scale=scale, kind=kind, qkind=qkind,
+                                      reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
+                                      n_local=n_local, lam=lam, monitor=monitor, out=out, lse=lse,
+                                      check=check, stream=stream)
     lib = _lib.load()
     for name, x in (("q", q), ("k", k), ("v", v)):
         if not isinstance(x, torch.Tensor) or x.dtype != torch.bfloat16 or x.device.type != "cuda":
@@ -368,6 +376,61 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws}
     if check:
         check_status(status)
+    return out, lse, info
+
+
+def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
+                           scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True,
+                           tc1=None, n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
+                           check=True, stream=None, device=None, chunk_kv_heads=1):
+    """The forward on HOST tensors (bf16 [B, Hq, Lq, d] / [B, Hkv, Lk, d], contiguous;
+    page-locked for full overlap) -> host (O bf16, LSE fp32, info), through the C ABI's
+    vfa_fwd_host: chunks of `chunk_kv_heads` KV heads are copied in, computed and copied
+    out on overlapping streams, so the PCIe transfers hide behind the attention kernels.
+    The result is in host memory when this returns (check=True) or once `stream` (default:
+    the current stream of `device`) is synchronized (check=False)."""
+    lib = _lib.load()
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(x, torch.Tensor) or x.dtype != torch.bfloat16 or x.device.type != "cpu":
+            raise TypeError(f"{name} must be a bf16 CPU tensor")
+        if x.dim() != 4:
+            raise ValueError(f"{name} must be 4-D [B, H, N, d]")
+        if not x.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    pin = q.is_pinned()
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=pin)
+    if lse is None:
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, pin_memory=pin)
+    for name, x, dt in (("out", out, torch.bfloat16), ("lse", lse, torch.float32)):
+        if x.device.type != "cpu" or x.dtype != dt or not x.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {dt} CPU tensor")
+    if tuple(out.shape) != tuple(q.shape) or tuple(lse.shape) != tuple(q.shape[:3]):
+        raise ValueError("out / lse shapes do not match q")
+    p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
+                scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
+                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor)
+    rc = lib.vfa_check_params(ctypes.byref(p))
+    if rc:
+        _raise_for(rc)
+    nbytes = int(lib.vfa_host_scratch_bytes(ctypes.byref(p), int(chunk_kv_heads)))
+    if nbytes == 0:
+        raise ValueError(f"chunk_kv_heads={chunk_kv_heads} must divide heads_kv={k.shape[1]}")
+    with torch.cuda.device(dev):
+        scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        stats = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=dev)
+        status = torch.empty(_lib.STATUS_COUNT, dtype=torch.int32, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.vfa_fwd_host(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                              lse.data_ptr(), scratch.data_ptr(), nbytes, stats.data_ptr(),
+                              status.data_ptr(), int(chunk_kv_heads), ctypes.c_void_p(st))
+    if rc:
+        _raise_for(rc)
+    info = {"stats": stats, "status": status, "skip_trace": None, "workspace": None}
+    if check:
+        check_status(status)  # reads the status word: synchronizes with the stream
+        torch.cuda.synchronize(dev)
     return out, lse, info
 
 

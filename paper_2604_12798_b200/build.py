@@ -23,25 +23,28 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+def up_to_date(out: str = OUT) -> bool:
+    if not os.path.exists(out):
         return False
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return all(os.path.getmtime(s) <= t for s in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SOURCES]
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Build libvfa_b200.so (trace=True: libvfa_b200_trace.so with the -DVFA_TRACE debug
+    timeline compiled in, for scripts/trace_timeline.py; never the product library)."""
+    out = OUT.replace(".so", "_trace.so") if trace else OUT
+    if not force and up_to_date(out):
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DVFA_TRACE"] if trace else []), "-o", out + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force="-f" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="-f" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -33,6 +33,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/vfa_b200.h"
 #include "ptx.cuh"
@@ -72,27 +73,21 @@ struct FwdArgs {
   unsigned long long* stats;
   unsigned int* status;
   unsigned char* skip_trace;
+  long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
 
-// debug timeline slots per visited block (CTA 0 only): softmax t: S ready, P done;
-// MMA t: P observed, next QK issued
+// debug timeline slots per visited block (CTA 0 only, builds with -DVFA_TRACE): softmax t:
+// S ready, P done; MMA t: P observed, next QK issued
 constexpr int kTraceSlots = 16;
-__device__ __forceinline__ void trace_event(const FwdArgs& a, int pos, int slot) {
-  if (a.trace != nullptr && blockIdx.x == 0) a.trace[pos * kTraceSlots + slot] = clock64();
-}
-// fine-grained softmax events (tile 0, half 0, row 0), compiled in only with -DVFA_TRACE_INNER
-#ifdef VFA_TRACE_INNER
-__device__ long long* g_inner_trace;
-__device__ int g_inner_pos;
-#define VFA_INNER(slot)                                                                    \
-  do {                                                                                     \
-    if (g_inner_trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0)                   \
-      g_inner_trace[g_inner_pos * kTraceSlots + (slot)] = clock64();                       \
+#ifdef VFA_TRACE
+#define VFA_TRACE_EVENT(args, pos, slot)                                                     \
+  do {                                                                                       \
+    if ((args).trace != nullptr && blockIdx.x == 0) (args).trace[(pos) * kTraceSlots + (slot)] = clock64(); \
   } while (0)
 #else
-#define VFA_INNER(slot) \
-  do {                  \
+#define VFA_TRACE_EVENT(args, pos, slot) \
+  do {                                   \
   } while (0)
 #endif
 
@@ -125,7 +120,8 @@ struct __align__(16) Ctl {
   uint64_t kv_empty[NS];
   uint64_t s_full[NQ];  // MMA -> softmax halves: S of sequence element g ready
   uint64_t s_free[NQ];  // softmax halves -> MMA: m-init chunk read (8 warps)
-  uint64_t p_full[NQ];  // softmax halves -> MMA: P ready / skip decided (8 warps)
+  uint64_t p_full[NQ][2];  // softmax halves -> MMA: P chunk c (32 columns of each half) ready /
+                           // skip decided (8 warps); PV of chunk 0 overlaps the softmax of chunk 1
   uint64_t o_final[NQ];  // MMA -> epilogue: last PV completed
   uint32_t tmem_base;
   uint32_t skip[NQ];
@@ -216,18 +212,14 @@ __device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o1
   }
 }
 
-// 32 consecutive columns: P = exp2(s*cs - m2) -> 16 packed bf16x2 words, row sum into acc.
-template <bool MON, bool MASK, int kPoly>
-__device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu2, int lim, uint32_t* u,
-                                          float2& acc, uint32_t& o32, uint32_t& o16) {
+// 32 consecutive columns (masked entries already -inf): P = exp2(s*cs - m2) -> 16 packed
+// bf16x2 words; row sums into two independent packed accumulators (halves the FADD2 chain).
+template <bool MON, int kPoly>
+__device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu2, uint32_t* u, float2 (&acc)[2],
+                                          uint32_t& o32, uint32_t& o16) {
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
-    float2 s = make_float2(v[e], v[e + 1]);
-    if (MASK) {
-      s.x = (e > lim) ? -INFINITY : s.x;
-      s.y = (e + 1 > lim) ? -INFINITY : s.y;
-    }
-    const float2 x = __ffma2_rn(s, cs2, nmu2);
+    const float2 x = __ffma2_rn(make_float2(v[e], v[e + 1]), cs2, nmu2);
     count_over<MON>(x, o32, o16);
     float2 p;
     if (((e >> 1) & 7) < kPoly) {
@@ -236,39 +228,8 @@ __device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu
       p.x = ex2_approx(x.x);
       p.y = ex2_approx(x.y);
     }
-    acc = __fadd2_rn(acc, p);
+    acc[(e >> 1) & 1] = __fadd2_rn(acc[(e >> 1) & 1], p);
     u[e >> 1] = pack_bf16x2(p.x, p.y);
-  }
-}
-
-// Frozen block: stream S from TMEM in 32-column chunks, write P (bf16) back over the
-// already-read columns. One chunk body in the instruction stream (unroll 1).
-template <int BC, bool MON, bool MASK, int kPoly>
-__device__ __forceinline__ void p_frozen(uint32_t tS, float2 cs2, float2 nmu2, int lim, float2& acc,
-                                         uint32_t& o32, uint32_t& o16) {
-#pragma unroll 1
-  for (int c = 0; c < BC / 32; ++c) {
-    float v[32];
-    tmem_ld32(tS + c * 32, v);
-    tmem_wait_ld();
-    reg_fence32(v);
-    VFA_INNER(8 + 2 * c);
-    uint32_t u[16];
-    p_chunk32<MON, MASK, kPoly>(v, cs2, nmu2, lim - c * 32, u, acc, o32, o16);
-    tmem_st16(tS + c * 16, u);
-    VFA_INNER(9 + 2 * c);
-  }
-}
-
-// Exact-update block: the row is already in registers (masked entries -inf).
-template <int BC, bool MON, int kPoly>
-__device__ __forceinline__ void p_row(const float* v, uint32_t tS, float2 cs2, float2 nmu2, float2& acc,
-                                      uint32_t& o32, uint32_t& o16) {
-#pragma unroll
-  for (int c = 0; c < BC / 32; ++c) {
-    uint32_t u[16];
-    p_chunk32<MON, false, kPoly>(v + c * 32, cs2, nmu2, BC, u, acc, o32, o16);
-    tmem_st16(tS + c * 16, u);
   }
 }
 
@@ -300,7 +261,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl->q_full[t], 1);
       mbar_init(&ctl->s_full[t], 1);
       mbar_init(&ctl->s_free[t], 8);
-      mbar_init(&ctl->p_full[t], 8);
+      mbar_init(&ctl->p_full[t][0], 8);
+      mbar_init(&ctl->p_full[t][1], 8);
       mbar_init(&ctl->o_final[t], 1);
     }
     for (int s = 0; s < NS; ++s) {
@@ -418,17 +380,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       };
-      // P of half h occupies TMEM columns [h*HC, h*HC + HC/2) of S_t (packed bf16 pairs)
-      auto issue_pv = [&](int t, int st, bool acc) {
+      // P of half h occupies TMEM columns [h*HC, h*HC + HC/2) of S_t (packed bf16 pairs).
+      // PV chunk c: the K-steps over P columns [c*32, c*32 + 32) of both halves.
+      auto issue_pv_chunk = [&](int t, int st, int c, bool& first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
-        for (int kk = 0; kk < BC / 16; ++kk) {
-          const uint32_t pcol = (kk * 16 / HC) * HC + (kk * 16 % HC) / 2;
-          if (elect_one())
-            mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + pcol,
-                   (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV,
-                   (acc || kk > 0) ? 1u : 0u);
-          __syncwarp();
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int kk = hh * (HC / 16) + c * 2 + k2;  // K-step (16 key rows of V)
+            const uint32_t pcol = hh * HC + (c * 32 + k2 * 16) / 2;
+            if (elect_one())
+              mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + pcol,
+                     (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV, first ? 0u : 1u);
+            __syncwarp();
+            first = false;
+          }
         }
       };
       uint32_t sfree_ph = 0, p_ph = 0, o_init = 0;
@@ -456,21 +423,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ks = -1;
         for (int t = 0; t < NQ; ++t) {
           if (main_blk) {
-            mbar_wait(&ctl->p_full[t], (p_ph >> t) & 1u);
-            p_ph ^= 1u << t;
-            tc_fence_after();
-            if (lane == 0) trace_event(a, pos, 4 + 2 * t);
-            const bool skip = (MODE == kVSA) && (ctl->skip[t] != 0);
-            if (!skip) {
-              issue_pv(t, vs, (o_init >> t) & 1u);
-              o_init |= 1u << t;
+            bool first = ((o_init >> t) & 1u) == 0;  // first PV of this tile initialises O
+            bool skip = false;
+#pragma unroll
+            for (int c = 0; c < HC / 32; ++c) {
+              mbar_wait(&ctl->p_full[t][c], (p_ph >> t) & 1u);
+              tc_fence_after();
+              if (c == 0) {
+                if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
+                skip = (MODE == kVSA) && (ctl->skip[t] != 0);
+              }
+              if (!skip) issue_pv_chunk(t, vs, c, first);
             }
+            p_ph ^= 1u << t;
+            if (!skip) o_init |= 1u << t;
             if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
           }
           if (next_s) {
             if (t == 0) ks = acquire();
             issue_s_tile(g + 1, t, ks);
-            if (main_blk && lane == 0) trace_event(a, pos, 5 + 2 * t);
+            if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 5 + 2 * t);
           }
         }
         if (ks >= 0) commit_elect(&ctl->kv_empty[ks]);
@@ -497,7 +469,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m2 = -INFINITY;  // running max, log2 units of scaled scores (identical in both halves)
       float l = 0.f;         // this half's share of the normalizer
       uint32_t s_ph = 0, xpar = 0;
-      int n_special = 0, n_frozen = 0, n_skipped = 0;
       uint32_t over32 = 0, over16 = 0;
       // half-row max exchange: returns max(mine, other half's) for this row
       auto exchange_max = [&](float mine) -> float {
@@ -534,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 
       const float2 cs2 = make_float2(cs, cs);
+      int n_skipped = 0, n_skipped_special = 0;  // VSA only (FA/VFA counts are closed-form)
       for (int pos = 0; pos < N; ++pos) {
         const int j = sched_block(sched, pos);
         const bool special = (MODE == kFA) || sched_is_special(sched, j);
@@ -542,25 +514,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&ctl->s_full[t], s_ph);
         s_ph ^= 1;
         tc_fence_after();
-        if (r == 0 && hf == 0) trace_event(a, pos, 2 * t);
-#ifdef VFA_TRACE_INNER
-        if (tid == 0) g_inner_pos = pos;
-#endif
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
+        // this half's S row: all HC columns in registers behind a single TMEM wait
+        float v[HC];
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < HC / 32; ++c) reg_fence32(v + c * 32);
+        if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
+#pragma unroll
+          for (int e = 0; e < HC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        }
         bool skipped = false;
-        float2 acc = make_float2(0.f, 0.f);  // fp32 row sum of this half's P (pairs)
         if (MODE == kFA || MODE == kVSA || special) {
           // ---- exact-update / skip-test block: rowmax over the full row (two halves,
-          //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale and exponentiate
-          float v[HC];
-#pragma unroll
-          for (int c = 0; c < HC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < HC / 32; ++c) reg_fence32(v + c * 32);
-          if (mask) {
-#pragma unroll
-            for (int e = 0; e < HC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
-          }
+          //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
           float mt = -INFINITY;
 #pragma unroll
           for (int e = 0; e < HC; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
@@ -574,56 +543,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (skipped) {
             ++n_skipped;
-          } else {
-            if (special) {
-              const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
-              m2 = m2n;
-              l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
-              // rescale this half of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
-              // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
-              const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
-              if (work) {
-                const float2 f2 = make_float2(f, f);
+            n_skipped_special += special ? 1 : 0;
+          } else if (special) {
+            const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
+            m2 = m2n;
+            l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
+            // rescale this half of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
+            // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
+            const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
+            if (work) {
+              const float2 f2 = make_float2(f, f);
 #pragma unroll 1
-                for (int c = 0; c < HD / 16; ++c) {
-                  float o[16];
-                  tmem_ld16(tO + c * 16, o);
-                  tmem_wait_ld();
-                  reg_fence16(o);
-                  uint32_t u[16];
+              for (int c = 0; c < HD / 16; ++c) {
+                float o[16];
+                tmem_ld16(tO + c * 16, o);
+                tmem_wait_ld();
+                reg_fence16(o);
+                uint32_t u[16];
 #pragma unroll
-                  for (int e = 0; e < 16; e += 2) {
-                    const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
-                    u[e] = __float_as_uint(x.x);
-                    u[e + 1] = __float_as_uint(x.y);
-                  }
-                  tmem_st16(tO + c * 16, u);
+                for (int e = 0; e < 16; e += 2) {
+                  const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+                  u[e] = __float_as_uint(x.x);
+                  u[e + 1] = __float_as_uint(x.y);
                 }
+                tmem_st16(tO + c * 16, u);
               }
-              ++n_special;
-            } else {
-              ++n_frozen;
             }
-            const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
-            // masked entries are -inf in v and exponentiate to exact zeros on both paths
-            if (a.monitor)
-              p_row<HC, true, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
-            else
-              p_row<HC, false, kPolyPairs>(v, tS, cs2, nmu2, acc, over32, over16);
           }
-        } else {
-          // ---- frozen block (VFA, src/vfa.py:209-215): no rowmax, no rescale, streamed chunks
-          const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
-          if (a.monitor) {
-            if (mask) p_frozen<HC, true, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-            else p_frozen<HC, true, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-          } else {
-            if (mask) p_frozen<HC, false, true, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-            else p_frozen<HC, false, false, kPolyPairs>(tS, cs2, nmu2, lim, acc, over32, over16);
-          }
-          ++n_frozen;
         }
-        if (!skipped) l = __fadd_rn(l, __fadd_rn(acc.x, acc.y));
+        // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
         if (r == 0 && hf == 0) {
           if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
           if (a.skip_trace) {
@@ -631,14 +579,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             a.skip_trace[idx] = skipped ? 2 : 1;
           }
         }
-        VFA_INNER(13);
-        tmem_wait_st();
-        VFA_INNER(14);
-        tc_fence_before();
-        __syncwarp();
-        if (r == 0 && hf == 0) trace_event(a, pos, 2 * t + 1);
-        if (lane == 0) mbar_arrive(&ctl->p_full[t]);
+        if (!skipped) {
+          // P = exp2(S*c - m2) chunk by chunk; each 32-column chunk is handed to the MMA warp
+          // as soon as it is in TMEM, so PV of chunk 0 runs under the softmax of chunk 1
+          const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
+          float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int c = 0; c < HC / 32; ++c) {
+            uint32_t u[16];
+            if (a.monitor)
+              p_chunk32<true, kPolyPairs>(v + c * 32, cs2, nmu2, u, acc, over32, over16);
+            else
+              p_chunk32<false, kPolyPairs>(v + c * 32, cs2, nmu2, u, acc, over32, over16);
+            tmem_st16(tS + c * 16, u);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
+          }
+          l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
+        } else {
+          __syncwarp();
+          if (lane == 0)
+            for (int c = 0; c < HC / 32; ++c) mbar_arrive(&ctl->p_full[t][c]);
+        }
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
       }
+      const int n_special = (MODE == kVSA) ? sched.n_spec - n_skipped_special : sched.n_spec;
+      const int n_frozen = N - sched.n_spec - ((MODE == kVSA) ? n_skipped - n_skipped_special : 0);
 
       // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l; l = l_lo + l_hi
       ctl->xl[t][hf][r] = l;
@@ -667,15 +635,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(u[4 * q4], u[4 * q4 + 1], u[4 * q4 + 2], u[4 * q4 + 3]);
       }
       const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
+      const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
       if (hf == 0 && a.lse) a.lse[lrow] = (m2 + __log2f(lsum)) * kLn2;
       if (a.status) {
         if (hf == 0 && lsum == 0.f) {
           if (m2 == -INFINITY) {
             atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
-            atomicMin(&a.status[VFA_STATUS_MASKED_ROW], static_cast<unsigned>(lrow));
+            atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
           } else {
             atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
-            atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], static_cast<unsigned>(lrow));
+            atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
           }
         }
         // a row is non-finite if either half is: combine through smem, count it once
@@ -891,6 +860,18 @@ int launch_krepr(const VfaParams* p, const void* k, void* out, cudaStream_t st) 
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
+  if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * VFA_STAT_COUNT, st);
+  if (status) {
+    cudaMemsetAsync(status, 0, sizeof(unsigned) * VFA_STATUS_COUNT, st);
+    cudaMemsetAsync(status + VFA_STATUS_UNDERFLOW_ROW, 0xff, sizeof(unsigned) * 2, st);
+  }
+}
+
+int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                 void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base);
+
 }  // namespace
 
 extern "C" {
@@ -948,7 +929,19 @@ int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, voi
   if (!q || !k || !v || !o) return fail(VFA_ERR_DATA, "NULL tensor pointer");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
     return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, skip_trace,
+                      static_cast<cudaStream_t>(stream), true, 0);
+}
+
+}  // extern "C"
+
+namespace {
+// The forward on device buffers. zero_counters: reset stats/status first (false when a
+// caller accumulates several launches into one status word, e.g. vfa_fwd_host's chunks).
+int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                 void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base) {
+  int rc = VFA_OK;
   const bool minit = p->variant != VFA_VARIANT_FA && p->use_m_init;
   const int64_t nrep = n_reprs(p);
   if (minit) {
@@ -974,11 +967,7 @@ int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, voi
   } else {
     mr = mk;
   }
-  if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * VFA_STAT_COUNT, st);
-  if (status) {
-    cudaMemsetAsync(status, 0, sizeof(unsigned) * VFA_STATUS_COUNT, st);
-    cudaMemsetAsync(status + VFA_STATUS_UNDERFLOW_ROW, 0xff, sizeof(unsigned) * 2, st);
-  }
+  if (zero_counters) reset_counters(stats, status, st);
   if (skip_trace)
     cudaMemsetAsync(skip_trace, 0,
                     static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * n_key_blocks(p)), st);
@@ -1012,12 +1001,172 @@ int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, voi
   a.stats = reinterpret_cast<unsigned long long*>(stats);
   a.status = status;
   a.skip_trace = skip_trace;
+  a.row_base = row_base;
   a.trace = g_debug_trace;
 
   if (D == 128 && BC == 128) return dispatch_nq<128, 128>(p, nq, mq, mk, mv, mr, a, st);
   if (D == 128 && BC == 64) return dispatch_nq<128, 64>(p, nq, mq, mk, mv, mr, a, st);
   if (D == 64 && BC == 128) return dispatch_nq<64, 128>(p, nq, mq, mk, mv, mr, a, st);
   return dispatch_nq<64, 64>(p, nq, mq, mk, mv, mr, a, st);
+}
+
+// ---------------------------------------------------------------- host-resident pipeline
+// vfa_fwd_host: the problem is cut into chunks of (one batch, `ck` KV heads with their GQA
+// query heads). Chunk c is copied host->device on the H2D stream into scratch slot c % S,
+// computed on compute stream c % 2 (so one chunk's causal tail overlaps the next chunk's
+// head), and its O / LSE copied back on the D2H stream, so PCIe transfers in both
+// directions overlap the attention kernels.
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct ChunkGeom {
+  int64_t ck, nq, chunks, slots;
+  size_t q_bytes, kv_bytes, lse_bytes, ws_bytes, slot_bytes;
+  VfaParams cp;  // the per-chunk problem (dense device layout)
+};
+
+ChunkGeom chunk_geom(const VfaParams* p, int chunk_kv_heads) {
+  ChunkGeom g{};
+  g.ck = chunk_kv_heads;
+  const int64_t group = p->heads_q / p->heads_kv;
+  g.nq = g.ck * group;
+  g.chunks = p->batch * (p->heads_kv / g.ck);
+  g.slots = g.chunks < 3 ? g.chunks : 3;
+  g.cp = *p;
+  g.cp.batch = 1;
+  g.cp.heads_q = g.nq;
+  g.cp.heads_kv = g.ck;
+  const int64_t D = p->head_dim;
+  const int64_t qs[3] = {g.nq * p->seq_q * D, p->seq_q * D, D};
+  const int64_t ks[3] = {g.ck * p->seq_k * D, p->seq_k * D, D};
+  for (int i = 0; i < 3; ++i) {
+    g.cp.q_stride[i] = g.cp.o_stride[i] = qs[i];
+    g.cp.k_stride[i] = g.cp.v_stride[i] = ks[i];
+  }
+  g.q_bytes = static_cast<size_t>(g.nq * p->seq_q * D * 2);
+  g.kv_bytes = static_cast<size_t>(g.ck * p->seq_k * D * 2);
+  g.lse_bytes = static_cast<size_t>(g.nq * p->seq_q * 4);
+  g.ws_bytes = vfa_workspace_bytes(&g.cp);
+  g.slot_bytes = 2 * align_up(g.q_bytes) + 2 * align_up(g.kv_bytes) + align_up(g.lse_bytes) + align_up(g.ws_bytes);
+  return g;
+}
+
+struct HostStreams {
+  int device = -1;
+  cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {nullptr, nullptr};
+};
+
+// per-thread, per-device streams of the pipeline (created once, non-blocking)
+int host_streams(HostStreams** out) {
+  thread_local HostStreams cache[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 16) return fail(VFA_ERR_CUDA, "cudaGetDevice failed");
+  HostStreams& s = cache[dev];
+  if (s.device != dev) {
+    cudaStream_t* all[4] = {&s.h2d, &s.d2h, &s.comp[0], &s.comp[1]};
+    for (cudaStream_t* x : all)
+      if (cudaStreamCreateWithFlags(x, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(VFA_ERR_CUDA, "cudaStreamCreateWithFlags failed");
+    s.device = dev;
+  }
+  *out = &s;
+  return VFA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads) {
+  if (!p || vfa_check_params(p) != VFA_OK || chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads) return 0;
+  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
+  return static_cast<size_t>(g.slots) * g.slot_bytes + kAlign;
+}
+
+int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host, void* o_host,
+                 float* lse_host, void* scratch, size_t scratch_bytes, long long* stats, unsigned int* status,
+                 int chunk_kv_heads, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!q_host || !k_host || !v_host || !o_host) return fail(VFA_ERR_DATA, "NULL host pointer");
+  if (chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads)
+    return fail(VFA_ERR_CONFIG, "chunk_kv_heads must divide heads_kv");
+  if (p->krepr_precomputed) return fail(VFA_ERR_CONFIG, "vfa_fwd_host computes the representations itself");
+  const size_t need = vfa_host_scratch_bytes(p, chunk_kv_heads);
+  if (!scratch || scratch_bytes < need) return fail(VFA_ERR_DATA, "scratch too small (vfa_host_scratch_bytes)");
+  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
+  HostStreams* hs = nullptr;
+  rc = host_streams(&hs);
+  if (rc) return rc;
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~uintptr_t(kAlign - 1));
+
+  std::vector<cudaEvent_t> ev;
+  auto new_event = [&]() -> cudaEvent_t {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    ev.push_back(e);
+    return e;
+  };
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);  // released once their work completes
+  };
+  // counters accumulate over chunks; scratch reuse is ordered after the caller's prior work
+  reset_counters(stats, status, caller);
+  cudaEvent_t entry = new_event();
+  if (!entry) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+  cudaEventRecord(entry, caller);
+  cudaStreamWaitEvent(hs->h2d, entry, 0);
+  cudaStreamWaitEvent(hs->comp[0], entry, 0);
+  cudaStreamWaitEvent(hs->comp[1], entry, 0);
+
+  const int64_t D = p->head_dim, group = p->heads_q / p->heads_kv;
+  const int64_t per_b = p->heads_kv / g.ck;
+  std::vector<cudaEvent_t> slot_free(static_cast<size_t>(g.slots), nullptr);
+  for (int64_t c = 0; c < g.chunks; ++c) {
+    const int64_t b = c / per_b, kv0 = (c % per_b) * g.ck, h0 = kv0 * group;
+    const int64_t s = c % g.slots;
+    uint8_t* sl = base + s * g.slot_bytes;
+    uint8_t* dq = sl;
+    uint8_t* dk = dq + align_up(g.q_bytes);
+    uint8_t* dv = dk + align_up(g.kv_bytes);
+    uint8_t* dout = dv + align_up(g.kv_bytes);
+    float* dlse = reinterpret_cast<float*>(dout + align_up(g.q_bytes));
+    uint8_t* dws = reinterpret_cast<uint8_t*>(dlse) + align_up(g.lse_bytes);
+    const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
+    const size_t koff = static_cast<size_t>((b * p->heads_kv + kv0) * p->seq_k * D) * 2;
+    const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
+    // H2D (after the slot's previous chunk has been copied out)
+    if (slot_free[s]) cudaStreamWaitEvent(hs->h2d, slot_free[s], 0);
+    cudaMemcpyAsync(dk, static_cast<const uint8_t*>(k_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
+    cudaMemcpyAsync(dv, static_cast<const uint8_t*>(v_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
+    cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, g.q_bytes, cudaMemcpyHostToDevice, hs->h2d);
+    cudaEvent_t in = new_event(), done = new_event(), out = new_event();
+    if (!in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+    cudaEventRecord(in, hs->h2d);
+    // compute
+    cudaStream_t cs = hs->comp[c & 1];
+    cudaStreamWaitEvent(cs, in, 0);
+    rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, cs, false,
+                      static_cast<long long>(loff));
+    if (rc) return cleanup(), rc;
+    cudaEventRecord(done, cs);
+    // D2H
+    cudaStreamWaitEvent(hs->d2h, done, 0);
+    cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
+    if (lse_host)
+      cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
+    cudaEventRecord(out, hs->d2h);
+    slot_free[s] = out;
+  }
+  cudaEvent_t exit_ev = new_event();
+  if (!exit_ev) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+  cudaEventRecord(exit_ev, hs->d2h);
+  cudaStreamWaitEvent(caller, exit_ev, 0);
+  cleanup();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("vfa_fwd_host: ") + cudaGetErrorString(e));
+  return VFA_OK;
 }
 
 int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local, int reorder,
@@ -1048,11 +1197,13 @@ int vfa_status_code(const unsigned int* status_host) {
 const char* vfa_last_error(void) { return g_last_error.c_str(); }
 
 int vfa_debug_trace(long long* device_buffer) {
+#ifdef VFA_TRACE
   g_debug_trace = device_buffer;
-#ifdef VFA_TRACE_INNER
-  cudaMemcpyToSymbol(vfa::g_inner_trace, &device_buffer, sizeof(device_buffer));
-#endif
   return VFA_OK;
+#else
+  (void)device_buffer;
+  return fail(VFA_ERR_CONFIG, "library built without -DVFA_TRACE (scripts/trace_timeline.py builds the trace variant)");
+#endif
 }
 
 const char* vfa_version(void) { return "vfa_b200 0.1.0 (sm_100a, tcgen05/TMEM/TMA)"; }

@@ -12,6 +12,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_12798_b200 import _lib, build  # noqa: E402
+
+_lib.LIB_PATH = build.build(trace=True)  # the -DVFA_TRACE variant of the library
 from bench import CONFIGS, Runner, make_inputs  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -54,8 +57,3 @@ for t in (0, 1):
 print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK]")
 for i in range(20, min(26, n)):
     print(" ", np.round(tr[i, :8]).astype(int).tolist())
-if np.isfinite(tr[:, 8]).any():
-    inner = tr[:, 8:15] - tr[:, [0]]
-    print("tile0/half0 inner (rel. S ready): chunk0 ld done, chunk0 st issued, chunk1 ld done, chunk1 st issued,"
-          " ..., before wait::st, after wait::st")
-    print("  median:", [int(x) for x in np.nanmedian(inner[8:n - 4], axis=0)])

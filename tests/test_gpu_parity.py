@@ -292,3 +292,40 @@ def test_dropin_api_mirrors_reference():
     o3, c3, stats, _ = vsa_forward(p, SkipConfig(lam=1e-9))
     assert stats.blocks_skipped == 0 and torch.equal(o3, out)
     assert c3.rowmax_reductions == stats.blocks_visited
+
+
+@pytest.mark.parametrize("variant,chunk,b", [("vfa", 1, 1), ("fa", 2, 1), ("vsa", 1, 2), ("vfa", 4, 2)])
+def test_host_pipeline_bitwise_equals_device_path(variant, chunk, b):
+    # vfa_fwd_host (chunked H2D / kernels / D2H) computes exactly what vfa_fwd computes
+    from paper_2604_12798_b200 import attention_forward, stats_dict
+    L, Hq, Hkv = 1024, 8, 4
+    q, k, v = _rand((b, Hq, L, 128), 101), _rand((b, Hkv, L, 128), 102), _rand((b, Hkv, L, 128), 103)
+    kw = dict(variant=variant, causal=True, lam=1e-2 if variant == "vsa" else None)
+    o1, l1, i1, st1 = _run_gpu(q, k, v, **kw)
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    from paper_2604_12798_b200 import attention_forward_host
+    o2, l2, i2 = attention_forward_host(qh, kh, vh, chunk_kv_heads=chunk, **kw)
+    assert o2.device.type == "cpu" and l2.device.type == "cpu"
+    assert torch.equal(o1.cpu(), o2) and torch.equal(l1.cpu(), l2)
+    assert stats_dict(i2) == st1
+    # and through the generic entry point with CPU tensors (pageable memory works too)
+    o3, l3, _ = attention_forward(q.cpu(), k.cpu(), v.cpu(), **kw)
+    assert torch.equal(o3, o2) and torch.equal(l3, l2)
+
+
+def test_host_pipeline_reports_whole_problem_row():
+    # the golden normalizer-underflow case (reference tests/test_cli.py:177-193 geometry at
+    # Br=Bc=128) placed at (batch 1, head 1) of a 2x2-head problem that runs as 4 chunks: the
+    # status must carry the whole-problem linear row ((b * Hq + h) * L + r)
+    from paper_2604_12798_b200 import attention_forward_host
+    from paper_2604_12798_b200.api import NormalizerUnderflowError
+    name = "vfa_underflow_kmax"
+    m = case(name)[0]
+    qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16) for x in case_bits(name))
+    B, H, (L, d) = 2, 2, qb.shape
+    q, k, v = (_rand((B, H, L, d), 7 + i, dev="cpu") for i in range(3))
+    q[1, 1], k[1, 1], v[1, 1] = qb, kb, vb
+    with pytest.raises(NormalizerUnderflowError) as ei:
+        attention_forward_host(q, k, v, variant="vfa", kind=m["kind"], causal=m["causal"],
+                               k_block=m["k_block"], chunk_kv_heads=1)
+    assert ei.value.row == (1 * H + 1) * L + int(m["error"].split(":")[1])

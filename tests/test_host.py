@@ -166,3 +166,15 @@ def test_entry_points_fail_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(_lib.LibraryNotBuilt):
         _lib.load()
+
+
+def test_host_scratch_bytes(lib):
+    p = _params()  # B=1, Hq=4, Hkv=2, L=1024, d=128
+    one = lib.vfa_host_scratch_bytes(ctypes.byref(p), 1)
+    two = lib.vfa_host_scratch_bytes(ctypes.byref(p), 2)
+    # a slot holds Q + O (2 query heads) + K + V (1 KV head) + LSE + the representation workspace
+    slot = 2 * (2 * 1024 * 128 * 2) + 2 * (1024 * 128 * 2) + 2 * 1024 * 4
+    assert one >= 2 * slot and two >= slot
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 3) == 0  # 3 does not divide Hkv = 2
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 0) == 0
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(_params(k_block=96)), 1) == 0
