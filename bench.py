@@ -199,13 +199,13 @@ def make_inputs(cfg, dev, seed=1234):
 class Runner:
     """Pre-allocated launcher for one variant over one (sharded) problem."""
 
-    def __init__(self, q, k, v, variant, lam=None, k_block=128, n_sink=1, n_local=1):
+    def __init__(self, q, k, v, variant, lam=None, k_block=128, n_sink=1, n_local=1, lib=None):
         import ctypes
 
         import torch
         from paper_2604_12798_b200 import _lib
         from paper_2604_12798_b200.api import _params
-        self.torch, self.ctypes, self.lib = torch, ctypes, _lib.load()
+        self.torch, self.ctypes, self.lib = torch, ctypes, lib if lib is not None else _lib.load()
         self.q, self.k, self.v = q, k, v
         self.o = torch.empty_like(q)
         self.lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)

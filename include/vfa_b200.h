@@ -92,7 +92,8 @@ typedef struct VfaParams {
   int32_t monitor;      /* count exp-argument overflows (OverflowMonitor, src/vfa.py:109-128) */
   double lam;           /* VSA threshold lambda in (0, 1]; <= 0 disables skipping (SkipConfig.lam=None) */
   int32_t krepr_precomputed; /* 1: workspace already holds vfa_krepr() output for this K; skip recomputing */
-  int32_t reserved;
+  int32_t softmax_split; /* threads sharing one row of a query tile: 0 = per-variant default,
+                           2 = per-tile warp sets, 4 = all softmax warps serve both tiles */
 } VfaParams;
 
 /* Host-only validation (no GPU needed). Returns VFA_OK or VFA_ERR_CONFIG / VFA_ERR_DATA. */

@@ -51,7 +51,7 @@ class VfaParams(ctypes.Structure):
         ("reorder", ctypes.c_int32), ("use_m_init", ctypes.c_int32), ("tc1", ctypes.c_int32),
         ("n_sink", ctypes.c_int32), ("n_local", ctypes.c_int32), ("monitor", ctypes.c_int32),
         ("lam", ctypes.c_double),
-        ("krepr_precomputed", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("krepr_precomputed", ctypes.c_int32), ("softmax_split", ctypes.c_int32),
     ]
 
 
@@ -63,6 +63,37 @@ class LibraryNotBuilt(RuntimeError):
     pass
 
 
+def bind(path: str):
+    """ctypes.CDLL of a libvfa_b200 build at `path` with every C-ABI signature set."""
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER(VfaParams)
+    vp = ctypes.c_void_p
+    lib.vfa_check_params.argtypes = [P]
+    lib.vfa_check_params.restype = ctypes.c_int
+    lib.vfa_workspace_bytes.argtypes = [P]
+    lib.vfa_workspace_bytes.restype = ctypes.c_size_t
+    lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    lib.vfa_fwd.restype = ctypes.c_int
+    lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int]
+    lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
+    lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, vp]
+    lib.vfa_fwd_host.restype = ctypes.c_int
+    lib.vfa_krepr.argtypes = [P, vp, vp, vp]
+    lib.vfa_krepr.restype = ctypes.c_int
+    lib.vfa_schedule.argtypes = [ctypes.c_int] * 9 + [ctypes.POINTER(ctypes.c_int),
+                                                     ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int]
+    lib.vfa_schedule.restype = ctypes.c_int
+    lib.vfa_status_code.argtypes = [ctypes.POINTER(ctypes.c_uint)]
+    lib.vfa_status_code.restype = ctypes.c_int
+    lib.vfa_last_error.argtypes = []
+    lib.vfa_last_error.restype = ctypes.c_char_p
+    lib.vfa_debug_trace.argtypes = [vp]
+    lib.vfa_debug_trace.restype = ctypes.c_int
+    lib.vfa_version.argtypes = []
+    lib.vfa_version.restype = ctypes.c_char_p
+    return lib
+
+
 def load():
     """Load libvfa_b200.so (raises LibraryNotBuilt if absent — there is no CPU fallback)."""
     global _lib
@@ -72,34 +103,8 @@ def load():
         if not os.path.exists(LIB_PATH):
             raise LibraryNotBuilt(
                 f"{LIB_PATH} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
-        lib = ctypes.CDLL(LIB_PATH)
-        P = ctypes.POINTER(VfaParams)
-        vp = ctypes.c_void_p
-        lib.vfa_check_params.argtypes = [P]
-        lib.vfa_check_params.restype = ctypes.c_int
-        lib.vfa_workspace_bytes.argtypes = [P]
-        lib.vfa_workspace_bytes.restype = ctypes.c_size_t
-        lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
-        lib.vfa_fwd.restype = ctypes.c_int
-        lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int]
-        lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
-        lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, vp]
-        lib.vfa_fwd_host.restype = ctypes.c_int
-        lib.vfa_krepr.argtypes = [P, vp, vp, vp]
-        lib.vfa_krepr.restype = ctypes.c_int
-        lib.vfa_schedule.argtypes = [ctypes.c_int] * 9 + [ctypes.POINTER(ctypes.c_int),
-                                                         ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int]
-        lib.vfa_schedule.restype = ctypes.c_int
-        lib.vfa_status_code.argtypes = [ctypes.POINTER(ctypes.c_uint)]
-        lib.vfa_status_code.restype = ctypes.c_int
-        lib.vfa_last_error.argtypes = []
-        lib.vfa_last_error.restype = ctypes.c_char_p
-        lib.vfa_debug_trace.argtypes = [vp]
-        lib.vfa_debug_trace.restype = ctypes.c_int
-        lib.vfa_version.argtypes = []
-        lib.vfa_version.restype = ctypes.c_char_p
-        _lib = lib
-        return lib
+        _lib = bind(LIB_PATH)
+        return _lib
 
 
 def last_error() -> str:

@@ -273,7 +273,7 @@ def _strides(x):
 
 
 def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind, reorder,
-            use_m_init, tc1, n_sink, n_local, lam, monitor):
+            use_m_init, tc1, n_sink, n_local, lam, monitor, softmax_split=0):
     if kind not in _lib.KEY_REPRS:
         raise ValueError(f"unknown key representation {kind!r}")
     if qkind not in _lib.QUERY_REPRS:
@@ -297,6 +297,7 @@ def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind
     p.n_sink, p.n_local = int(n_sink), int(n_local)
     p.monitor = int(bool(monitor))
     p.lam = float(lam) if lam is not None else 0.0
+    p.softmax_split = int(softmax_split)
     return p
 
 
@@ -311,7 +312,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                       kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
                       n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
                       check=True, skip_trace=False, stream=None, workspace=None,
-                      krepr_precomputed=False):
+                      krepr_precomputed=False, softmax_split=0):
     """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
 
     Returns (out, lse, info) with info = {"stats": int64 device tensor | dict,
@@ -320,6 +321,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     FullyMaskedRowError / NormalizerUnderflowError raised like src/core.py:101-109.
     workspace: optional uint8 device buffer (>= vfa_workspace_bytes) holding the key-block
     representations; with krepr_precomputed=True they are reused instead of recomputed.
+    softmax_split: 0 (per-variant default), 2 or 4 threads per row of a query tile (a layout
+    choice: results are within tolerance of each other, bitwise-stable for a fixed split).
     """
     if variant not in _lib.VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
@@ -332,7 +335,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                                       k_block=k_block, scale=scale, kind=kind, qkind=qkind,
                                       reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
                                       n_local=n_local, lam=lam, monitor=monitor, out=out, lse=lse,
-                                      check=check, stream=stream)
+                                      check=check, stream=stream, softmax_split=softmax_split)
     lib = _lib.load()
     for name, x in (("q", q), ("k", k), ("v", v)):
         if not isinstance(x, torch.Tensor) or x.dtype != torch.bfloat16 or x.device.type != "cuda":
@@ -346,7 +349,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
         lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
-                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor)
+                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
+                softmax_split=softmax_split)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)
@@ -382,7 +386,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
 def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
                            scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True,
                            tc1=None, n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
-                           check=True, stream=None, device=None, chunk_kv_heads=1):
+                           check=True, stream=None, device=None, chunk_kv_heads=1, softmax_split=0):
     """The forward on HOST tensors (bf16 [B, Hq, Lq, d] / [B, Hkv, Lk, d], contiguous;
     page-locked for full overlap) -> host (O bf16, LSE fp32, info), through the C ABI's
     vfa_fwd_host: chunks of `chunk_kv_heads` KV heads are copied in, computed and copied
@@ -410,7 +414,8 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
         raise ValueError("out / lse shapes do not match q")
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
-                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor)
+                tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
+                softmax_split=softmax_split)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)

@@ -91,14 +91,18 @@ constexpr int kTraceSlots = 16;
   } while (0)
 #endif
 
-template <int D, int BC, int NQ>
+template <int D, int BC, int NQ, int SPLIT>
 struct Cfg {
   static constexpr int kQBytes = kBR * D * 2;
   static constexpr int kKVBytes = BC * D * 2;
   static constexpr int kDCh = D / 64;  // 64-column (128-byte) swizzle chunks
-  static constexpr int kHC = BC / 2;   // S columns per softmax half (column split of each row)
-  static constexpr int kHD = D / 2;    // O columns rescaled / stored by each half
-  static constexpr int kCtlBytes = 12288;
+  // softmax column split: each row of a tile is shared by SPLIT threads (one per warpgroup)
+  static constexpr int kCP = BC / SPLIT;             // S columns per part
+  static constexpr int kOP = D / SPLIT;              // O columns rescaled / stored per part
+  static constexpr int kNCH = kCP >= 32 ? 2 : 1;     // P hand-off chunks per block
+  static constexpr int kCW = kCP / kNCH;             // columns per P chunk (16 or 32)
+  static constexpr int kWarpsPerTile = SPLIT * 4;    // softmax warps covering one tile
+  static constexpr int kCtlBytes = 16384;
   static constexpr int kAvail = kMaxSmem - 1024 - kCtlBytes - NQ * kQBytes;
   static constexpr int kStagesRaw = kAvail / kKVBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -110,7 +114,8 @@ struct Cfg {
   static constexpr uint32_t kTmemCols = kColsUsed <= 256 ? 256 : 512;
   static_assert(kColsUsed <= 512, "TMEM over-subscribed");
   static_assert(kStages >= 3, "not enough shared memory for a K/V ring");
-  static_assert(kHC % 32 == 0, "half row must be whole 32-column chunks");
+  static_assert(kCW % 16 == 0 && kOP % 16 == 0, "parts must be whole 16-column chunks");
+  static_assert(SPLIT == 2 || SPLIT == 4, "SPLIT is 2 (per-tile warp sets) or 4 (all warps, both tiles)");
 };
 
 template <int NS, int NQ>
@@ -118,16 +123,16 @@ struct __align__(16) Ctl {
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
-  uint64_t s_full[NQ];  // MMA -> softmax halves: S of sequence element g ready
-  uint64_t s_free[NQ];  // softmax halves -> MMA: m-init chunk read (8 warps)
-  uint64_t p_full[NQ][2];  // softmax halves -> MMA: P chunk c (32 columns of each half) ready /
-                           // skip decided (8 warps); PV of chunk 0 overlaps the softmax of chunk 1
-  uint64_t o_final[NQ];  // MMA -> epilogue: last PV completed
+  uint64_t s_full[NQ];     // MMA -> softmax: S of sequence element g ready
+  uint64_t s_free[NQ];     // softmax -> MMA: m-init chunk read (16 warps)
+  uint64_t p_full[NQ][2];  // softmax -> MMA: P chunk c (16 columns of each quarter = one PV
+                           // K-step per quarter) ready / skip decided (16 warps)
+  uint64_t o_final[NQ];    // MMA -> epilogue: last PV completed
   uint32_t tmem_base;
   uint32_t skip[NQ];
-  float xmax[NQ][2][2][kBR];  // [tile][parity][half][row]: half-row maxima exchange
-  float xl[NQ][2][kBR];       // [tile][half][row]: final half-row sums
-  uint32_t xfin[NQ][2][kBR];  // [tile][half][row]: output finite flags
+  float xmax[NQ][2][4][kBR];    // [tile][parity][quarter][row]: quarter-row maxima exchange
+  float xl[NQ][4][kBR];         // [tile][quarter][row]: final quarter-row sums
+  uint8_t xfin[NQ][4][kBR];     // [tile][quarter][row]: output finite flags
 };
 
 struct Unit {
@@ -177,10 +182,27 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
 // on MUFU.EX2 for most pairs and on the FMA pipe (degree-4 polynomial, |rel err| < 3e-6)
 // for kPoly of every 8 pairs, so that neither the XU nor the FMA pipe limits the
 // tensor core; row sums accumulate in packed FADD2; P is packed to bf16 pairs.
-#ifndef VFA_POLY_PAIRS
-#define VFA_POLY_PAIRS 3
+#ifdef VFA_POLY_PAIRS
+constexpr int kPolyOverride = VFA_POLY_PAIRS;  // tuning experiments (scripts/ab.py)
+#else
+constexpr int kPolyOverride = -1;
 #endif
-constexpr int kPolyPairs = VFA_POLY_PAIRS;  // of every 8 element pairs (tuning knob)
+// Element pairs (of every 8) whose exp2 runs on the FMA pipe (degree-4 polynomial) instead
+// of MUFU.EX2. Under the B200's 1 kW power cap the 13-instruction polynomial costs more
+// energy (lower clocks) than it saves in MUFU time: measured best is 0 for both softmax
+// splits (profiles/ab_r01_poly.txt); the polynomial stays as a tuning knob. Kept identical
+// for every split so P (hence O) does not depend on the split.
+__host__ __device__ constexpr int poly_pairs() { return kPolyOverride >= 0 ? kPolyOverride : 0; }
+// softmax column split per mode (see the softmax role): measured best per variant
+#ifndef VFA_SPLIT_FA
+#define VFA_SPLIT_FA 2
+#endif
+#ifndef VFA_SPLIT_VFA
+#define VFA_SPLIT_VFA 4
+#endif
+#ifndef VFA_SPLIT_VSA
+#define VFA_SPLIT_VSA 2
+#endif
 
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   // clamp to [-127, 128]: x <= -127 (incl. masked -inf) gives exactly +0 (the exponent add
@@ -212,13 +234,13 @@ __device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o1
   }
 }
 
-// 32 consecutive columns (masked entries already -inf): P = exp2(s*cs - m2) -> 16 packed
+// W consecutive columns (masked entries already -inf): P = exp2(s*cs - m2) -> W/2 packed
 // bf16x2 words; row sums into two independent packed accumulators (halves the FADD2 chain).
-template <bool MON, int kPoly>
-__device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu2, uint32_t* u, float2 (&acc)[2],
-                                          uint32_t& o32, uint32_t& o16) {
+template <int W, bool MON, int kPoly>
+__device__ __forceinline__ void p_chunk(const float* v, float2 cs2, float2 nmu2, uint32_t* u, float2 (&acc)[2],
+                                        uint32_t& o32, uint32_t& o16) {
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) {
+  for (int e = 0; e < W; e += 2) {
     const float2 x = __ffma2_rn(make_float2(v[e], v[e + 1]), cs2, nmu2);
     count_over<MON>(x, o32, o16);
     float2 p;
@@ -234,15 +256,18 @@ __device__ __forceinline__ void p_chunk32(const float* v, float2 cs2, float2 nmu
 }
 
 // ------------------------------------------------------------------------------------
-template <int D, int BC, int NQ, int MODE>
+template <int D, int BC, int NQ, int MODE, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
-  using C = Cfg<D, BC, NQ>;
+  using C = Cfg<D, BC, NQ, SPLIT>;
   constexpr int NS = C::kStages;
-  constexpr int HC = C::kHC;
-  constexpr int HD = C::kHD;
+  constexpr int CP = C::kCP;
+  constexpr int OP = C::kOP;
+  constexpr int NCH = C::kNCH;
+  constexpr int CW = C::kCW;
+  constexpr int kPoly = poly_pairs();
   using CtlT = Ctl<NS, NQ>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
 
@@ -260,9 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&ctl->q_full[t], 1);
       mbar_init(&ctl->s_full[t], 1);
-      mbar_init(&ctl->s_free[t], 8);
-      mbar_init(&ctl->p_full[t][0], 8);
-      mbar_init(&ctl->p_full[t][1], 8);
+      mbar_init(&ctl->s_free[t], C::kWarpsPerTile);
+      mbar_init(&ctl->p_full[t][0], C::kWarpsPerTile);
+      mbar_init(&ctl->p_full[t][1], C::kWarpsPerTile);
       mbar_init(&ctl->o_final[t], 1);
     }
     for (int s = 0; s < NS; ++s) {
@@ -380,16 +405,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       };
-      // P of half h occupies TMEM columns [h*HC, h*HC + HC/2) of S_t (packed bf16 pairs).
-      // PV chunk c: the K-steps over P columns [c*32, c*32 + 32) of both halves.
+      // P of part pp occupies TMEM columns [pp*CP, pp*CP + CP/2) of S_t (packed bf16 pairs).
+      // PV chunk c: the K-steps over P columns [c*CW, c*CW + CW) of every part.
       auto issue_pv_chunk = [&](int t, int st, int c, bool& first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        for (int pp = 0; pp < SPLIT; ++pp) {
 #pragma unroll
-          for (int k2 = 0; k2 < 2; ++k2) {
-            const int kk = hh * (HC / 16) + c * 2 + k2;  // K-step (16 key rows of V)
-            const uint32_t pcol = hh * HC + (c * 32 + k2 * 16) / 2;
+          for (int k2 = 0; k2 < CW / 16; ++k2) {
+            const int kk = pp * (CP / 16) + c * (CW / 16) + k2;  // K-step (16 key rows of V)
+            const uint32_t pcol = pp * CP + c * (CW / 2) + k2 * 8;
             if (elect_one())
               mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + pcol,
                      (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV, first ? 0u : 1u);
@@ -426,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool first = ((o_init >> t) & 1u) == 0;  // first PV of this tile initialises O
             bool skip = false;
 #pragma unroll
-            for (int c = 0; c < HC / 32; ++c) {
+            for (int c = 0; c < NCH; ++c) {
               mbar_wait(&ctl->p_full[t][c], (p_ph >> t) & 1u);
               tc_fence_after();
               if (c == 0) {
@@ -451,57 +476,88 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ============================ softmax WGs ============================
-    // WG w = warp/4: query tile t = w/2, column half hf = w%2. Each thread owns row r of
-    // its tile (TMEM lane r) and HC = BC/2 columns of every S tile and D/2 columns of O.
+    // Each row of a query tile is shared by SPLIT threads (TMEM lane r of SPLIT warpgroups),
+    // each owning CP = BC/SPLIT S columns and OP = D/SPLIT O columns.
+    //   SPLIT == 2: warpgroups 2t, 2t+1 serve query tile t only (two independent warp sets
+    //               that run in anti-phase, each hiding under the other tile's MMA window);
+    //   SPLIT == 4: all four warpgroups serve both tiles in turn (tile 0 then tile 1 of each
+    //               key block): half the per-thread work per tile-block, one shared issue stream.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-    const int t = warp >> 3;
-    const int hf = (warp >> 2) & 1;
-    const int r = tid & 127;
-    if (t < NQ) {
+    constexpr int NT = (SPLIT == 4) ? NQ : 1;  // query tiles this thread serves
+    const int part = (SPLIT == 4) ? (warp >> 2) : ((warp >> 2) & 1);
+    const int tile0 = (SPLIT == 4) ? 0 : (warp >> 3);
+    if (tile0 < NQ) {
+      const int r = tid & 127;
       VFA_ROLE_SETUP();
-      const int h = unit.h0 + t;
-      const int R = unit.qt * kBR + r;  // absolute query row
       const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t tS = tbase + C::s_off(t) + hf * HC + lane_off;  // this half's S columns
-      const uint32_t tO = tbase + C::kOBase + t * D + hf * HD + lane_off;
-      const uint32_t pair_bar = 1 + t;  // named barrier of the tile's two halves (256 threads)
+      const int R = unit.qt * kBR + r;  // absolute query row
       const float cs = a.c_scale;
-      float m2 = -INFINITY;  // running max, log2 units of scaled scores (identical in both halves)
-      float l = 0.f;         // this half's share of the normalizer
-      uint32_t s_ph = 0, xpar = 0;
+      float m2[NT], l[NT];  // running max (log2 units of scaled scores; identical in all parts)
+      uint32_t xpar[NT];    // and this part's share of the normalizer, per served tile
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti) {
+        m2[ti] = -INFINITY;
+        l[ti] = 0.f;
+        xpar[ti] = 0;
+      }
+      uint32_t s_ph = 0;  // bit ti: s_full phase
       uint32_t over32 = 0, over16 = 0;
-      // half-row max exchange: returns max(mine, other half's) for this row
-      auto exchange_max = [&](float mine) -> float {
-        ctl->xmax[t][xpar][hf][r] = mine;
-        named_bar_sync(pair_bar, 2 * kBR);
-        const float other = ctl->xmax[t][xpar][hf ^ 1][r];
-        xpar ^= 1;
-        return fmaxf(mine, other);
+      auto tS = [&](int t) { return tbase + C::s_off(t) + part * CP + lane_off; };
+      auto tO = [&](int t) { return tbase + C::kOBase + t * D + part * OP + lane_off; };
+      // row-max exchange across the SPLIT parts of a row (named barrier 1 + t)
+      auto exchange_max = [&](int ti, int t, float mine) -> float {
+        ctl->xmax[t][xpar[ti]][part][r] = mine;
+        named_bar_sync(1 + t, SPLIT * kBR);
+        const float* x = ctl->xmax[t][xpar[ti]][0];
+        float m = fmaxf(x[r], x[kBR + r]);
+        if constexpr (SPLIT == 4) m = fmaxf(m, fmaxf(x[2 * kBR + r], x[3 * kBR + r]));
+        xpar[ti] ^= 1;
+        return m;
+      };
+      auto wait_s = [&](int ti, int t) {
+        mbar_wait(&ctl->s_full[t], (s_ph >> ti) & 1u);
+        s_ph ^= 1u << ti;
+        tc_fence_after();
+      };
+      auto load_part = [&](int t, float* v) {
+        if constexpr (CP >= 32) {
+#pragma unroll
+          for (int c = 0; c < CP / 32; ++c) tmem_ld32(tS(t) + c * 32, v + c * 32);
+        } else {
+          tmem_ld16(tS(t), v);
+        }
+        tmem_wait_ld();
+        if constexpr (CP >= 32) {
+#pragma unroll
+          for (int c = 0; c < CP / 32; ++c) reg_fence32(v + c * 32);
+        } else {
+          reg_fence16(v);
+        }
       };
 
       // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
       if (nchunks > 0) {
-        float mx = -INFINITY;
+        float mx[NT];
+#pragma unroll
+        for (int ti = 0; ti < NT; ++ti) mx[ti] = -INFINITY;
         for (int ch = 0; ch < nchunks; ++ch) {
-          mbar_wait(&ctl->s_full[t], s_ph);
-          s_ph ^= 1;
-          tc_fence_after();
-          const int valid = nrep - ch * BC - hf * HC;
+          const int valid = nrep - ch * BC - part * CP;
 #pragma unroll
-          for (int c = 0; c < HC / 32; ++c) {
-            float v[32];
-            tmem_ld32(tS + c * 32, v);
-            tmem_wait_ld();
-            reg_fence32(v);
+          for (int ti = 0; ti < NT; ++ti) {
+            const int t = tile0 + ti;
+            wait_s(ti, t);
+            float v[CP];
+            load_part(t, v);
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c * 32 + e < valid) mx = fmaxf(mx, v[e]);
+            for (int e = 0; e < CP; ++e)
+              if (e < valid) mx[ti] = fmaxf(mx[ti], v[e]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->s_free[t]);
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->s_free[t]);
         }
-        m2 = exchange_max(mx) * cs;
+#pragma unroll
+        for (int ti = 0; ti < NT; ++ti) m2[ti] = exchange_max(ti, tile0 + ti, mx[ti]) * cs;
       }
 
       const float2 cs2 = make_float2(cs, cs);
@@ -510,158 +566,166 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int j = sched_block(sched, pos);
         const bool special = (MODE == kFA) || sched_is_special(sched, j);
         const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
-        const int lim = R - (j - 1) * BC - hf * HC;  // this half's columns > lim are masked
-        mbar_wait(&ctl->s_full[t], s_ph);
-        s_ph ^= 1;
-        tc_fence_after();
-        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
-        // this half's S row: all HC columns in registers behind a single TMEM wait
-        float v[HC];
+        const int lim = R - (j - 1) * BC - part * CP;  // this part's columns > lim are masked
 #pragma unroll
-        for (int c = 0; c < HC / 32; ++c) tmem_ld32(tS + c * 32, v + c * 32);
-        tmem_wait_ld();
+        for (int ti = 0; ti < NT; ++ti) {
+          const int t = tile0 + ti;
+          wait_s(ti, t);
+          if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
+          float v[CP];
+          load_part(t, v);
+          if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
 #pragma unroll
-        for (int c = 0; c < HC / 32; ++c) reg_fence32(v + c * 32);
-        if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
-#pragma unroll
-          for (int e = 0; e < HC; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
-        }
-        bool skipped = false;
-        if (MODE == kFA || MODE == kVSA || special) {
-          // ---- exact-update / skip-test block: rowmax over the full row (two halves,
-          //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
-          float mt = -INFINITY;
-#pragma unroll
-          for (int e = 0; e < HC; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
-          mt = exchange_max(mt);
-          const float mt2 = mt * cs;
-          const float m2n = fmaxf(m2, mt2);
-          if (MODE == kVSA) {
-            const bool below = (mt2 - m2n < a.log2_lambda) ||
-                               (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
-            skipped = named_bar_and(pair_bar, 2 * kBR, below);
+            for (int e = 0; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
           }
-          if (skipped) {
-            ++n_skipped;
-            n_skipped_special += special ? 1 : 0;
-          } else if (special) {
-            const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
-            m2 = m2n;
-            l = __fmul_rn(l, f);  // no FMA contraction: identical l-recurrence in every mode
-            // rescale this half of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
-            // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
-            const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
-            if (work) {
-              const float2 f2 = make_float2(f, f);
-#pragma unroll 1
-              for (int c = 0; c < HD / 16; ++c) {
-                float o[16];
-                tmem_ld16(tO + c * 16, o);
-                tmem_wait_ld();
-                reg_fence16(o);
-                uint32_t u[16];
+          bool skipped = false;
+          if (MODE == kFA || MODE == kVSA || special) {
+            // ---- exact-update / skip-test block: rowmax over the full row (four quarters,
+            //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
+            float mt = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < 16; e += 2) {
-                  const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
-                  u[e] = __float_as_uint(x.x);
-                  u[e + 1] = __float_as_uint(x.y);
+            for (int e = 0; e < CP; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
+            mt = exchange_max(ti, t, mt);
+            const float mt2 = mt * cs;
+            const float m2n = fmaxf(m2[ti], mt2);
+            if (MODE == kVSA) {
+              const bool below = (mt2 - m2n < a.log2_lambda) ||
+                                 (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
+              skipped = named_bar_and(1 + t, SPLIT * kBR, below);
+            }
+            if (skipped) {
+              ++n_skipped;
+              n_skipped_special += special ? 1 : 0;
+            } else if (special) {
+              const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
+              m2[ti] = m2n;
+              l[ti] = __fmul_rn(l[ti], f);  // no FMA contraction: identical l-recurrence in every mode
+              // rescale this part of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
+              // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
+              const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
+              if (work) {
+                const float2 f2 = make_float2(f, f);
+#pragma unroll(SPLIT == 4 ? 2 : 1)
+                for (int c = 0; c < OP / 16; ++c) {
+                  float o[16];
+                  tmem_ld16(tO(t) + c * 16, o);
+                  tmem_wait_ld();
+                  reg_fence16(o);
+                  uint32_t u[16];
+#pragma unroll
+                  for (int e = 0; e < 16; e += 2) {
+                    const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+                    u[e] = __float_as_uint(x.x);
+                    u[e + 1] = __float_as_uint(x.y);
+                  }
+                  tmem_st16(tO(t) + c * 16, u);
                 }
-                tmem_st16(tO + c * 16, u);
               }
             }
           }
-        }
-        // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
-        if (r == 0 && hf == 0) {
-          if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
-          if (a.skip_trace) {
-            const size_t idx = ((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos;
-            a.skip_trace[idx] = skipped ? 2 : 1;
+          // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
+          if (r == 0 && part == 0) {
+            if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
+            if (a.skip_trace) {
+              const size_t idx =
+                  ((static_cast<size_t>(unit.b) * a.Hq + unit.h0 + t) * a.Tr + unit.qt) * a.Tc + pos;
+              a.skip_trace[idx] = skipped ? 2 : 1;
+            }
           }
-        }
-        if (!skipped) {
-          // P = exp2(S*c - m2) chunk by chunk; each 32-column chunk is handed to the MMA warp
-          // as soon as it is in TMEM, so PV of chunk 0 runs under the softmax of chunk 1
-          const float2 nmu2 = make_float2(m2 == -INFINITY ? 0.f : -m2, m2 == -INFINITY ? 0.f : -m2);
-          float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          if (!skipped) {
+            // P = exp2(S*c - m2) in CW-column chunks; each chunk is handed to the MMA warp as
+            // soon as it is in TMEM (PV of chunk 0 overlaps the softmax of chunk 1)
+            const float nm = m2[ti] == -INFINITY ? 0.f : -m2[ti];
+            const float2 nmu2 = make_float2(nm, nm);
+            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-          for (int c = 0; c < HC / 32; ++c) {
-            uint32_t u[16];
-            if (a.monitor)
-              p_chunk32<true, kPolyPairs>(v + c * 32, cs2, nmu2, u, acc, over32, over16);
-            else
-              p_chunk32<false, kPolyPairs>(v + c * 32, cs2, nmu2, u, acc, over32, over16);
-            tmem_st16(tS + c * 16, u);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
-          }
-          l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
-        } else {
-          __syncwarp();
-          if (lane == 0)
-            for (int c = 0; c < HC / 32; ++c) mbar_arrive(&ctl->p_full[t][c]);
-        }
-        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
-      }
-      const int n_special = (MODE == kVSA) ? sched.n_spec - n_skipped_special : sched.n_spec;
-      const int n_frozen = N - sched.n_spec - ((MODE == kVSA) ? n_skipped - n_skipped_special : 0);
-
-      // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l; l = l_lo + l_hi
-      ctl->xl[t][hf][r] = l;
-      named_bar_sync(pair_bar, 2 * kBR);
-      const float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
-      mbar_wait(&ctl->o_final[t], 0);
-      tc_fence_after();
-      const float inv = 1.0f / lsum;
-      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr + hf * HD;
-      bool finite = true;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        float v[32];
-        tmem_ld32(tO + c * 32, v);
-        tmem_wait_ld();
-        reg_fence32(v);
-        uint32_t u[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
-          finite = finite && isfinite(o0) && isfinite(o1);
-          u[e >> 1] = pack_bf16x2(o0, o1);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(u[4 * q4], u[4 * q4 + 1], u[4 * q4 + 2], u[4 * q4 + 3]);
-      }
-      const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
-      const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
-      if (hf == 0 && a.lse) a.lse[lrow] = (m2 + __log2f(lsum)) * kLn2;
-      if (a.status) {
-        if (hf == 0 && lsum == 0.f) {
-          if (m2 == -INFINITY) {
-            atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
-            atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
+            for (int c = 0; c < NCH; ++c) {
+              uint32_t u[CW / 2];
+              if (a.monitor)
+                p_chunk<CW, true, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
+              else
+                p_chunk<CW, false, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
+              if constexpr (CW == 32) tmem_st16(tS(t) + c * 16, u);
+              else tmem_st8(tS(t) + c * 8, u);
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
+            }
+            l[ti] = __fadd_rn(l[ti], __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
           } else {
-            atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
-            atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+            __syncwarp();
+            if (lane == 0)
+              for (int c = 0; c < NCH; ++c) mbar_arrive(&ctl->p_full[t][c]);
           }
-        }
-        // a row is non-finite if either half is: combine through smem, count it once
-        ctl->xfin[t][hf][r] = finite ? 1u : 0u;
-        named_bar_sync(pair_bar, 2 * kBR);
-        if (hf == 0 && !(ctl->xfin[t][0][r] && ctl->xfin[t][1][r])) {
-          atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
-          atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+          if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
         }
       }
+      const int n_special = NT * sched.n_spec - n_skipped_special;
+      const int n_frozen = NT * (N - sched.n_spec) - (n_skipped - n_skipped_special);
+
+      // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l; l = sum over the parts
+      bool any_nonfinite = false;
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti) {
+        const int t = tile0 + ti;
+        const int h = unit.h0 + t;
+        ctl->xl[t][part][r] = l[ti];
+        named_bar_sync(1 + t, SPLIT * kBR);
+        float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
+        if constexpr (SPLIT == 4) lsum = __fadd_rn(lsum, __fadd_rn(ctl->xl[t][2][r], ctl->xl[t][3][r]));
+        mbar_wait(&ctl->o_final[t], 0);
+        tc_fence_after();
+        const float inv = 1.0f / lsum;
+        __nv_bfloat16* orow =
+            a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr + part * OP;
+        bool finite = true;
+#pragma unroll
+        for (int c = 0; c < OP / 16; ++c) {
+          float v[16];
+          tmem_ld16(tO(t) + c * 16, v);
+          tmem_wait_ld();
+          reg_fence16(v);
+          uint32_t u[8];
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
+            finite = finite && isfinite(o0) && isfinite(o1);
+            u[e >> 1] = pack_bf16x2(o0, o1);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+          dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+        }
+        const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
+        const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
+        if (part == 0 && a.lse) a.lse[lrow] = (m2[ti] + __log2f(lsum)) * kLn2;
+        if (a.status) {
+          if (part == 0 && lsum == 0.f) {
+            if (m2[ti] == -INFINITY) {
+              atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
+              atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
+            } else {
+              atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
+              atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+            }
+          }
+          // a row is non-finite if any part is: combine through smem, count it once
+          ctl->xfin[t][part][r] = finite ? 1 : 0;
+          named_bar_sync(1 + t, SPLIT * kBR);
+          bool row_ok = ctl->xfin[t][0][r] && ctl->xfin[t][1][r];
+          if constexpr (SPLIT == 4) row_ok = row_ok && ctl->xfin[t][2][r] && ctl->xfin[t][3][r];
+          if (part == 0 && !row_ok) any_nonfinite = true, atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+        }
+      }
+      if (any_nonfinite) atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
       if (a.stats) {
         if (a.monitor) {
           atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
           atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
         }
-        if (r == 0 && hf == 0) {
-          atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
+        if (r == 0 && part == 0) {
+          atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(NT * N));
           atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
           atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_special));
           atomicAdd(&a.stats[VFA_STAT_FROZEN], static_cast<unsigned long long>(n_frozen));
@@ -797,11 +861,11 @@ int64_t n_reprs(const VfaParams* p) {
   return (p->tc1 > 0 && p->tc1 < tc) ? p->tc1 : tc;
 }
 
-template <int D, int BC, int NQ, int MODE>
+template <int D, int BC, int NQ, int MODE, int SPLIT>
 int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
-  using C = vfa::Cfg<D, BC, NQ>;
-  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE>;
+  using C = vfa::Cfg<D, BC, NQ, SPLIT>;
+  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -822,16 +886,32 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
   return VFA_OK;
 }
 
+// Softmax column split per variant (params.softmax_split = 0), measured best on B200
+// (profiles/ab_r01_split.txt): VFA's frozen blocks need no cross-thread exchange, so all
+// warps serving both tiles wins; FA / VSA exchange a row max on every block, which per-tile
+// warp sets overlap with the other tile's work. One query tile per CTA: always 4.
+constexpr int default_split(int variant) {
+  return variant == VFA_VARIANT_FA ? VFA_SPLIT_FA : (variant == VFA_VARIANT_VFA ? VFA_SPLIT_VFA : VFA_SPLIT_VSA);
+}
+
+template <int D, int BC, int NQ, int MODE>
+int dispatch_split(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                   const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
+  const int split = p->softmax_split ? p->softmax_split : default_split(p->variant);
+  if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
+  return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
+}
+
 template <int D, int BC, int NQ>
 int dispatch_mode(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                   const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
   switch (p->variant) {
     case VFA_VARIANT_FA:
-      return launch_fwd<D, BC, NQ, vfa::kFA>(p, mq, mk, mv, mr, args, st);
+      return dispatch_split<D, BC, NQ, vfa::kFA>(p, mq, mk, mv, mr, args, st);
     case VFA_VARIANT_VFA:
-      return launch_fwd<D, BC, NQ, vfa::kVFA>(p, mq, mk, mv, mr, args, st);
+      return dispatch_split<D, BC, NQ, vfa::kVFA>(p, mq, mk, mv, mr, args, st);
     default:
-      return launch_fwd<D, BC, NQ, vfa::kVSA>(p, mq, mk, mv, mr, args, st);
+      return dispatch_split<D, BC, NQ, vfa::kVSA>(p, mq, mk, mv, mr, args, st);
   }
 }
 
@@ -887,6 +967,8 @@ int vfa_check_params(const VfaParams* p) {
   if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
   if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
   if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
+  if (p->softmax_split != 0 && p->softmax_split != 2 && p->softmax_split != 4)
+    return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 2 or 4");
   if (p->variant == VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
   if (p->batch < 1 || p->heads_q < 1 || p->heads_kv < 1 || p->seq_q < 1 || p->seq_k < 1)
     return fail(VFA_ERR_DATA, "all dimensions must be >= 1");

@@ -203,22 +203,44 @@ def test_vsa_skip_decisions(lam):
         assert np.abs(_f64(out) - ref_o).max() <= O_ABS
 
 
-def test_vsa_tiny_lambda_bitwise_equals_vfa():
-    # reference tests/test_sparse.py:148-153 on the device path
+@pytest.mark.parametrize("split", [2, 4])
+def test_vsa_tiny_lambda_bitwise_equals_vfa(split):
+    # reference tests/test_sparse.py:148-153 on the device path (same softmax layout)
     q, k, v = _rand((1, 4, 1024, 128), 51), _rand((1, 2, 1024, 128), 52), _rand((1, 2, 1024, 128), 53)
-    base = dict(causal=True, q_block=128, k_block=128)
+    base = dict(causal=True, q_block=128, k_block=128, softmax_split=split)
     o1, l1, _, _ = _run_gpu(q, k, v, variant="vfa", **base)
     o2, l2, _, st = _run_gpu(q, k, v, variant="vsa", lam=1e-9, **base)
     assert st["skipped"] == 0
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
-def test_single_key_block_vfa_equals_fa():
+@pytest.mark.parametrize("split", [2, 4])
+def test_single_key_block_vfa_equals_fa(split):
     # reference tests/test_vfa.py:115-125: T_c = 1 -> the one block is special
     q, k, v = _rand((1, 2, 128, 64), 61), _rand((1, 1, 128, 64), 62), _rand((1, 1, 128, 64), 63)
-    o1, l1, _, _ = _run_gpu(q, k, v, variant="fa", causal=True)
-    o2, l2, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True, use_m_init=False)
+    o1, l1, _, _ = _run_gpu(q, k, v, variant="fa", causal=True, softmax_split=split)
+    o2, l2, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True, use_m_init=False, softmax_split=split)
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa"])
+@pytest.mark.parametrize("d,bc", [(128, 128), (64, 64), (128, 64), (64, 128)])
+def test_softmax_splits_agree_with_oracle(variant, d, bc):
+    # both softmax layouts (2 or 4 threads per row) against the oracle, and the per-variant
+    # default is one of them
+    B, Hq, Hkv, L = 1, 4, 2, 512
+    q, k, v = _rand((B, Hq, L, d), 111), _rand((B, Hkv, L, d), 112), _rand((B, Hkv, L, d), 113)
+    kw = dict(variant=variant, causal=True, q_block=128, k_block=bc)
+    if variant == "vsa":
+        kw["lam"] = 1e-2
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    outs = {}
+    for split in (0, 2, 4):
+        out, lse, _, st = _run_gpu(q, k, v, softmax_split=split, **kw)
+        _compare(out, lse, ref_o, ref_lse, f"{kw} split={split}")
+        assert st["visited"] == ref_st["visited"]
+        outs[split] = out
+    assert torch.equal(outs[0], outs[2]) or torch.equal(outs[0], outs[4])
 
 
 def test_deterministic_and_head_sharding_invariant():
