@@ -48,6 +48,10 @@ extern "C" {
 #define VFA_VARIANT_FA 0  /* fa_forward: rescale every block, ascending order */
 #define VFA_VARIANT_VFA 1 /* vfa_forward: m-init + sink/local reorder + frozen max */
 #define VFA_VARIANT_VSA 2 /* vsa_forward: VFA + BLASST block skip */
+/* the BLASST family, src/sparse.py:112-253 (m0 = -inf, every block exact, no m-init) */
+#define VFA_VARIANT_BLASST 3         /* blasst_forward: order = reorder ? sink_local : sequential */
+#define VFA_VARIANT_BLASST_FA4 4     /* blasst_fa4_forward: + rescale elision (params.tau) */
+#define VFA_VARIANT_BLASST_ROWSKIP 5 /* blasst_rowskip_forward: row-granular threshold */
 
 /* key representation kind: KEY_REPRS, src/vfa.py:39 */
 #define VFA_KREPR_SABSMAX 0
@@ -62,6 +66,8 @@ extern "C" {
 #define VFA_STAT_FROZEN 3         /* processed with the frozen max */
 #define VFA_STAT_OVER_F32 4       /* monitor: exp args > 88.7228 (OverflowMonitor) */
 #define VFA_STAT_OVER_F16 5       /* monitor: exp args > ln(65504) */
+#define VFA_STAT_ELIDED 6         /* BLASST-FA4: SkipStats.rescales_elided */
+#define VFA_STAT_ROWS_MASKED 7    /* BLASST rowskip: SkipStats.rows_masked */
 #define VFA_STAT_COUNT 8
 
 /* status[] slots (uint32, device; initialised by vfa_fwd when non-NULL) */
@@ -84,7 +90,7 @@ typedef struct VfaParams {
   int32_t variant;      /* VFA_VARIANT_* */
   int32_t kind;         /* VFA_KREPR_* */
   int32_t qkind;        /* 0 = row_wise (the only query representation on the GPU path) */
-  int32_t reorder;      /* vfa_forward(reorder=...) */
+  int32_t reorder;      /* vfa_forward(reorder=...); BLASST: 1 = order 'sink_local' */
   int32_t use_m_init;   /* vfa_forward(use_m_init=...) */
   int32_t tc1;          /* representations for key blocks 1..tc1; 0 = all (src/vfa.py:79-88) */
   int32_t n_sink;       /* sink blocks taking the exact update (reference: 1) */
@@ -94,6 +100,7 @@ typedef struct VfaParams {
   int32_t krepr_precomputed; /* 1: workspace already holds vfa_krepr() output for this K; skip recomputing */
   int32_t softmax_split; /* threads sharing one row of a query tile: 0 = per-variant default,
                            2 = per-tile warp sets, 4 = all softmax warps serve both tiles */
+  double tau;           /* BLASST-FA4 rescale elision: max increase <= tau * ln 2 (SkipConfig.tau) */
 } VfaParams;
 
 /* Host-only validation (no GPU needed). Returns VFA_OK or VFA_ERR_CONFIG / VFA_ERR_DATA. */

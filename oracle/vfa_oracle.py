@@ -229,17 +229,24 @@ class HeadResult:
     # per q-block list of (block j, skipped?, margin) in visit order (VSA only)
     decisions: list = field(default_factory=list)
     error: Exception | None = None
+    elided: int = 0       # BLASST-FA4: processed blocks whose rescale was elided
+    rows_masked: int = 0  # BLASST rowskip: suppressed row slots (skipped blocks count all rows)
 
 
-VARIANTS = ("fa", "vfa", "vsa")
+VARIANTS = ("fa", "vfa", "vsa", "blasst", "blasst_fa4", "blasst_rowskip")
+BLASST_VARIANTS = ("blasst", "blasst_fa4", "blasst_rowskip")
 
 
 def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
                  scale=None, kind="sabsmax", qkind="row_wise", reorder=True,
-                 use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None,
-                 raise_errors=True, record_decisions=False, q_blocks=None) -> HeadResult:
-    """One head of fa_forward (src/fa.py:28-61), vfa_forward (src/vfa.py:156-223) or
-    vsa_forward (src/sparse.py:256-329), float64, returning O, LSE and visit statistics.
+                 use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None, tau=0.0,
+                 order="sequential", raise_errors=True, record_decisions=False,
+                 q_blocks=None) -> HeadResult:
+    """One head of fa_forward (src/fa.py:28-61), vfa_forward (src/vfa.py:156-223),
+    vsa_forward (src/sparse.py:256-329) or the BLASST family -- blasst_forward (order
+    'sequential' | 'sink_local', src/sparse.py:112-152), blasst_fa4_forward (tau rescale
+    elision, :155-203), blasst_rowskip_forward (row-granular, :206-253) -- float64,
+    returning O, LSE and visit statistics.
 
     q_blocks: optional iterable of 1-based query blocks to compute (the others are left
     NaN); used to time bounded samples of large problems. Query blocks are independent
@@ -263,9 +270,19 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
         reorder, use_m_init, n_sink = False, False, 0
     if variant == "vsa":
         reorder, use_m_init = True, True  # src/sparse.py:288-290
-    ln_lam = NEG_INF if (variant != "vsa" or lam is None) else math.log(lam)
-    if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
+    if variant in BLASST_VARIANTS:
+        if variant == "blasst" and order not in ("sequential", "sink_local"):
+            raise ValueError(f"unknown order {order!r}")  # src/sparse.py:121-122
+        # m0 = -inf, every visited block takes the exact update; only blasst may reorder
+        reorder = variant == "blasst" and order == "sink_local"
+        use_m_init, n_sink, n_local = False, 1, 1
+    skipping = variant in ("vsa", "blasst", "blasst_fa4", "blasst_rowskip")
+    ln_lam = NEG_INF if (not skipping or lam is None) else math.log(lam)
+    if skipping and lam is not None and not (0.0 < lam <= 1.0):
         raise ValueError(f"lambda must be in (0, 1], got {lam}")
+    if tau < 0:
+        raise ValueError(f"tau must be >= 0, got {tau}")  # src/sparse.py:52-53
+    tau_ln2 = tau * math.log(2.0)
     t_r, t_c = nq // qb, nk // kb
     out = np.full((nq, d), np.nan)
     lse = np.full(nq, np.nan)
@@ -275,10 +292,14 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
     for i in (range(1, t_r + 1) if q_blocks is None else q_blocks):
         vmax = visible_key_blocks(i, qb, kb, t_c, causal)
         local = local_key_block(i, qb, kb, t_c)
-        if variant == "fa":
-            order, special = tuple(range(1, vmax + 1)), frozenset(range(1, vmax + 1))
+        if variant in ("fa", "blasst", "blasst_fa4", "blasst_rowskip"):
+            if reorder:  # blasst order='sink_local': the VFA visit order, every block exact
+                visit, _ = build_schedule(i, vmax, local, True, n_sink, n_local)
+            else:
+                visit = tuple(range(1, vmax + 1))
+            special = frozenset(range(1, vmax + 1))
         else:
-            order, special = build_schedule(i, vmax, local, reorder, n_sink, n_local)
+            visit, special = build_schedule(i, vmax, local, reorder, n_sink, n_local)
         qi = q[(i - 1) * qb: i * qb]
         if use_m_init:
             m = m_init(qi, kreprs[: min(vmax, len(kreprs))], scale, qkind)
@@ -287,7 +308,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
         l = np.zeros(qb)
         o = np.zeros((qb, d))
         dec = []
-        for j in order:
+        for j in visit:
             s = tile_scores(q, k, scale, causal, i, j, qb, kb)
             v_j = v[(j - 1) * kb: j * kb]
             res.visited += 1
@@ -295,12 +316,43 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
             if need_max:
                 m_tilde = s.max(axis=1)
                 m_new = np.maximum(m, m_tilde)
-            if variant == "vsa":
+            if variant == "blasst_rowskip":  # src/sparse.py:223-249
+                with np.errstate(invalid="ignore"):
+                    keep = (m_tilde - m_new) >= ln_lam
+                if ln_lam == NEG_INF:
+                    keep = np.ones(qb, dtype=bool)
+                if record_decisions:
+                    dec.append((j, not keep.any(), _skip_margin(m_tilde, m_new, ln_lam)))
+                if not keep.any():
+                    res.skipped += 1
+                    res.rows_masked += qb
+                    continue
+                f = np.where(keep, _rescale_factor(m, m_new), 1.0)
+                s_kept = np.where(keep[:, None], s, NEG_INF)
+                p_t = np.exp(_exp_args(s_kept, m_new))
+                l = f * l + _rowsum(p_t)
+                o = f[:, None] * o + p_t @ v_j
+                m = np.where(keep, m_new, m)
+                res.special += 1
+                res.rows_masked += qb - int(keep.sum())
+                continue
+            if skipping:
                 skip = _tile_skippable(m_tilde, m_new, ln_lam)
                 if record_decisions:
                     dec.append((j, skip, _skip_margin(m_tilde, m_new, ln_lam)))
                 if skip:
                     res.skipped += 1
+                    continue
+            if variant == "blasst_fa4":  # src/sparse.py:185-199
+                prev_finite = not np.isneginf(m).any()
+                if prev_finite and float(np.max(m_new - m)) <= tau_ln2:
+                    args = _exp_args(s, m)
+                    with np.errstate(over="ignore"):
+                        p_t = np.exp(args)
+                    l = l + _rowsum(p_t)
+                    o = o + p_t @ v_j
+                    res.frozen += 1
+                    res.elided += 1
                     continue
             if j in special:
                 args = _exp_args(s, m_new)
@@ -364,9 +416,11 @@ def forward(q, k, v, **kw):
 
 
 def _stats(results):
-    st = {"visited": 0, "skipped": 0, "special": 0, "frozen": 0,
+    st = {"visited": 0, "skipped": 0, "special": 0, "frozen": 0, "elided": 0, "rows_masked": 0,
           "count_over_f16": 0, "count_over_f32": 0, "exp_arg_max": NEG_INF}
     for r in results:
+        st["elided"] += r.elided
+        st["rows_masked"] += r.rows_masked
         st["visited"] += r.visited
         st["skipped"] += r.skipped
         st["special"] += r.special

@@ -22,11 +22,12 @@ VFA_ERR_DATA = 3
 VFA_ERR_NUMERICAL = 4
 VFA_ERR_CUDA = 5
 
-VARIANTS = {"fa": 0, "vfa": 1, "vsa": 2}
+VARIANTS = {"fa": 0, "vfa": 1, "vsa": 2, "blasst": 3, "blasst_fa4": 4, "blasst_rowskip": 5}
 KEY_REPRS = ("sabsmax", "k_max", "k_mean", "k_absmax_unsigned")  # src/vfa.py:39
 QUERY_REPRS = ("row_wise", "q_absmax", "q_sabsmax", "q_mean")  # src/vfa.py:40
 
-STAT_VISITED, STAT_SKIPPED, STAT_SPECIAL, STAT_FROZEN, STAT_OVER_F32, STAT_OVER_F16 = range(6)
+(STAT_VISITED, STAT_SKIPPED, STAT_SPECIAL, STAT_FROZEN, STAT_OVER_F32, STAT_OVER_F16, STAT_ELIDED,
+ STAT_ROWS_MASKED) = range(8)
 STAT_COUNT = 8
 STATUS_FLAGS, STATUS_UNDERFLOW_ROW, STATUS_MASKED_ROW, STATUS_NONFINITE_ROWS = range(4)
 STATUS_COUNT = 4
@@ -52,6 +53,7 @@ class VfaParams(ctypes.Structure):
         ("n_sink", ctypes.c_int32), ("n_local", ctypes.c_int32), ("monitor", ctypes.c_int32),
         ("lam", ctypes.c_double),
         ("krepr_precomputed", ctypes.c_int32), ("softmax_split", ctypes.c_int32),
+        ("tau", ctypes.c_double),
     ]
 
 

@@ -240,6 +240,59 @@ class OpCounters:
         self.blocks_processed += full + frozen
         self.blocks_skipped += skipped
 
+    @classmethod
+    def from_stats(cls, variant: str, st: dict, q: int, k: int, d: int) -> "OpCounters":
+        """Counters of a whole pass from its per-class block counts (device stats or oracle
+        results: visited / skipped / special / frozen / elided / rows_masked), charged
+        exactly as the reference variant charges each block."""
+        c = cls()
+        if variant == "blasst_rowskip":
+            skipped_rows = st["skipped"] * q
+            kept = st["special"] * q - (st["rows_masked"] - skipped_rows)
+            c.charge(0, 0, st["skipped"], q, k, d, False)
+            c.charge_rowskip(st["special"], kept, q, k, d)
+            c.rows_masked += skipped_rows  # src/sparse.py:232-233
+        elif variant == "blasst_fa4":
+            c.charge(st["special"], 0, st["skipped"], q, k, d, False)
+            c.charge_elided(st["elided"], q, k, d)
+        else:
+            c.charge(st["special"], st["frozen"], st["skipped"], q, k, d, variant == "vsa")
+        return c
+
+    def charge_elided(self, n: int, q: int, k: int, d: int):
+        """n * charge_elided_block (src/counters.py:102-114)."""
+        qk = q * k
+        self.mul_scale += n * qk
+        self.max_rowreduce += n * qk
+        self.max_running += n * q
+        self.sub_broadcast += n * qk
+        self.exp_evals += n * qk
+        self.sum_rowreduce += n * qk
+        self.mad_l += n * q
+        self.tensor_macs += n * 2 * qk * d
+        self.rowmax_reductions += n
+        self.rescales_elided += n
+        self.blocks_processed += n
+
+    def charge_rowskip(self, n: int, kept: int, q: int, k: int, d: int):
+        """Sum of charge_rowskip_block (src/counters.py:116-131) over n processed blocks that
+        kept `kept` rows in total (the charge is linear in kept)."""
+        qk = q * k
+        self.mul_scale += n * qk
+        self.max_rowreduce += n * qk
+        self.max_running += n * q
+        self.sub_broadcast += kept * k
+        self.exp_evals += kept * k + kept
+        self.sum_rowreduce += kept * k
+        self.mad_l += n * q
+        self.rescale_mul_l += kept
+        self.rescale_mul_O += kept * d
+        self.tensor_macs += n * 2 * qk * d
+        self.rowmax_reductions += n
+        self.rescale_events += n
+        self.rows_masked += n * q - kept
+        self.blocks_processed += n
+
 
 @dataclass
 class OverflowMonitor:
@@ -273,7 +326,7 @@ def _strides(x):
 
 
 def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind, reorder,
-            use_m_init, tc1, n_sink, n_local, lam, monitor, softmax_split=0):
+            use_m_init, tc1, n_sink, n_local, lam, monitor, softmax_split=0, tau=0.0):
     if kind not in _lib.KEY_REPRS:
         raise ValueError(f"unknown key representation {kind!r}")
     if qkind not in _lib.QUERY_REPRS:
@@ -297,6 +350,7 @@ def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind
     p.n_sink, p.n_local = int(n_sink), int(n_local)
     p.monitor = int(bool(monitor))
     p.lam = float(lam) if lam is not None else 0.0
+    p.tau = float(tau)
     p.softmax_split = int(softmax_split)
     return p
 
@@ -310,7 +364,7 @@ def _raise_for(rc):
 
 def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128, scale=None,
                       kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
-                      n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
+                      n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None, lse=None,
                       check=True, skip_trace=False, stream=None, workspace=None,
                       krepr_precomputed=False, softmax_split=0):
     """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
@@ -321,20 +375,26 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     FullyMaskedRowError / NormalizerUnderflowError raised like src/core.py:101-109.
     workspace: optional uint8 device buffer (>= vfa_workspace_bytes) holding the key-block
     representations; with krepr_precomputed=True they are reused instead of recomputed.
+    variant: fa | vfa | vsa | blasst | blasst_fa4 | blasst_rowskip. reorder selects the
+    sink/local-first visit order (VFA / VSA; for blasst it is order='sink_local', so pass
+    reorder=False for the reference's default sequential blasst). lam: skip threshold of the
+    skipping variants; tau: blasst_fa4 rescale-elision threshold (SkipConfig.tau).
     softmax_split: 0 (per-variant default), 2 or 4 threads per row of a query tile (a layout
     choice: results are within tolerance of each other, bitwise-stable for a fixed split).
     """
     if variant not in _lib.VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
-    if variant == "vsa" and lam is not None and not (0.0 < lam <= 1.0):
+    if variant not in ("fa", "vfa") and lam is not None and not (0.0 < lam <= 1.0):
         raise ValueError(f"lambda must be in (0, 1], got {lam}")
+    if not tau >= 0:
+        raise ValueError(f"tau must be >= 0, got {tau}")
     if all(isinstance(x, torch.Tensor) and x.device.type == "cpu" for x in (q, k, v)):
         if skip_trace or krepr_precomputed or workspace is not None:
             raise ValueError("skip_trace / krepr_precomputed / workspace need device-resident inputs")
         return attention_forward_host(q, k, v, variant=variant, causal=causal, q_block=q_block,
                                       k_block=k_block, scale=scale, kind=kind, qkind=qkind,
                                       reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
-                                      n_local=n_local, lam=lam, monitor=monitor, out=out, lse=lse,
+                                      n_local=n_local, lam=lam, tau=tau, monitor=monitor, out=out, lse=lse,
                                       check=check, stream=stream, softmax_split=softmax_split)
     lib = _lib.load()
     for name, x in (("q", q), ("k", k), ("v", v)):
@@ -350,7 +410,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
                 tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
-                softmax_split=softmax_split)
+                softmax_split=softmax_split, tau=tau)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)
@@ -385,7 +445,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
 
 def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
                            scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True,
-                           tc1=None, n_sink=1, n_local=1, lam=None, monitor=False, out=None, lse=None,
+                           tc1=None, n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None,
+                           lse=None,
                            check=True, stream=None, device=None, chunk_kv_heads=1, softmax_split=0):
     """The forward on HOST tensors (bf16 [B, Hq, Lq, d] / [B, Hkv, Lk, d], contiguous;
     page-locked for full overlap) -> host (O bf16, LSE fp32, info), through the C ABI's
@@ -415,7 +476,7 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
                 tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
-                softmax_split=softmax_split)
+                softmax_split=softmax_split, tau=tau)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)
@@ -454,6 +515,7 @@ def stats_dict(info) -> dict:
     s = info["stats"].cpu().tolist()
     return {"visited": s[_lib.STAT_VISITED], "skipped": s[_lib.STAT_SKIPPED],
             "special": s[_lib.STAT_SPECIAL], "frozen": s[_lib.STAT_FROZEN],
+            "elided": s[_lib.STAT_ELIDED], "rows_masked": s[_lib.STAT_ROWS_MASKED],
             "count_over_f32": s[_lib.STAT_OVER_F32], "count_over_f16": s[_lib.STAT_OVER_F16],
             "nonfinite_rows": int(info["status"].cpu()[_lib.STATUS_NONFINITE_ROWS])}
 
@@ -473,11 +535,8 @@ def _run(p: AttentionProblem, variant, **kw):
     return out, lse, st
 
 
-def _counters(st, p: AttentionProblem, frozen_rowmax: bool) -> OpCounters:
-    c = OpCounters()
-    c.charge(st["special"], st["frozen"], st["skipped"], p.blocks.q_block, p.blocks.k_block,
-             p.blocks.head_dim, frozen_rowmax)
-    return c
+def _counters(st, p: AttentionProblem, variant: str) -> OpCounters:
+    return OpCounters.from_stats(variant, st, p.blocks.q_block, p.blocks.k_block, p.blocks.head_dim)
 
 
 def _monitor(st, monitor: bool) -> OverflowMonitor:
@@ -497,7 +556,7 @@ def fa_forward(p: AttentionProblem, order_hook=None):
     if order_hook is not None:
         raise ValueError("order_hook is not supported by the GPU fa_forward")
     out, lse, st = _run(p, "fa")
-    return ForwardResult((out, _counters(st, p, False), None), lse, st)
+    return ForwardResult((out, _counters(st, p, "fa"), None), lse, st)
 
 
 def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True,
@@ -515,7 +574,7 @@ def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True
         raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
     out, lse, st = _run(p, "vfa", kind=kind, reorder=reorder, use_m_init=use_m_init, qkind=qkind,
                         tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor)
-    return ForwardResult((out, _counters(st, p, False), None, _monitor(st, monitor)), lse, st)
+    return ForwardResult((out, _counters(st, p, "vfa"), None, _monitor(st, monitor)), lse, st)
 
 
 def vsa_forward(p: AttentionProblem, cfg: SkipConfig, kind: str = "sabsmax", qkind: str = "row_wise",
@@ -535,7 +594,51 @@ def vsa_forward(p: AttentionProblem, cfg: SkipConfig, kind: str = "sabsmax", qki
     stats = SkipStats(blocks_visited=st["visited"], blocks_skipped=st["skipped"],
                       blocks_processed=st["special"] + st["frozen"],
                       processed_special=st["special"], processed_frozen=st["frozen"])
-    return ForwardResult((out, _counters(st, p, True), stats, _monitor(st, monitor)), lse, st)
+    return ForwardResult((out, _counters(st, p, "vsa"), stats, _monitor(st, monitor)), lse, st)
+
+
+def _skip_stats(st, qb, row_slots=False) -> SkipStats:
+    return SkipStats(blocks_visited=st["visited"], blocks_skipped=st["skipped"],
+                     rows_masked=st["rows_masked"], row_slots=st["visited"] * qb if row_slots else 0,
+                     rescales_elided=st["elided"], blocks_processed=st["special"] + st["frozen"])
+
+
+def blasst_forward(p: AttentionProblem, cfg: SkipConfig, order: str = "sequential"):
+    """Threshold block skipping on the baseline recurrence (src/sparse.py:112-152).
+
+    order='sink_local' visits the sink and local blocks first (the VFA order) with the
+    skip rule unchanged. Returns (O, counters, SkipStats) with `.lse`.
+    """
+    if cfg.granularity != "block":
+        raise ValueError("blasst_forward requires block granularity")
+    if order not in ("sequential", "sink_local"):
+        raise ValueError(f"unknown order {order!r}")
+    out, lse, st = _run(p, "blasst", lam=cfg.lam, reorder=order == "sink_local")
+    b = p.blocks
+    c = OpCounters.from_stats("blasst", st, b.q_block, b.k_block, b.head_dim)
+    return ForwardResult((out, c, _skip_stats(st, b.q_block)), lse, st)
+
+
+def blasst_fa4_forward(p: AttentionProblem, cfg: SkipConfig):
+    """Block skipping plus rescale elision when no row max rises by more than tau*ln2
+    (src/sparse.py:155-203). Returns (O, counters, SkipStats) with `.lse`."""
+    if cfg.granularity != "block":
+        raise ValueError("blasst_fa4_forward requires block granularity")
+    out, lse, st = _run(p, "blasst_fa4", lam=cfg.lam, tau=cfg.tau)
+    b = p.blocks
+    c = OpCounters.from_stats("blasst_fa4", st, b.q_block, b.k_block, b.head_dim)
+    return ForwardResult((out, c, _skip_stats(st, b.q_block)), lse, st)
+
+
+def blasst_rowskip_forward(p: AttentionProblem, cfg: SkipConfig):
+    """Row-granular thresholding: suppressed rows contribute zero mass
+    (src/sparse.py:206-253). Returns (O, counters, SkipStats) with `.lse`."""
+    if cfg.granularity != "row":
+        raise ValueError("blasst_rowskip_forward requires row granularity")
+    out, lse, st = _run(p, "blasst_rowskip", lam=cfg.lam)
+    b = p.blocks
+    c = OpCounters.from_stats("blasst_rowskip", st, b.q_block, b.k_block, b.head_dim)
+    return ForwardResult((out, c, _skip_stats(st, b.q_block, row_slots=True)), lse, st)
 
 
 def precompute_kreprs(p: AttentionProblem, kind: str, tc1: int | None = None) -> torch.Tensor:

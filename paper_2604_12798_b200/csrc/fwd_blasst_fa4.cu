@@ -1,0 +1,9 @@
+// vfa_fwd_kernel instantiations for variant blasst_fa4 (vfa::kBL4); see vfa_kernel.cuh.
+#include "fwd_dispatch.cuh"
+
+namespace vfa_host {
+int launch_blasst_fa4(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                     const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
+  return launch_mode<vfa::kBL4>(p, nq, mq, mk, mv, mr, a, st);
+}
+}  // namespace vfa_host

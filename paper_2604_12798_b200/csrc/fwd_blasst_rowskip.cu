@@ -1,0 +1,9 @@
+// vfa_fwd_kernel instantiations for variant blasst_rowskip (vfa::kBLR); see vfa_kernel.cuh.
+#include "fwd_dispatch.cuh"
+
+namespace vfa_host {
+int launch_blasst_rowskip(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                         const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
+  return launch_mode<vfa::kBLR>(p, nq, mq, mk, mv, mr, a, st);
+}
+}  // namespace vfa_host

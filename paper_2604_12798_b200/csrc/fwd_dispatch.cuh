@@ -1,0 +1,67 @@
+// Host-side launch templates for vfa_fwd_kernel, included by the per-variant TUs
+// (fwd_<variant>.cu). Each TU instantiates one MODE for every head dim / key block /
+// query-tiles-per-CTA / softmax split.
+#pragma once
+#include <string>
+
+#include "vfa_internal.h"
+#include "vfa_kernel.cuh"
+
+namespace vfa_host {
+
+template <int D, int BC, int NQ, int MODE, int SPLIT>
+int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+               const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
+  using C = vfa::Cfg<D, BC, NQ, SPLIT>;
+  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("cudaFuncGetAttributes: ") + cudaGetErrorString(e));
+    if (vfa::kRegBudget > fa.numRegs * vfa::kThreads)
+      return vfa_host::fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(vfa::kRegBudget) + " exceeds the launch allocation " +
+                                    std::to_string(fa.numRegs * vfa::kThreads) + " (would deadlock)");
+    attr_set = true;
+  }
+  const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
+  if (units <= 0) return VFA_OK;
+  kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return VFA_OK;
+}
+
+// Softmax column split per variant (params.softmax_split = 0), measured best on B200
+// (profiles/ab_r01_split.txt): VFA's frozen blocks need no cross-thread exchange, so all
+// warps serving both tiles wins; FA / VSA exchange a row max on every block, which per-tile
+// warp sets overlap with the other tile's work. One query tile per CTA: always 4.
+constexpr int default_split(int mode) {
+  return mode == vfa::kVFA ? VFA_SPLIT_VFA : (mode == vfa::kFA ? VFA_SPLIT_FA : VFA_SPLIT_VSA);
+}
+
+template <int D, int BC, int NQ, int MODE>
+int dispatch_split(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                   const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
+  const int split = p->softmax_split ? p->softmax_split : default_split(MODE);
+  if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
+  return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
+}
+
+template <int MODE>
+int launch_mode(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
+  const int D = static_cast<int>(p->head_dim), BC = p->k_block;
+#define VFA_NQ(DD, BB)                                                                          \
+  return nq == 2 ? dispatch_split<DD, BB, 2, MODE>(p, mq, mk, mv, mr, a, st)                    \
+                 : dispatch_split<DD, BB, 1, MODE>(p, mq, mk, mv, mr, a, st)
+  if (D == 128 && BC == 128) VFA_NQ(128, 128);
+  if (D == 128 && BC == 64) VFA_NQ(128, 64);
+  if (D == 64 && BC == 128) VFA_NQ(64, 128);
+  VFA_NQ(64, 64);
+#undef VFA_NQ
+}
+
+}  // namespace vfa_host

@@ -1,0 +1,38 @@
+// Declarations shared by the host translation units of libvfa_b200.so (not part of the
+// C ABI): the error channel and the per-variant kernel launchers (one TU each, so the
+// kernel instantiations compile in parallel).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/vfa_b200.h"
+
+namespace vfa {
+struct FwdArgs;
+}
+
+namespace vfa_host {
+
+// Sets the thread-local message returned by vfa_last_error() and returns `code`.
+int fail(int code, const std::string& msg);
+
+// Launches vfa_fwd_kernel for one variant (params.variant), dispatching head dim, key
+// block, query tiles per CTA (nq) and the softmax split. Defined in fwd_<variant>.cu.
+using LaunchFn = int (*)(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk,
+                         const CUtensorMap& mv, const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st);
+int launch_fa(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+              const vfa::FwdArgs&, cudaStream_t);
+int launch_vfa(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+               const vfa::FwdArgs&, cudaStream_t);
+int launch_vsa(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+               const vfa::FwdArgs&, cudaStream_t);
+int launch_blasst(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                  const CUtensorMap&, const vfa::FwdArgs&, cudaStream_t);
+int launch_blasst_fa4(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                      const CUtensorMap&, const vfa::FwdArgs&, cudaStream_t);
+int launch_blasst_rowskip(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                          const CUtensorMap&, const vfa::FwdArgs&, cudaStream_t);
+
+}  // namespace vfa_host

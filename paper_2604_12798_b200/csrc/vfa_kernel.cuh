@@ -5,15 +5,20 @@
 // loaded into shared memory and share the tile schedule (same rows => same
 // causal extent, same sink/local blocks).
 //
-// Warp roles (16 warps):
-//   warps 0-3   softmax WG for query tile 0   (thread r owns row r, TMEM lane r)
-//   warps 4-7   softmax WG for query tile 1
-//   warps 8-11  correction WG: O rescale in TMEM on exact-update blocks only
-//   warp 12     MMA issuer (one thread), TMEM allocator
-//   warp 13     TMA producer (one thread)
-//   warps 14-15 idle
-// TMEM (512 columns): S_t at t*128 (P_t bf16 aliased over its first BC/2 columns),
-// O_t at 256 + t*D.
+// Warp roles (20 warps, 640 threads):
+//   warps 0-15  softmax: 4 warpgroups; each row of a query tile is shared by SPLIT
+//               threads (TMEM lane r of SPLIT warpgroups). SPLIT 2: warpgroups 2t, 2t+1
+//               serve tile t; SPLIT 4: all four serve both tiles in turn. The softmax also
+//               rescales its part of O in TMEM on exact-update blocks (O is quiescent then).
+//   warp 16     MMA issuer (converged warp, elect.sync), TMEM allocator
+//   warp 17     TMA producer (one lane)
+//   warps 18-19 idle (complete the last warpgroup for setmaxnreg)
+// TMEM (512 columns): S_t at t*128 (P_t bf16 packed over the first half of each part's
+// columns), O_t at NQ*128 + t*D.
+// Modes (C-ABI variant codes): FA, VFA, VSA and the BLASST family (src/sparse.py:112-253):
+// BL (threshold skip on the baseline recurrence, sequential or sink/local order), BL4
+// (plus rescale elision when no row max rises by more than tau*ln2), BLR (row-granular
+// threshold: suppressed rows contribute zero mass).
 //
 // Reference algorithm (src/X.py = /root/reference/pkg/src/vfa_lab/X.py):
 //   precompute_kreprs / block_repr / sabsmax   src/vfa.py:47-88     -> krepr_kernel
@@ -24,6 +29,7 @@
 //   BLASST skip (all rows m~ - m_new < ln l)   src/sparse.py:99-109, 296-304
 //   fa_forward (rescale every block)           src/fa.py:28-61
 //   finalize (O / l, l == 0 errors)            src/core.py:101-109
+#pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -59,13 +65,19 @@ constexpr int kRegBudget = kSoftmaxWarps * 32 * kRegsSoftmax + (kThreads - kSoft
 constexpr int kMaxSmem = 227 * 1024;
 constexpr float kLn2 = 0.6931471805599453f;
 
-enum Mode { kFA = 0, kVFA = 1, kVSA = 2 };
+// kernel modes = C-ABI variant codes (include/vfa_b200.h)
+enum Mode { kFA = 0, kVFA = 1, kVSA = 2, kBL = 3, kBL4 = 4, kBLR = 5 };
+// every visited block takes the exact (rowmax + rescale) update
+constexpr bool all_exact(int m) { return m == kFA || m == kBL || m == kBL4 || m == kBLR; }
+// the block-skip test runs on every visited block
+constexpr bool skips(int m) { return m == kVSA || m == kBL || m == kBL4 || m == kBLR; }
 
 struct FwdArgs {
   int B, Hq, Hkv, Lq, Lk, group, Tr, Tc;
   int units_per_kvh, heads_per_unit;
   float c_scale;      // softmax scale * log2(e)
   float log2_lambda;  // skip threshold in log2 units (-inf: no skipping)
+  float tau;          // BLASST-FA4 elision threshold: max increase tau*ln2 (natural) = tau (log2)
   int causal, reorder, use_m_init, nrep_cap, n_sink, n_local, monitor;
   __nv_bfloat16* o;
   long long o_sb, o_sh, o_sr;
@@ -154,14 +166,17 @@ __device__ __forceinline__ Unit decode_unit(const FwdArgs& a, int u) {
 
 template <int MODE>
 __device__ __forceinline__ TileSchedule unit_schedule(const FwdArgs& a, int qt, int BC) {
-  return make_schedule(qt + 1, kBR, BC, a.Tc, a.causal != 0, a.n_sink, a.n_local,
-                       MODE == kFA ? false : (a.reorder != 0), MODE == kFA);
+  // FA / BLASST-FA4 / rowskip: ascending, all exact; BLASST: the VFA visit order when
+  // reorder (order='sink_local', src/sparse.py:133) but every block exact
+  constexpr bool kSeq = MODE == kFA || MODE == kBL4 || MODE == kBLR;
+  return make_schedule(qt + 1, kBR, BC, a.Tc, a.causal != 0, a.n_sink, a.n_local, kSeq ? false : (a.reorder != 0),
+                       kSeq);
 }
 
 // number of m-init chunks (BC representations per chunk)
 template <int MODE>
 __device__ __forceinline__ int minit_chunks(const FwdArgs& a, const TileSchedule& s, int BC, int* nrep) {
-  if (MODE == kFA || !a.use_m_init) {
+  if ((MODE != kVFA && MODE != kVSA) || !a.use_m_init) {
     *nrep = 0;
     return 0;
   }
@@ -456,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_after();
               if (c == 0) {
                 if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
-                skip = (MODE == kVSA) && (ctl->skip[t] != 0);
+                skip = skips(MODE) && (ctl->skip[t] != 0);
               }
               if (!skip) issue_pv_chunk(t, vs, c, first);
             }
@@ -561,10 +576,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 
       const float2 cs2 = make_float2(cs, cs);
-      int n_skipped = 0, n_skipped_special = 0;  // VSA only (FA/VFA counts are closed-form)
+      // block-class counts beyond the closed form (skip / elision / row-mask variants only)
+      int n_skipped = 0, n_skipped_special = 0, n_elided = 0, n_rows_masked = 0;
       for (int pos = 0; pos < N; ++pos) {
         const int j = sched_block(sched, pos);
-        const bool special = (MODE == kFA) || sched_is_special(sched, j);
+        const bool special = all_exact(MODE) || sched_is_special(sched, j);
         const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
         const int lim = R - (j - 1) * BC - part * CP;  // this part's columns > lim are masked
 #pragma unroll
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
           }
           bool skipped = false;
-          if (MODE == kFA || MODE == kVSA || special) {
+          if (MODE != kVFA || special) {
             // ---- exact-update / skip-test block: rowmax over the full row (four quarters,
             //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
             float mt = -INFINITY;
@@ -588,17 +604,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             mt = exchange_max(ti, t, mt);
             const float mt2 = mt * cs;
             const float m2n = fmaxf(m2[ti], mt2);
-            if (MODE == kVSA) {
+            bool keep = true;  // rowskip: this row takes part in the update
+            if (MODE == kBLR) {
+              // row-granular threshold (src/sparse.py:223-227): NaN (dead row) is not kept
+              keep = (a.log2_lambda == -INFINITY) || (mt2 - m2n >= a.log2_lambda);
+              skipped = named_bar_and(1 + t, SPLIT * kBR, !keep);
+            } else if (skips(MODE)) {
               const bool below = (mt2 - m2n < a.log2_lambda) ||
                                  (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
               skipped = named_bar_and(1 + t, SPLIT * kBR, below);
             }
+            bool elide = false;
+            if (MODE == kBL4 && !skipped) {
+              // rescale elision (src/sparse.py:187-193): every row had a finite max and none rose
+              // by more than tau*ln2 -> keep the old max, factor exactly 1
+              elide = named_bar_and(1 + t, SPLIT * kBR, m2[ti] != -INFINITY && m2n - m2[ti] <= a.tau);
+              n_elided += elide ? 1 : 0;
+            }
+            if (MODE == kBLR) n_rows_masked += (skipped || !keep) ? 1 : 0;
             if (skipped) {
               ++n_skipped;
               n_skipped_special += special ? 1 : 0;
-            } else if (special) {
-              const float f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
-              m2[ti] = m2n;
+            } else if (special && !elide) {
+              // (warp-uniform branch: skipped / elide are CTA-wide decisions) rowskip: a
+              // suppressed row keeps factor 1 and its max, and adds zero mass (src/sparse.py:241-247)
+              const bool upd = (MODE != kBLR) || keep;
+              const float f = (!upd || m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
+              if (upd) m2[ti] = m2n;
+              if (!upd) {
+#pragma unroll
+                for (int e = 0; e < CP; ++e) v[e] = -INFINITY;
+              }
               l[ti] = __fmul_rn(l[ti], f);  // no FMA contraction: identical l-recurrence in every mode
               // rescale this part of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
               // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
@@ -625,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
           if (r == 0 && part == 0) {
-            if (MODE == kVSA) ctl->skip[t] = skipped ? 1u : 0u;
+            if (skips(MODE)) ctl->skip[t] = skipped ? 1u : 0u;
             if (a.skip_trace) {
               const size_t idx =
                   ((static_cast<size_t>(unit.b) * a.Hq + unit.h0 + t) * a.Tr + unit.qt) * a.Tc + pos;
@@ -661,8 +697,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
         }
       }
-      const int n_special = NT * sched.n_spec - n_skipped_special;
-      const int n_frozen = NT * (N - sched.n_spec) - (n_skipped - n_skipped_special);
+      const int n_exact = all_exact(MODE) ? N : sched.n_spec;  // exact-update blocks per tile
+      const int n_special = NT * n_exact - n_skipped_special - n_elided;
+      const int n_frozen = NT * (N - n_exact) - (n_skipped - n_skipped_special) + n_elided;
 
       // ---- epilogue: O / l (src/core.py:101-109), LSE = m + ln l; l = sum over the parts
       bool any_nonfinite = false;
@@ -724,7 +761,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
           atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
         }
+        if (MODE == kBLR && part == 0) {
+          const unsigned masked = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_rows_masked));
+          if (lane == 0) atomicAdd(&a.stats[VFA_STAT_ROWS_MASKED], static_cast<unsigned long long>(masked));
+        }
         if (r == 0 && part == 0) {
+          if (MODE == kBL4) atomicAdd(&a.stats[VFA_STAT_ELIDED], static_cast<unsigned long long>(n_elided));
           atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(NT * N));
           atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
           atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_special));
@@ -807,487 +849,3 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
 }
 
 }  // namespace vfa
-
-// ====================================================================================
-// Host side
-// ====================================================================================
-namespace {
-
-thread_local std::string g_last_error;
-long long* g_debug_trace = nullptr;  // debug only: set by vfa_debug_trace()
-
-int fail(int code, const std::string& msg) {
-  g_last_error = msg;
-  return code;
-}
-
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// 4-D bf16 tensor [B, H, L, D] (innermost D) with element strides; box {64, box_rows, 1, 1}.
-bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t H, int64_t L, int64_t D, int64_t sb,
-              int64_t sh, int64_t sr, int box_rows) {
-  EncodeTiledFn fn = get_encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(H),
-                        static_cast<cuuint64_t>(B)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(sr * 2), static_cast<cuuint64_t>(sh * 2),
-                           static_cast<cuuint64_t>(sb * 2)};
-  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_rows), 1, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-int64_t n_key_blocks(const VfaParams* p) { return p->seq_k / p->k_block; }
-int64_t n_reprs(const VfaParams* p) {
-  int64_t tc = n_key_blocks(p);
-  return (p->tc1 > 0 && p->tc1 < tc) ? p->tc1 : tc;
-}
-
-template <int D, int BC, int NQ, int MODE, int SPLIT>
-int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-               const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
-  using C = vfa::Cfg<D, BC, NQ, SPLIT>;
-  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncGetAttributes: ") + cudaGetErrorString(e));
-    if (vfa::kRegBudget > fa.numRegs * vfa::kThreads)
-      return fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(vfa::kRegBudget) + " exceeds the launch allocation " +
-                                    std::to_string(fa.numRegs * vfa::kThreads) + " (would deadlock)");
-    attr_set = true;
-  }
-  const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
-  if (units <= 0) return VFA_OK;
-  kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
-  return VFA_OK;
-}
-
-// Softmax column split per variant (params.softmax_split = 0), measured best on B200
-// (profiles/ab_r01_split.txt): VFA's frozen blocks need no cross-thread exchange, so all
-// warps serving both tiles wins; FA / VSA exchange a row max on every block, which per-tile
-// warp sets overlap with the other tile's work. One query tile per CTA: always 4.
-constexpr int default_split(int variant) {
-  return variant == VFA_VARIANT_FA ? VFA_SPLIT_FA : (variant == VFA_VARIANT_VFA ? VFA_SPLIT_VFA : VFA_SPLIT_VSA);
-}
-
-template <int D, int BC, int NQ, int MODE>
-int dispatch_split(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                   const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
-  const int split = p->softmax_split ? p->softmax_split : default_split(p->variant);
-  if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
-  return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
-}
-
-template <int D, int BC, int NQ>
-int dispatch_mode(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                  const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
-  switch (p->variant) {
-    case VFA_VARIANT_FA:
-      return dispatch_split<D, BC, NQ, vfa::kFA>(p, mq, mk, mv, mr, args, st);
-    case VFA_VARIANT_VFA:
-      return dispatch_split<D, BC, NQ, vfa::kVFA>(p, mq, mk, mv, mr, args, st);
-    default:
-      return dispatch_split<D, BC, NQ, vfa::kVSA>(p, mq, mk, mv, mr, args, st);
-  }
-}
-
-template <int D, int BC>
-int dispatch_nq(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
-  return nq == 2 ? dispatch_mode<D, BC, 2>(p, mq, mk, mv, mr, args, st)
-                 : dispatch_mode<D, BC, 1>(p, mq, mk, mv, mr, args, st);
-}
-
-int launch_krepr(const VfaParams* p, const void* k, void* out, cudaStream_t st) {
-  const int nblk = static_cast<int>(n_reprs(p));
-  dim3 grid((nblk + 3) / 4, static_cast<unsigned>(p->heads_kv), static_cast<unsigned>(p->batch));
-  if (p->head_dim == 128)
-    vfa::krepr_kernel<128><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
-                                                p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
-                                                p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
-  else
-    vfa::krepr_kernel<64><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
-                                               p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
-                                               p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("krepr launch: ") + cudaGetErrorString(e));
-  return VFA_OK;
-}
-
-bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
-
-void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
-  if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * VFA_STAT_COUNT, st);
-  if (status) {
-    cudaMemsetAsync(status, 0, sizeof(unsigned) * VFA_STATUS_COUNT, st);
-    cudaMemsetAsync(status + VFA_STATUS_UNDERFLOW_ROW, 0xff, sizeof(unsigned) * 2, st);
-  }
-}
-
-int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
-                 void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base);
-
-}  // namespace
-
-extern "C" {
-
-int vfa_check_params(const VfaParams* p) {
-  if (!p) return fail(VFA_ERR_CONFIG, "params is NULL");
-  if (p->variant < VFA_VARIANT_FA || p->variant > VFA_VARIANT_VSA)
-    return fail(VFA_ERR_CONFIG, "variant must be 0 (fa), 1 (vfa) or 2 (vsa)");
-  if (p->kind < VFA_KREPR_SABSMAX || p->kind > VFA_KREPR_K_ABSMAX_UNSIGNED)
-    return fail(VFA_ERR_CONFIG, "unknown key representation");
-  if (p->qkind != 0) return fail(VFA_ERR_CONFIG, "only the row_wise query representation runs on the GPU path");
-  if (p->q_block != 128) return fail(VFA_ERR_CONFIG, "q_block must be 128 (tcgen05 M = 128)");
-  if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
-  if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
-  if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
-  if (p->softmax_split != 0 && p->softmax_split != 2 && p->softmax_split != 4)
-    return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 2 or 4");
-  if (p->variant == VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
-  if (p->batch < 1 || p->heads_q < 1 || p->heads_kv < 1 || p->seq_q < 1 || p->seq_k < 1)
-    return fail(VFA_ERR_DATA, "all dimensions must be >= 1");
-  if (p->heads_q % p->heads_kv) return fail(VFA_ERR_DATA, "heads_q must be a multiple of heads_kv");
-  if (p->seq_q % p->q_block)
-    return fail(VFA_ERR_DATA, "seq_len_q=" + std::to_string(p->seq_q) + " not divisible by q_block=" +
-                                  std::to_string(p->q_block));
-  if (p->seq_k % p->k_block)
-    return fail(VFA_ERR_DATA, "seq_len_k=" + std::to_string(p->seq_k) + " not divisible by k_block=" +
-                                  std::to_string(p->k_block));
-  if (p->causal && p->seq_q != p->seq_k) return fail(VFA_ERR_DATA, "causal masking requires N_q == N_k");
-  if (p->tc1 < 0 || p->tc1 > n_key_blocks(p))
-    return fail(VFA_ERR_CONFIG, "tc1 must be in 1..T_c (0 = all)");
-  const int64_t* strides[4] = {p->q_stride, p->k_stride, p->v_stride, p->o_stride};
-  for (int i = 0; i < 4; ++i)
-    for (int j = 0; j < 3; ++j)
-      if (strides[i][j] % 8 != 0 || strides[i][j] < 0)
-        return fail(VFA_ERR_DATA, "strides must be non-negative multiples of 8 elements (16 bytes)");
-  if (p->seq_q * p->heads_q * p->batch >= 0xffffffffLL) return fail(VFA_ERR_DATA, "too many rows");
-  return VFA_OK;
-}
-
-size_t vfa_workspace_bytes(const VfaParams* p) {
-  if (!p || vfa_check_params(p) != VFA_OK) return 0;
-  return static_cast<size_t>(p->batch * p->heads_kv * n_reprs(p) * p->head_dim * 2) + 256;
-}
-
-int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream) {
-  int rc = vfa_check_params(p);
-  if (rc) return rc;
-  if (!k || !out) return fail(VFA_ERR_DATA, "NULL pointer");
-  return launch_krepr(p, k, out, static_cast<cudaStream_t>(stream));
-}
-
-int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
-            void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-            unsigned char* skip_trace, void* stream) {
-  int rc = vfa_check_params(p);
-  if (rc) return rc;
-  if (!q || !k || !v || !o) return fail(VFA_ERR_DATA, "NULL tensor pointer");
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
-    return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
-  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, skip_trace,
-                      static_cast<cudaStream_t>(stream), true, 0);
-}
-
-}  // extern "C"
-
-namespace {
-// The forward on device buffers. zero_counters: reset stats/status first (false when a
-// caller accumulates several launches into one status word, e.g. vfa_fwd_host's chunks).
-int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
-                 void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base) {
-  int rc = VFA_OK;
-  const bool minit = p->variant != VFA_VARIANT_FA && p->use_m_init;
-  const int64_t nrep = n_reprs(p);
-  if (minit) {
-    if (!workspace || workspace_bytes < vfa_workspace_bytes(p) || !aligned16(workspace))
-      return fail(VFA_ERR_DATA, "workspace too small or misaligned");
-  }
-  const int D = static_cast<int>(p->head_dim), BC = p->k_block;
-  const int group = static_cast<int>(p->heads_q / p->heads_kv);
-  const int nq = (group % 2 == 0) ? 2 : 1;
-
-  CUtensorMap mq, mk, mv, mr;
-  if (!make_map(&mq, q, p->batch, p->heads_q, p->seq_q, D, p->q_stride[0], p->q_stride[1], p->q_stride[2], 128) ||
-      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2], BC) ||
-      !make_map(&mv, v, p->batch, p->heads_kv, p->seq_k, D, p->v_stride[0], p->v_stride[1], p->v_stride[2], BC))
-    return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  if (minit) {
-    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, BC))
-      return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed (krepr)");
-    if (!p->krepr_precomputed) {
-      rc = launch_krepr(p, k, workspace, st);
-      if (rc) return rc;
-    }
-  } else {
-    mr = mk;
-  }
-  if (zero_counters) reset_counters(stats, status, st);
-  if (skip_trace)
-    cudaMemsetAsync(skip_trace, 0,
-                    static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * n_key_blocks(p)), st);
-
-  vfa::FwdArgs a;
-  a.B = static_cast<int>(p->batch);
-  a.Hq = static_cast<int>(p->heads_q);
-  a.Hkv = static_cast<int>(p->heads_kv);
-  a.Lq = static_cast<int>(p->seq_q);
-  a.Lk = static_cast<int>(p->seq_k);
-  a.group = group;
-  a.Tr = static_cast<int>(p->seq_q / 128);
-  a.Tc = static_cast<int>(n_key_blocks(p));
-  a.heads_per_unit = nq;
-  a.units_per_kvh = a.Tr * (group / nq);
-  const double scale = p->scale > 0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(D));
-  a.c_scale = static_cast<float>(scale * 1.4426950408889634);
-  a.log2_lambda = (p->variant == VFA_VARIANT_VSA && p->lam > 0) ? static_cast<float>(std::log2(p->lam)) : -INFINITY;
-  a.causal = p->causal ? 1 : 0;
-  a.reorder = p->reorder ? 1 : 0;
-  a.use_m_init = minit ? 1 : 0;
-  a.nrep_cap = static_cast<int>(nrep);
-  a.n_sink = p->n_sink;
-  a.n_local = p->n_local;
-  a.monitor = p->monitor ? 1 : 0;
-  a.o = static_cast<__nv_bfloat16*>(o);
-  a.o_sb = p->o_stride[0];
-  a.o_sh = p->o_stride[1];
-  a.o_sr = p->o_stride[2];
-  a.lse = lse;
-  a.stats = reinterpret_cast<unsigned long long*>(stats);
-  a.status = status;
-  a.skip_trace = skip_trace;
-  a.row_base = row_base;
-  a.trace = g_debug_trace;
-
-  if (D == 128 && BC == 128) return dispatch_nq<128, 128>(p, nq, mq, mk, mv, mr, a, st);
-  if (D == 128 && BC == 64) return dispatch_nq<128, 64>(p, nq, mq, mk, mv, mr, a, st);
-  if (D == 64 && BC == 128) return dispatch_nq<64, 128>(p, nq, mq, mk, mv, mr, a, st);
-  return dispatch_nq<64, 64>(p, nq, mq, mk, mv, mr, a, st);
-}
-
-// ---------------------------------------------------------------- host-resident pipeline
-// vfa_fwd_host: the problem is cut into chunks of (one batch, `ck` KV heads with their GQA
-// query heads). Chunk c is copied host->device on the H2D stream into scratch slot c % S,
-// computed on compute stream c % 2 (so one chunk's causal tail overlaps the next chunk's
-// head), and its O / LSE copied back on the D2H stream, so PCIe transfers in both
-// directions overlap the attention kernels.
-constexpr size_t kAlign = 256;
-size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-
-struct ChunkGeom {
-  int64_t ck, nq, chunks, slots;
-  size_t q_bytes, kv_bytes, lse_bytes, ws_bytes, slot_bytes;
-  VfaParams cp;  // the per-chunk problem (dense device layout)
-};
-
-ChunkGeom chunk_geom(const VfaParams* p, int chunk_kv_heads) {
-  ChunkGeom g{};
-  g.ck = chunk_kv_heads;
-  const int64_t group = p->heads_q / p->heads_kv;
-  g.nq = g.ck * group;
-  g.chunks = p->batch * (p->heads_kv / g.ck);
-  g.slots = g.chunks < 3 ? g.chunks : 3;
-  g.cp = *p;
-  g.cp.batch = 1;
-  g.cp.heads_q = g.nq;
-  g.cp.heads_kv = g.ck;
-  const int64_t D = p->head_dim;
-  const int64_t qs[3] = {g.nq * p->seq_q * D, p->seq_q * D, D};
-  const int64_t ks[3] = {g.ck * p->seq_k * D, p->seq_k * D, D};
-  for (int i = 0; i < 3; ++i) {
-    g.cp.q_stride[i] = g.cp.o_stride[i] = qs[i];
-    g.cp.k_stride[i] = g.cp.v_stride[i] = ks[i];
-  }
-  g.q_bytes = static_cast<size_t>(g.nq * p->seq_q * D * 2);
-  g.kv_bytes = static_cast<size_t>(g.ck * p->seq_k * D * 2);
-  g.lse_bytes = static_cast<size_t>(g.nq * p->seq_q * 4);
-  g.ws_bytes = vfa_workspace_bytes(&g.cp);
-  g.slot_bytes = 2 * align_up(g.q_bytes) + 2 * align_up(g.kv_bytes) + align_up(g.lse_bytes) + align_up(g.ws_bytes);
-  return g;
-}
-
-struct HostStreams {
-  int device = -1;
-  cudaStream_t h2d = nullptr, d2h = nullptr, comp[2] = {nullptr, nullptr};
-};
-
-// per-thread, per-device streams of the pipeline (created once, non-blocking)
-int host_streams(HostStreams** out) {
-  thread_local HostStreams cache[16];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess || dev < 0 || dev >= 16) return fail(VFA_ERR_CUDA, "cudaGetDevice failed");
-  HostStreams& s = cache[dev];
-  if (s.device != dev) {
-    cudaStream_t* all[4] = {&s.h2d, &s.d2h, &s.comp[0], &s.comp[1]};
-    for (cudaStream_t* x : all)
-      if (cudaStreamCreateWithFlags(x, cudaStreamNonBlocking) != cudaSuccess)
-        return fail(VFA_ERR_CUDA, "cudaStreamCreateWithFlags failed");
-    s.device = dev;
-  }
-  *out = &s;
-  return VFA_OK;
-}
-}  // namespace
-
-extern "C" {
-
-size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads) {
-  if (!p || vfa_check_params(p) != VFA_OK || chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads) return 0;
-  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
-  return static_cast<size_t>(g.slots) * g.slot_bytes + kAlign;
-}
-
-int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host, void* o_host,
-                 float* lse_host, void* scratch, size_t scratch_bytes, long long* stats, unsigned int* status,
-                 int chunk_kv_heads, void* stream) {
-  int rc = vfa_check_params(p);
-  if (rc) return rc;
-  if (!q_host || !k_host || !v_host || !o_host) return fail(VFA_ERR_DATA, "NULL host pointer");
-  if (chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads)
-    return fail(VFA_ERR_CONFIG, "chunk_kv_heads must divide heads_kv");
-  if (p->krepr_precomputed) return fail(VFA_ERR_CONFIG, "vfa_fwd_host computes the representations itself");
-  const size_t need = vfa_host_scratch_bytes(p, chunk_kv_heads);
-  if (!scratch || scratch_bytes < need) return fail(VFA_ERR_DATA, "scratch too small (vfa_host_scratch_bytes)");
-  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
-  HostStreams* hs = nullptr;
-  rc = host_streams(&hs);
-  if (rc) return rc;
-  cudaStream_t caller = static_cast<cudaStream_t>(stream);
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~uintptr_t(kAlign - 1));
-
-  std::vector<cudaEvent_t> ev;
-  auto new_event = [&]() -> cudaEvent_t {
-    cudaEvent_t e = nullptr;
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    ev.push_back(e);
-    return e;
-  };
-  auto cleanup = [&]() {
-    for (cudaEvent_t e : ev) cudaEventDestroy(e);  // released once their work completes
-  };
-  // counters accumulate over chunks; scratch reuse is ordered after the caller's prior work
-  reset_counters(stats, status, caller);
-  cudaEvent_t entry = new_event();
-  if (!entry) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
-  cudaEventRecord(entry, caller);
-  cudaStreamWaitEvent(hs->h2d, entry, 0);
-  cudaStreamWaitEvent(hs->comp[0], entry, 0);
-  cudaStreamWaitEvent(hs->comp[1], entry, 0);
-
-  const int64_t D = p->head_dim, group = p->heads_q / p->heads_kv;
-  const int64_t per_b = p->heads_kv / g.ck;
-  std::vector<cudaEvent_t> slot_free(static_cast<size_t>(g.slots), nullptr);
-  for (int64_t c = 0; c < g.chunks; ++c) {
-    const int64_t b = c / per_b, kv0 = (c % per_b) * g.ck, h0 = kv0 * group;
-    const int64_t s = c % g.slots;
-    uint8_t* sl = base + s * g.slot_bytes;
-    uint8_t* dq = sl;
-    uint8_t* dk = dq + align_up(g.q_bytes);
-    uint8_t* dv = dk + align_up(g.kv_bytes);
-    uint8_t* dout = dv + align_up(g.kv_bytes);
-    float* dlse = reinterpret_cast<float*>(dout + align_up(g.q_bytes));
-    uint8_t* dws = reinterpret_cast<uint8_t*>(dlse) + align_up(g.lse_bytes);
-    const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
-    const size_t koff = static_cast<size_t>((b * p->heads_kv + kv0) * p->seq_k * D) * 2;
-    const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
-    // H2D (after the slot's previous chunk has been copied out)
-    if (slot_free[s]) cudaStreamWaitEvent(hs->h2d, slot_free[s], 0);
-    cudaMemcpyAsync(dk, static_cast<const uint8_t*>(k_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
-    cudaMemcpyAsync(dv, static_cast<const uint8_t*>(v_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
-    cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, g.q_bytes, cudaMemcpyHostToDevice, hs->h2d);
-    cudaEvent_t in = new_event(), done = new_event(), out = new_event();
-    if (!in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
-    cudaEventRecord(in, hs->h2d);
-    // compute
-    cudaStream_t cs = hs->comp[c & 1];
-    cudaStreamWaitEvent(cs, in, 0);
-    rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, cs, false,
-                      static_cast<long long>(loff));
-    if (rc) return cleanup(), rc;
-    cudaEventRecord(done, cs);
-    // D2H
-    cudaStreamWaitEvent(hs->d2h, done, 0);
-    cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
-    if (lse_host)
-      cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
-    cudaEventRecord(out, hs->d2h);
-    slot_free[s] = out;
-  }
-  cudaEvent_t exit_ev = new_event();
-  if (!exit_ev) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
-  cudaEventRecord(exit_ev, hs->d2h);
-  cudaStreamWaitEvent(caller, exit_ev, 0);
-  cleanup();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("vfa_fwd_host: ") + cudaGetErrorString(e));
-  return VFA_OK;
-}
-
-int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local, int reorder,
-                 int variant, int* order_out, unsigned char* special_out, int cap) {
-  if (i < 1 || q_block < 1 || k_block < 1 || t_c < 1) return -VFA_ERR_CONFIG;
-  vfa::TileSchedule s = vfa::make_schedule(i, q_block, k_block, t_c, causal != 0, n_sink, n_local,
-                                           variant != VFA_VARIANT_FA && reorder != 0, variant == VFA_VARIANT_FA);
-  for (int pos = 0; pos < s.vmax && pos < cap; ++pos) {
-    int j = vfa::sched_block(s, pos);
-    if (order_out) order_out[pos] = j;
-    if (special_out) special_out[pos] = vfa::sched_is_special(s, j) ? 1 : 0;
-  }
-  return s.vmax;
-}
-
-int vfa_status_code(const unsigned int* status_host) {
-  if (!status_host) return fail(VFA_ERR_CONFIG, "status is NULL");
-  if (status_host[VFA_STATUS_FLAGS] & 3u) {
-    if (status_host[VFA_STATUS_FLAGS] & 1u)
-      return fail(VFA_ERR_NUMERICAL, "query row " + std::to_string(status_host[VFA_STATUS_MASKED_ROW]) +
-                                         " is fully masked; cannot normalize");
-    return fail(VFA_ERR_NUMERICAL,
-                "normalizer underflow at query row " + std::to_string(status_host[VFA_STATUS_UNDERFLOW_ROW]));
-  }
-  return VFA_OK;
-}
-
-const char* vfa_last_error(void) { return g_last_error.c_str(); }
-
-int vfa_debug_trace(long long* device_buffer) {
-#ifdef VFA_TRACE
-  g_debug_trace = device_buffer;
-  return VFA_OK;
-#else
-  (void)device_buffer;
-  return fail(VFA_ERR_CONFIG, "library built without -DVFA_TRACE (scripts/trace_timeline.py builds the trace variant)");
-#endif
-}
-
-const char* vfa_version(void) { return "vfa_b200 0.1.0 (sm_100a, tcgen05/TMEM/TMA)"; }
-
-}  // extern "C"

@@ -18,6 +18,7 @@ Call-time hooks (no fork of the reference):
 from __future__ import annotations
 
 import hashlib
+import json
 import os
 import sys
 
@@ -97,6 +98,18 @@ def run_case(name, spec, data, causal, variant, **kw):
             lam = kw.pop("lam")
             out, counters, stats, mon = vfa_lab.vsa_forward(p, SkipConfig(lam=lam), **kw)
             rec["lam"] = lam
+        elif variant == "blasst":
+            lam, order = kw.pop("lam"), kw.pop("order", "sequential")
+            out, counters, stats = vfa_lab.blasst_forward(p, SkipConfig(lam=lam), order=order)
+            rec["lam"], rec["order"] = lam, order
+        elif variant == "blasst_fa4":
+            lam, tau = kw.pop("lam"), kw.pop("tau")
+            out, counters, stats = vfa_lab.blasst_fa4_forward(p, SkipConfig(lam=lam, tau=tau))
+            rec["lam"], rec["tau"] = lam, tau
+        elif variant == "blasst_rowskip":
+            lam = kw.pop("lam")
+            out, counters, stats = vfa_lab.blasst_rowskip_forward(p, SkipConfig(lam=lam, granularity="row"))
+            rec["lam"] = lam
         else:
             raise ValueError(variant)
     except (vfa_lab.FullyMaskedRowError, vfa_lab.NormalizerUnderflowError) as e:
@@ -121,7 +134,8 @@ def run_case(name, spec, data, causal, variant, **kw):
         for f, val in counters.as_dict().items():
             rec[f"counters.{f}"] = val
     if stats is not None:
-        for f in ("blocks_visited", "blocks_skipped", "processed_special", "processed_frozen"):
+        for f in ("blocks_visited", "blocks_skipped", "processed_special", "processed_frozen",
+                  "rescales_elided", "rows_masked", "row_slots", "blocks_processed"):
             rec[f"stats.{f}"] = getattr(stats, f)
     if mon is not None:
         rec["mon.count_over_f16"] = mon.count_over_f16
@@ -159,6 +173,7 @@ def main():
     k[:, 0] = 0.0
     k[:128, 0] = amp
     cases.append(("vsa_sink_lam1e-2", s, (q, k, v), True, "vsa", dict(lam=1e-2)))
+    sink = (q.copy(), k.copy(), v.copy())
     cases.append(("vsa_sink_lam1e-1", s, (q, k, v), True, "vsa", dict(lam=1e-1)))
     # frozen-max overflow without m-init (SURVEY.md §8d non-finite check)
     s = BlockSpec(512, 512, 128, 128, 128)
@@ -174,6 +189,23 @@ def main():
     s = BlockSpec(128, 128, 64, 128, 128)
     cases.append(("vfa_underflow_kmax", s, (q, k, v), False, "vfa", dict(kind="k_max")))
 
+    # BLASST family (src/sparse.py:112-253), SURVEY.md §8f row 1
+    s = BlockSpec(1024, 1024, 64, 128, 128)
+    mp = gen_structured(s, 11, "middle_peak", 8.0)
+    mp = (mp.q, mp.k, mp.v)
+    cases.append(("blasst_seq_sink_lam1e-2", s, sink, True, "blasst", dict(lam=1e-2)))
+    cases.append(("blasst_swa_sink_lam1e-2", s, sink, True, "blasst", dict(lam=1e-2, order="sink_local")))
+    cases.append(("blasst_nolam_gauss", s, gen_gaussian(s, 10), True, "blasst", dict(lam=None)))
+    cases.append(("blasst_fa4_tau0_midpeak", s, mp, True, "blasst_fa4", dict(lam=None, tau=0.0)))
+    cases.append(("blasst_fa4_tau8_sink_lam1e-3", s, sink, True, "blasst_fa4", dict(lam=1e-3, tau=8.0)))
+    cases.append(("blasst_fa4_tauinf_gauss", s, gen_gaussian(s, 12), True, "blasst_fa4",
+                  dict(lam=None, tau=float("inf"))))
+    cases.append(("blasst_rowskip_sink_lam1e-3", s, sink, True, "blasst_rowskip", dict(lam=1e-3)))
+    cases.append(("blasst_rowskip_nolam_gauss", s, gen_gaussian(s, 13), True, "blasst_rowskip", dict(lam=None)))
+    s = BlockSpec(1024, 1024, 64, 128, 64)
+    cases.append(("blasst_fa4_k64_tau2_sink", s, sink, True, "blasst_fa4", dict(lam=1e-2, tau=2.0)))
+    cases.append(("blasst_rowskip_k64_midpeak_lam1e-2", s, mp, True, "blasst_rowskip", dict(lam=1e-2)))
+
     arrays, meta = {}, []
     for name, spec, data, causal, variant, kw in cases:
         a, rec = run_case(name, spec, data, causal, variant, **dict(kw))
@@ -181,7 +213,7 @@ def main():
         arrays.update(a)
         meta.append(rec)
         print(name, {k2: v2 for k2, v2 in rec.items() if k2.startswith(("stats", "error", "mon.count"))})
-    arrays["meta"] = np.array(repr(meta))
+    arrays["meta"] = np.array(json.dumps(meta))  # json: carries inf / nan (tau = inf)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
 
 

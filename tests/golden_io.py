@@ -1,7 +1,7 @@
 """Loader for tests/golden/golden.npz (written by tests/golden/make_golden.py)."""
 
-import ast
 import functools
+import json
 import os
 
 import numpy as np
@@ -12,7 +12,7 @@ PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golde
 @functools.lru_cache(maxsize=1)
 def _load():
     z = np.load(PATH)
-    meta = ast.literal_eval(str(z["meta"]))
+    meta = json.loads(str(z["meta"]))
     arrays = {k: z[k] for k in z.files if k != "meta"}
     return arrays, {m["name"]: m for m in meta}
 

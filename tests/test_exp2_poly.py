@@ -1,5 +1,5 @@
 """CPU emulation (float32, numpy) of the kernel's FMA-pipe exp2 (ex2_poly2 in
-paper_2604_12798_b200/csrc/vfa_fwd.cu): coefficients are parsed from the source so the
+paper_2604_12798_b200/csrc/vfa_kernel.cuh): coefficients are parsed from the source so the
 test tracks the kernel. Pins accuracy (< 4e-6 relative), exact zeros for x <= -127 and
 masked -inf (so l == 0 underflow semantics match MUFU.EX2.FTZ), +inf for x >= 128."""
 
@@ -9,7 +9,7 @@ import re
 import numpy as np
 
 SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                   "paper_2604_12798_b200", "csrc", "vfa_fwd.cu")
+                   "paper_2604_12798_b200", "csrc", "vfa_kernel.cuh")
 
 
 def _coeffs():

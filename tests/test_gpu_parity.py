@@ -107,6 +107,17 @@ def test_vfa_options(kind, opts):
     assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
 
 
+def _golden_kw(m):
+    kw = dict(variant=m["variant"], causal=m["causal"], q_block=128, k_block=m["k_block"],
+              n_sink=m["n_sink"], n_local=m["n_local"])
+    for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau"):
+        if key in m:
+            kw[key] = m[key]
+    if m.get("order") == "sink_local":
+        kw["reorder"] = True
+    return kw
+
+
 @pytest.mark.parametrize("name", [n for n in case_names()])
 def test_golden_vectors(name):
     m, q, k, v, out32, lse = case(name)
@@ -116,11 +127,7 @@ def test_golden_vectors(name):
     from paper_2604_12798_b200.api import NormalizerUnderflowError
     qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda()[None, None]
                   for x in case_bits(name))
-    kw = dict(variant=m["variant"], causal=m["causal"], q_block=128, k_block=m["k_block"],
-              n_sink=m["n_sink"], n_local=m["n_local"])
-    for key in ("kind", "reorder", "use_m_init", "tc1", "lam"):
-        if key in m:
-            kw[key] = m[key]
+    kw = _golden_kw(m)
     if m["error"]:
         with pytest.raises(NormalizerUnderflowError) as ei:
             attention_forward(qb, kb, vb, **kw)
@@ -139,11 +146,102 @@ def test_golden_vectors(name):
     if "stats.blocks_visited" in m:
         assert st["visited"] == m["stats.blocks_visited"]
         assert st["skipped"] == m["stats.blocks_skipped"]
-        assert st["special"] == m["stats.processed_special"]
-        assert st["frozen"] == m["stats.processed_frozen"]
-    if "counters.rescale_events" in m and m["variant"] != "vsa":
+        if m["variant"] == "vsa":
+            assert st["special"] == m["stats.processed_special"]
+            assert st["frozen"] == m["stats.processed_frozen"]
+        if "stats.blocks_processed" in m:
+            assert st["special"] + st["frozen"] == m["stats.blocks_processed"]
+            assert st["elided"] == m["stats.rescales_elided"]
+            assert st["rows_masked"] == m["stats.rows_masked"]
+    if "counters.rescale_events" in m and m["variant"] in ("fa", "vfa"):
         assert st["special"] == m["counters.rescale_events"]
         assert st["special"] + st["frozen"] == m["counters.blocks_processed"]
+
+
+@pytest.mark.parametrize("name", [n for n in case_names() if n.startswith("blasst")])
+def test_blasst_golden_counters_integer_equal(name):
+    # the reference-shaped entry points charge OpCounters from the device's block-class
+    # counts: integer-equal to the reference's instrumented counters (src/counters.py)
+    from paper_2604_12798_b200 import (AttentionProblem, BlockSpec, SkipConfig, blasst_fa4_forward,
+                                       blasst_forward, blasst_rowskip_forward)
+    m, q, k, v, out32, lse = case(name)
+    qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda() for x in case_bits(name))
+    L, d = qb.shape
+    p = AttentionProblem(qb, kb, vb, blocks=BlockSpec(L, L, d, 128, m["k_block"]), causal=m["causal"])
+    if m["variant"] == "blasst":
+        out, c, stats = blasst_forward(p, SkipConfig(lam=m["lam"]), order=m.get("order", "sequential"))
+    elif m["variant"] == "blasst_fa4":
+        out, c, stats = blasst_fa4_forward(p, SkipConfig(lam=m["lam"], tau=m["tau"]))
+    else:
+        out, c, stats = blasst_rowskip_forward(p, SkipConfig(lam=m["lam"], granularity="row"))
+    for f, val in c.as_dict().items():
+        assert val == m[f"counters.{f}"], (f, val, m[f"counters.{f}"])
+    for f in ("blocks_visited", "blocks_skipped", "rescales_elided", "rows_masked", "row_slots",
+              "blocks_processed"):
+        assert getattr(stats, f) == m[f"stats.{f}"], f
+    assert vo.max_rel_err(_f64(out), out32.astype(np.float64)) <= O_REL
+
+
+BLASST_CASES = [("blasst", dict(lam=1e-2)), ("blasst", dict(lam=1e-2, reorder=True)),
+                ("blasst", dict(lam=None)), ("blasst_fa4", dict(lam=None, tau=0.0)),
+                ("blasst_fa4", dict(lam=1e-3, tau=8.0)), ("blasst_fa4", dict(lam=None, tau=float("inf"))),
+                ("blasst_rowskip", dict(lam=1e-3)), ("blasst_rowskip", dict(lam=None))]
+
+
+@pytest.mark.parametrize("variant,opts", BLASST_CASES)
+@pytest.mark.parametrize("d,bc", [(128, 128), (64, 64)])
+def test_blasst_family_against_oracle(variant, opts, d, bc):
+    # planted sink (src/tensor.py:153-165 trick) so that skips / elisions / masked rows occur
+    B, Hq, Hkv, L = 1, 4, 2, 1024
+    q, k, v = _rand((B, Hq, L, d), 121), _rand((B, Hkv, L, d), 122), _rand((B, Hkv, L, d), 123)
+    amp = float(np.sqrt(8.0 * np.sqrt(d)))
+    q[..., 0] = amp
+    k[..., 0] = 0
+    k[:, :, :bc, 0] = amp
+    kw = dict(variant=variant, causal=True, q_block=128, k_block=bc, **opts)
+    order = "sink_local" if opts.get("reorder") else "sequential"
+    okw = {key: val for key, val in kw.items() if key != "reorder"}
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    qf, kf, vf = _f64(q), _f64(k), _f64(v)
+    o_ref = np.empty(out.shape)
+    l_ref = np.empty(lse.shape)
+    ref = {"visited": 0, "skipped": 0, "elided": 0, "rows_masked": 0}
+    tight = True
+    for h in range(Hq):
+        r = vo.forward_head(qf[0, h], kf[0, h // 2], vf[0, h // 2], order=order, record_decisions=True, **okw)
+        o_ref[0, h], l_ref[0, h] = r.out, r.lse
+        for key in ref:
+            ref[key] += getattr(r, key)
+        tight &= all(mg > 1e-3 for blk in r.decisions for (_, _, mg) in blk)
+    _compare(out, lse, o_ref, l_ref, str(kw))
+    assert st["visited"] == ref["visited"]
+    if tight:  # no decision within fp32 rounding of its threshold: counts are exact
+        assert st["skipped"] == ref["skipped"]
+        assert st["rows_masked"] == ref["rows_masked"]
+    if variant != "blasst_fa4" or opts["tau"] in (float("inf"),):
+        assert st["elided"] == ref["elided"]
+
+
+@pytest.mark.parametrize("split", [2, 4])
+def test_blasst_without_threshold_is_bitwise_fa(split):
+    # reference tests/test_sparse.py:32-38 (blasst) and :122-128 (rowskip): lam=None -> FA
+    q, k, v = _rand((1, 4, 1024, 128), 131), _rand((1, 2, 1024, 128), 132), _rand((1, 2, 1024, 128), 133)
+    base = dict(causal=True, softmax_split=split)
+    o_fa, l_fa, _, _ = _run_gpu(q, k, v, variant="fa", **base)
+    for variant in ("blasst", "blasst_rowskip"):
+        o, l, _, st = _run_gpu(q, k, v, variant=variant, lam=None, reorder=False, **base)
+        assert st["skipped"] == 0 and st["rows_masked"] == 0
+        assert torch.equal(o, o_fa) and torch.equal(l, l_fa), variant
+
+
+def test_blasst_fa4_tau_zero_equals_plain_skip():
+    # reference tests/test_sparse.py:184-192: tau = 0 elides only where the max did not rise,
+    # which changes nothing numerically
+    q, k, v = _rand((1, 4, 1024, 128), 141), _rand((1, 2, 1024, 128), 142), _rand((1, 2, 1024, 128), 143)
+    o1, l1, _, s1 = _run_gpu(q, k, v, variant="blasst", lam=1e-3, causal=True, reorder=False)
+    o2, l2, _, s2 = _run_gpu(q, k, v, variant="blasst_fa4", lam=1e-3, tau=0.0, causal=True)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert s1["skipped"] == s2["skipped"]
 
 
 @pytest.mark.parametrize("d", [64, 128])

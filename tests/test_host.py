@@ -40,7 +40,8 @@ def test_library_exports_every_header_symbol(lib):
 def test_params_struct_layout_matches_header():
     from paper_2604_12798_b200._lib import VfaParams
     # 6 int64 + 12 int64 strides + double + 12 int32 + double + 2 int32
-    assert ctypes.sizeof(VfaParams) == 6 * 8 + 12 * 8 + 8 + 12 * 4 + 8 + 2 * 4
+    # + softmax_split (int32) and tau (double)
+    assert ctypes.sizeof(VfaParams) == 6 * 8 + 12 * 8 + 8 + 12 * 4 + 8 + 2 * 4 + 8
 
 
 def _params(**kw):
@@ -60,7 +61,7 @@ def _params(**kw):
 @pytest.mark.parametrize("field,value,code", [
     ("variant", 7, 2), ("kind", 9, 2), ("qkind", 2, 2), ("q_block", 64, 2), ("k_block", 96, 2),
     ("head_dim", 96, 2), ("seq_q", 1000, 3), ("seq_k", 1000, 3), ("heads_q", 3, 3), ("tc1", 99, 2),
-    ("n_sink", -1, 2),
+    ("n_sink", -1, 2), ("tau", -1.0, 2), ("softmax_split", 3, 2), ("variant", 6, 2),
 ])
 def test_check_params_codes(lib, field, value, code):
     assert lib.vfa_check_params(ctypes.byref(_params())) == 0
@@ -130,15 +131,13 @@ def test_op_counters_integer_equal_reference(name):
     m, q, k, v, _, _ = case(name)
     if "counters.blocks_processed" not in m or m["error"]:
         pytest.skip("no counters recorded")
-    kw = {key: m[key] for key in ("kind", "reorder", "use_m_init", "tc1", "lam") if key in m}
+    kw = {key: m[key] for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau", "order") if key in m}
     r = vo.forward_head(q, k, v, variant=m["variant"], causal=m["causal"], q_block=m["q_block"],
                         k_block=m["k_block"], n_sink=m["n_sink"], n_local=m["n_local"], **kw)
-    c = OpCounters()
-    c.charge(r.special, r.frozen, r.skipped, m["q_block"], m["k_block"], q.shape[1],
-             frozen_rowmax=m["variant"] == "vsa")
+    st = dict(visited=r.visited, skipped=r.skipped, special=r.special, frozen=r.frozen,
+              elided=r.elided, rows_masked=r.rows_masked)
+    c = OpCounters.from_stats(m["variant"], st, m["q_block"], m["k_block"], q.shape[1])
     for f, val in c.as_dict().items():
-        if f in ("rescales_elided", "rows_masked"):
-            continue
         assert val == m[f"counters.{f}"], f
 
 

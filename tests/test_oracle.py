@@ -19,7 +19,7 @@ def _kw(m):
     kw = dict(variant=m["variant"], causal=m["causal"], q_block=m["q_block"],
               k_block=m["k_block"], n_sink=m["n_sink"], n_local=m["n_local"],
               raise_errors=False)
-    for key in ("kind", "reorder", "use_m_init", "tc1", "lam"):
+    for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau", "order"):
         if key in m:
             kw[key] = m[key]
     return kw
@@ -43,9 +43,14 @@ def test_oracle_bitwise_equals_reference(name):
     if "stats.blocks_visited" in m:
         assert r.visited == m["stats.blocks_visited"]
         assert r.skipped == m["stats.blocks_skipped"]
-        assert r.special == m["stats.processed_special"]
-        assert r.frozen == m["stats.processed_frozen"]
-    if "counters.rowmax_reductions" in m and m["variant"] != "vsa":
+        if m["variant"] == "vsa":
+            assert r.special == m["stats.processed_special"]
+            assert r.frozen == m["stats.processed_frozen"]
+        if "stats.blocks_processed" in m:
+            assert r.special + r.frozen == m["stats.blocks_processed"]
+            assert r.elided == m["stats.rescales_elided"]
+            assert r.rows_masked == m["stats.rows_masked"]
+    if "counters.rowmax_reductions" in m and m["variant"] in ("fa", "vfa"):
         assert r.special == m["counters.rescale_events"]
     if "mon.count_over_f32" in m:
         assert r.monitor.count_over_f32 == m["mon.count_over_f32"]
