@@ -38,6 +38,13 @@
 extern "C" {
 #endif
 
+/* the library is built with hidden visibility; only these entry points are exported */
+#if defined(__GNUC__)
+#define VFA_API __attribute__((visibility("default")))
+#else
+#define VFA_API
+#endif
+
 #define VFA_OK 0
 #define VFA_ERR_CONFIG 2
 #define VFA_ERR_DATA 3
@@ -104,23 +111,23 @@ typedef struct VfaParams {
 } VfaParams;
 
 /* Host-only validation (no GPU needed). Returns VFA_OK or VFA_ERR_CONFIG / VFA_ERR_DATA. */
-int vfa_check_params(const VfaParams* p);
+VFA_API int vfa_check_params(const VfaParams* p);
 
 /* Bytes of device workspace vfa_fwd needs (key-block representations). */
-size_t vfa_workspace_bytes(const VfaParams* p);
+VFA_API size_t vfa_workspace_bytes(const VfaParams* p);
 
 /* The attention forward. q,k,v: bf16 device; o: bf16 device; lse: float32 device
  * [B,Hq,Lq] (nullable). workspace: >= vfa_workspace_bytes. stats: int64[VFA_STAT_COUNT]
  * (nullable). status: uint32[VFA_STATUS_COUNT] (nullable). skip_trace: uint8
  * [B, Hq, Lq/128, Lk/k_block] (nullable): per visit position, 1 = processed,
  * 2 = skipped, 0 = not visited. stream: cudaStream_t (NULL = legacy default). */
-int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+VFA_API int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
             void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
             unsigned char* skip_trace, void* stream);
 
 /* Bytes of device scratch vfa_fwd_host needs (a ring of per-chunk Q/K/V/O/LSE/workspace
  * slots), or 0 if the parameters or chunking are invalid. */
-size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads);
+VFA_API size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads);
 
 /* End-to-end forward from HOST memory (the reference's own calling convention: arrays in,
  * arrays out). q/k/v/o are dense host bf16 [B,H,L,D] (strides in *p are ignored), lse a
@@ -130,34 +137,34 @@ size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads);
  * library-owned streams. stats/status are device buffers (nullable) accumulated over all
  * chunks with whole-problem row indices. `stream` is made to wait for the last copy, so a
  * synchronize on it means o/lse are in host memory. krepr_precomputed must be 0. */
-int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host,
+VFA_API int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host,
                  void* o_host, float* lse_host, void* scratch, size_t scratch_bytes,
                  long long* stats, unsigned int* status, int chunk_kv_heads, void* stream);
 
 /* Key-block representations only (precompute_kreprs): k bf16 [B,Hkv,Lk,D] ->
  * out bf16 contiguous [B, Hkv, n_blocks, D], n_blocks = tc1 or Lk/k_block. */
-int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream);
+VFA_API int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream);
 
 /* Host mirror of the device tile scheduler (build_schedule, src/vfa.py:146-153,
  * generalised to n_sink/n_local). i is the 1-based query block. Writes up to `cap`
  * visited key blocks (1-based) in visit order to order_out and their special
  * flag to special_out; returns the number visited (vmax) or a negative error. */
-int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local,
+VFA_API int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local,
                  int reorder, int variant, int* order_out, unsigned char* special_out, int cap);
 
 /* Maps a host copy of the status word to VFA_OK / VFA_ERR_NUMERICAL. */
-int vfa_status_code(const unsigned int* status_host);
+VFA_API int vfa_status_code(const unsigned int* status_host);
 
 /* Message for the last non-zero return on this thread. */
-const char* vfa_last_error(void);
+VFA_API const char* vfa_last_error(void);
 
 /* Debug only: when non-NULL, subsequent vfa_fwd calls record clock64() timestamps of the
  * first CTA into device_buffer (long long[Lk/k_block * 8]: per visited block, softmax tile
  * 0/1 "S ready"/"P done", MMA tile 0/1 "P observed"/"next QK issued"). NULL disables. */
-int vfa_debug_trace(long long* device_buffer);
+VFA_API int vfa_debug_trace(long long* device_buffer);
 
 /* Library version string. */
-const char* vfa_version(void);
+VFA_API const char* vfa_version(void);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ namespace vfa_host {
 template <int D, int BC, int NQ, int MODE, int SPLIT>
 int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
-  using C = vfa::Cfg<D, BC, NQ, SPLIT>;
+  using C = vfa::Cfg<D, BC, NQ, SPLIT, MODE>;
   auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT>;
   static bool attr_set = false;
   if (!attr_set) {

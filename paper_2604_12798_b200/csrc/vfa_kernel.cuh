@@ -89,6 +89,10 @@ struct FwdArgs {
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
 
+#ifndef VFA_SB_MAX
+#define VFA_SB_MAX 2  // S buffers per tile (tuning experiments: 1 disables double buffering)
+#endif
+
 // debug timeline slots per visited block (CTA 0 only, builds with -DVFA_TRACE): softmax t:
 // S ready, P done; MMA t: P observed, next QK issued
 constexpr int kTraceSlots = 16;
@@ -103,7 +107,7 @@ constexpr int kTraceSlots = 16;
   } while (0)
 #endif
 
-template <int D, int BC, int NQ, int SPLIT>
+template <int D, int BC, int NQ, int SPLIT, int MODE>
 struct Cfg {
   static constexpr int kQBytes = kBR * D * 2;
   static constexpr int kKVBytes = BC * D * 2;
@@ -119,9 +123,17 @@ struct Cfg {
   static constexpr int kStagesRaw = kAvail / kKVBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kSmem = 1024 + NQ * kQBytes + kStages * kKVBytes + kCtlBytes;
-  // TMEM: S_t (BC fp32 columns; P_t aliased as packed bf16 inside each half's region), O_t.
-  static __host__ __device__ constexpr uint32_t s_off(int t) { return static_cast<uint32_t>(t * 128); }
-  static constexpr int kOBase = NQ * 128;
+  // TMEM: S buffers (BC fp32 columns each; P aliased as packed bf16 inside each part's
+  // region), then O_t. Two S buffers per tile when they fit (BC = 64, or one query tile):
+  // QK of block n+2 is then issued before the softmax of block n+1 starts, so the softmax
+  // never waits on the PV -> QK latency of the previous block. Used for the all-exact modes
+  // only: measured faster for FA at BC = 64, slower for VFA / VSA (profiles/ab_r01_sb.txt).
+  static constexpr int kSB =
+      (NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && all_exact(MODE)) ? 2 : 1;
+  static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
+    return static_cast<uint32_t>(kSB == 2 ? (t * 2 + b) * BC : t * 128);
+  }
+  static constexpr int kOBase = kSB == 2 ? NQ * 2 * BC : NQ * 128;
   static constexpr int kColsUsed = kOBase + NQ * D;
   static constexpr uint32_t kTmemCols = kColsUsed <= 256 ? 256 : 512;
   static_assert(kColsUsed <= 512, "TMEM over-subscribed");
@@ -130,18 +142,19 @@ struct Cfg {
   static_assert(SPLIT == 2 || SPLIT == 4, "SPLIT is 2 (per-tile warp sets) or 4 (all warps, both tiles)");
 };
 
-template <int NS, int NQ>
+template <int NS, int NQ, int SB>
 struct __align__(16) Ctl {
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
-  uint64_t s_full[NQ];     // MMA -> softmax: S of sequence element g ready
-  uint64_t s_free[NQ];     // softmax -> MMA: m-init chunk read (16 warps)
-  uint64_t p_full[NQ][2];  // softmax -> MMA: P chunk c (16 columns of each quarter = one PV
-                           // K-step per quarter) ready / skip decided (16 warps)
+  uint64_t s_full[NQ][SB];     // MMA -> softmax: S of sequence element g ready (buffer g % SB)
+  uint64_t s_free[NQ][SB];     // softmax -> MMA: m-init chunk read
+  uint64_t p_full[NQ][SB][2];  // softmax -> MMA: P chunk c (CW columns of every part) ready /
+                               // skip decided; PV of chunk 0 overlaps the softmax of chunk 1
+  uint64_t pv_done[NQ];        // MMA -> softmax (SB 2): PV before the next exact block done
   uint64_t o_final[NQ];    // MMA -> epilogue: last PV completed
   uint32_t tmem_base;
-  uint32_t skip[NQ];
+  uint32_t skip[NQ][SB];
   float xmax[NQ][2][4][kBR];    // [tile][parity][quarter][row]: quarter-row maxima exchange
   float xl[NQ][4][kBR];         // [tile][quarter][row]: final quarter-row sums
   uint8_t xfin[NQ][4][kBR];     // [tile][quarter][row]: output finite flags
@@ -276,14 +289,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
-  using C = Cfg<D, BC, NQ, SPLIT>;
+  using C = Cfg<D, BC, NQ, SPLIT, MODE>;
   constexpr int NS = C::kStages;
   constexpr int CP = C::kCP;
   constexpr int OP = C::kOP;
   constexpr int NCH = C::kNCH;
   constexpr int CW = C::kCW;
   constexpr int kPoly = poly_pairs();
-  using CtlT = Ctl<NS, NQ>;
+  constexpr int SB = C::kSB;
+  using CtlT = Ctl<NS, NQ, SB>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
 
   extern __shared__ uint8_t smem_raw[];
@@ -299,10 +313,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&ctl->q_full[t], 1);
-      mbar_init(&ctl->s_full[t], 1);
-      mbar_init(&ctl->s_free[t], C::kWarpsPerTile);
-      mbar_init(&ctl->p_full[t][0], C::kWarpsPerTile);
-      mbar_init(&ctl->p_full[t][1], C::kWarpsPerTile);
+      for (int b = 0; b < SB; ++b) {
+        mbar_init(&ctl->s_full[t][b], 1);
+        mbar_init(&ctl->s_free[t][b], C::kWarpsPerTile);
+        mbar_init(&ctl->p_full[t][b][0], C::kWarpsPerTile);
+        mbar_init(&ctl->p_full[t][b][1], C::kWarpsPerTile);
+      }
+      mbar_init(&ctl->pv_done[t], 1);
       mbar_init(&ctl->o_final[t], 1);
     }
     for (int s = 0; s < NS; ++s) {
@@ -364,17 +381,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         };
-        // the MMA warp's consumption order: op(0); per g: [V(g)], op(g+1)
+        // the MMA warp's consumption order: op(0 .. SB-1); per g: [V(g)], op(g+SB)
         auto load_s_operand = [&](int g) {
           if (g < nchunks)
             load_tile(&tmR, g * BC);
           else
             load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
         };
-        load_s_operand(0);
+        for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
         for (int g = 0; g < G; ++g) {
           if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
-          if (g + 1 < G) load_s_operand(g + 1);
+          if (g + SB < G) load_s_operand(g + SB);
         }
       }
     } else if (warp == kMmaWarp) {
@@ -407,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return st;
       };
-      auto issue_qk = [&](int t, int st) {
+      auto issue_qk = [&](int t, int b, int st) {
         const uint32_t a_lo = q_lo + t * (C::kQBytes >> 4) + kLboK;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
 #pragma unroll
@@ -415,14 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
           const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
           if (elect_one())
-            mma_ss(tbase + C::s_off(t), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
+            mma_ss(tbase + C::s_off(t, b), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
                    (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
           __syncwarp();
         }
       };
       // P of part pp occupies TMEM columns [pp*CP, pp*CP + CP/2) of S_t (packed bf16 pairs).
       // PV chunk c: the K-steps over P columns [c*CW, c*CW + CW) of every part.
-      auto issue_pv_chunk = [&](int t, int st, int c, bool& first) {
+      auto issue_pv_chunk = [&](int t, int b, int st, int c, bool& first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
 #pragma unroll
         for (int pp = 0; pp < SPLIT; ++pp) {
@@ -431,34 +448,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int kk = pp * (CP / 16) + c * (CW / 16) + k2;  // K-step (16 key rows of V)
             const uint32_t pcol = pp * CP + c * (CW / 2) + k2 * 8;
             if (elect_one())
-              mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t) + pcol,
+              mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol,
                      (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV, first ? 0u : 1u);
             __syncwarp();
             first = false;
           }
         }
       };
-      uint32_t sfree_ph = 0, p_ph = 0, o_init = 0;
+      uint32_t o_init = 0, p_ph = 0;  // p_ph bit t*SB+b: p_full[t][b] phase (visited blocks only)
       auto issue_s_tile = [&](int g, int t, int st) {
-        // S_t's previous occupant g - 1: an m-init chunk must have been read (s_free);
+        // the buffer's previous occupant g - SB: an m-init chunk must have been read (s_free);
         // a visited block's P was consumed by its PV, issued before this QK
-        if (g >= 1 && g - 1 < nchunks) {
-          mbar_wait(&ctl->s_free[t], (sfree_ph >> t) & 1u);
-          sfree_ph ^= 1u << t;
+        const int b = g % SB;
+        if (g >= SB && g - SB < nchunks) {
+          mbar_wait(&ctl->s_free[t][b], ((g - SB) / SB) & 1);
           tc_fence_after();
         }
-        issue_qk(t, st);
-        commit_elect(&ctl->s_full[t]);
+        issue_qk(t, b, st);
+        commit_elect(&ctl->s_full[t][b]);
       };
-      {
+      for (int g = 0; g < SB && g < G; ++g) {
         const int st = acquire();
-        for (int t = 0; t < NQ; ++t) issue_s_tile(0, t, st);
+        for (int t = 0; t < NQ; ++t) issue_s_tile(g, t, st);
         commit_elect(&ctl->kv_empty[st]);
       }
       for (int g = 0; g < G; ++g) {
         const bool main_blk = g >= nchunks;
         const int pos = g - nchunks;
-        const bool next_s = g + 1 < G;
+        const int b = g % SB;
+        const bool next_s = g + SB < G;
+        // SB 2: the softmax of the next exact-update block rescales O, so it waits for this PV
+        const bool signal_pv = SB == 2 && main_blk && pos + 1 < N &&
+                               (all_exact(MODE) || sched_is_special(sched, sched_block(sched, pos + 1)));
         const int vs = main_blk ? acquire() : -1;
         int ks = -1;
         for (int t = 0; t < NQ; ++t) {
@@ -467,21 +488,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool skip = false;
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-              mbar_wait(&ctl->p_full[t][c], (p_ph >> t) & 1u);
+              mbar_wait(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
               tc_fence_after();
               if (c == 0) {
                 if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
-                skip = skips(MODE) && (ctl->skip[t] != 0);
+                skip = skips(MODE) && (ctl->skip[t][b] != 0);
               }
-              if (!skip) issue_pv_chunk(t, vs, c, first);
+              if (!skip) issue_pv_chunk(t, b, vs, c, first);
             }
-            p_ph ^= 1u << t;
+            p_ph ^= 1u << (t * SB + b);
             if (!skip) o_init |= 1u << t;
+            if (signal_pv) commit_elect(&ctl->pv_done[t]);
             if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
           }
           if (next_s) {
             if (t == 0) ks = acquire();
-            issue_s_tile(g + 1, t, ks);
+            issue_s_tile(g + SB, t, ks);
             if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 5 + 2 * t);
           }
         }
@@ -515,9 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         l[ti] = 0.f;
         xpar[ti] = 0;
       }
-      uint32_t s_ph = 0;  // bit ti: s_full phase
       uint32_t over32 = 0, over16 = 0;
-      auto tS = [&](int t) { return tbase + C::s_off(t) + part * CP + lane_off; };
+      uint32_t pv_ph = 0;  // bit ti: pv_done phase (SB 2)
+      auto tS = [&](int t, int b) { return tbase + C::s_off(t, b) + part * CP + lane_off; };
       auto tO = [&](int t) { return tbase + C::kOBase + t * D + part * OP + lane_off; };
       // row-max exchange across the SPLIT parts of a row (named barrier 1 + t)
       auto exchange_max = [&](int ti, int t, float mine) -> float {
@@ -529,17 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         xpar[ti] ^= 1;
         return m;
       };
-      auto wait_s = [&](int ti, int t) {
-        mbar_wait(&ctl->s_full[t], (s_ph >> ti) & 1u);
-        s_ph ^= 1u << ti;
+      // sequence element g (m-init chunks, then visited blocks) lives in S buffer g % SB
+      auto wait_s = [&](int t, int g) {
+        mbar_wait(&ctl->s_full[t][g % SB], (g / SB) & 1);
         tc_fence_after();
       };
-      auto load_part = [&](int t, float* v) {
+      auto load_part = [&](int t, int b, float* v) {
         if constexpr (CP >= 32) {
 #pragma unroll
-          for (int c = 0; c < CP / 32; ++c) tmem_ld32(tS(t) + c * 32, v + c * 32);
+          for (int c = 0; c < CP / 32; ++c) tmem_ld32(tS(t, b) + c * 32, v + c * 32);
         } else {
-          tmem_ld16(tS(t), v);
+          tmem_ld16(tS(t, b), v);
         }
         tmem_wait_ld();
         if constexpr (CP >= 32) {
@@ -560,15 +582,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int ti = 0; ti < NT; ++ti) {
             const int t = tile0 + ti;
-            wait_s(ti, t);
+            wait_s(t, ch);
             float v[CP];
-            load_part(t, v);
+            load_part(t, ch % SB, v);
 #pragma unroll
             for (int e = 0; e < CP; ++e)
               if (e < valid) mx[ti] = fmaxf(mx[ti], v[e]);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl->s_free[t]);
+            if (lane == 0) mbar_arrive(&ctl->s_free[t][ch % SB]);
           }
         }
 #pragma unroll
@@ -586,17 +608,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ti = 0; ti < NT; ++ti) {
           const int t = tile0 + ti;
-          wait_s(ti, t);
+          const int g = nchunks + pos;
+          const int b = g % SB;
+          wait_s(t, g);
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
           float v[CP];
-          load_part(t, v);
+          load_part(t, b, v);
           if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
 #pragma unroll
             for (int e = 0; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
           }
           bool skipped = false;
+          bool rescale = false;  // this block rescales O by f (exact update, not skipped / elided)
+          float f = 1.0f;
           if (MODE != kVFA || special) {
-            // ---- exact-update / skip-test block: rowmax over the full row (four quarters,
+            // ---- exact-update / skip-test block: rowmax over the full row (all parts,
             //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
             float mt = -INFINITY;
 #pragma unroll
@@ -629,39 +655,44 @@ __global__ void __launch_bounds__(kThreads, 1)
               // (warp-uniform branch: skipped / elide are CTA-wide decisions) rowskip: a
               // suppressed row keeps factor 1 and its max, and adds zero mass (src/sparse.py:241-247)
               const bool upd = (MODE != kBLR) || keep;
-              const float f = (!upd || m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
+              f = (!upd || m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
               if (upd) m2[ti] = m2n;
               if (!upd) {
 #pragma unroll
                 for (int e = 0; e < CP; ++e) v[e] = -INFINITY;
               }
               l[ti] = __fmul_rn(l[ti], f);  // no FMA contraction: identical l-recurrence in every mode
-              // rescale this part of O in TMEM (src/core.py:91). O is quiescent here: PV(pos-1)
-              // completed before S(pos) (in-order tensor pipe), PV(pos) waits for p_full.
-              const bool work = (pos > 0) && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
-              if (work) {
-                const float2 f2 = make_float2(f, f);
-#pragma unroll(SPLIT == 4 ? 2 : 1)
-                for (int c = 0; c < OP / 16; ++c) {
-                  float o[16];
-                  tmem_ld16(tO(t) + c * 16, o);
-                  tmem_wait_ld();
-                  reg_fence16(o);
-                  uint32_t u[16];
-#pragma unroll
-                  for (int e = 0; e < 16; e += 2) {
-                    const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
-                    u[e] = __float_as_uint(x.x);
-                    u[e + 1] = __float_as_uint(x.y);
-                  }
-                  tmem_st16(tO(t) + c * 16, u);
-                }
-              }
+              rescale = pos > 0 && ((MODE == kFA) || !__all_sync(0xffffffffu, f == 1.0f));
             }
           }
+          // rescale this part of O in TMEM (src/core.py:91) before PV(pos) accumulates into it
+          auto rescale_o = [&]() {
+            const float2 f2 = make_float2(f, f);
+#pragma unroll(SPLIT == 4 ? 2 : 1)
+            for (int c = 0; c < OP / 16; ++c) {
+              float o[16];
+              tmem_ld16(tO(t) + c * 16, o);
+              tmem_wait_ld();
+              reg_fence16(o);
+              uint32_t u[16];
+#pragma unroll
+              for (int e = 0; e < 16; e += 2) {
+                const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+                u[e] = __float_as_uint(x.x);
+                u[e + 1] = __float_as_uint(x.y);
+              }
+              tmem_st16(tO(t) + c * 16, u);
+            }
+          };
+          // SB 1: O is quiescent here (PV(pos-1) completed before S(pos): in-order tensor pipe).
+          // SB 2: S(pos) was computed before PV(pos-1) was issued, so an exact block waits for
+          // PV(pos-1) (pv_done, committed by the MMA warp ahead of every exact block) and hands
+          // its P over only after the rescale.
+          const bool defer = SB == 2 && special && pos > 0;
+          if (SB == 1 && rescale) rescale_o();
           // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
           if (r == 0 && part == 0) {
-            if (skips(MODE)) ctl->skip[t] = skipped ? 1u : 0u;
+            if (skips(MODE)) ctl->skip[t][b] = skipped ? 1u : 0u;
             if (a.skip_trace) {
               const size_t idx =
                   ((static_cast<size_t>(unit.b) * a.Hq + unit.h0 + t) * a.Tr + unit.qt) * a.Tc + pos;
@@ -681,18 +712,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p_chunk<CW, true, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
               else
                 p_chunk<CW, false, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
-              if constexpr (CW == 32) tmem_st16(tS(t) + c * 16, u);
-              else tmem_st8(tS(t) + c * 8, u);
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
+              if constexpr (CW == 32) tmem_st16(tS(t, b) + c * 16, u);
+              else tmem_st8(tS(t, b) + c * 8, u);
+              if (!defer) {
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ctl->p_full[t][b][c]);
+              }
             }
             l[ti] = __fadd_rn(l[ti], __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
-          } else {
+          }
+          if (defer) {
+            mbar_wait(&ctl->pv_done[t], (pv_ph >> ti) & 1u);
+            pv_ph ^= 1u << ti;
+            tc_fence_after();
+            if (rescale) rescale_o();
+          }
+          if (skipped || defer) {
+            tmem_wait_st();
+            tc_fence_before();
             __syncwarp();
             if (lane == 0)
-              for (int c = 0; c < NCH; ++c) mbar_arrive(&ctl->p_full[t][c]);
+              for (int c = 0; c < NCH; ++c) mbar_arrive(&ctl->p_full[t][b][c]);
           }
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
         }

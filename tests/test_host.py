@@ -25,7 +25,7 @@ def lib():
 
 def _header_symbols():
     txt = open(os.path.join(ROOT, "include", "vfa_b200.h")).read()
-    return sorted(set(re.findall(r"^(?:int|size_t|const char\*)\s+(vfa_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^VFA_API\s+(?:int|size_t|const char\*)\s+(vfa_\w+)\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol(lib):
