@@ -270,7 +270,7 @@ def time_interleaved(runners, steps, flush, barrier):
     return out
 
 
-def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam, chunk=1):
+def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam, chunk=1, qchunk=2):
     """End-to-end through the public API on HOST tensors: attention_forward(q_h, k_h, v_h)
     with page-locked inputs runs the library's pipelined path (chunked H2D copy, kernels,
     D2H copy of O + LSE on overlapping streams); timed with CUDA events on the caller's
@@ -284,7 +284,7 @@ def e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, steps, variant, lam, chunk=1):
         torch.cuda.synchronize()
         e0.record(stream)
         attention_forward_host(q_h, k_h, v_h, variant=variant, causal=True, lam=lam, out=o_h, lse=lse_h,
-                               check=False, chunk_kv_heads=chunk)
+                               check=False, chunk_kv_heads=chunk, chunk_q_heads=qchunk)
         e1.record(stream)
         torch.cuda.synchronize()
         total += e0.elapsed_time(e1)
@@ -381,9 +381,9 @@ def main_ours(args):
         v_h = v.cpu().pin_memory()
         o_h = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
         lse_h = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
-        e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, 1, "vfa", None, args.e2e_chunk)  # warm-up
+        e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, 1, "vfa", None, args.e2e_chunk, args.e2e_qchunk)  # warm-up
         e2e_ms, h2d, d2h = e2e_steps(q_h, k_h, v_h, o_h, lse_h, dev, args.e2e_steps, "vfa", None,
-                                     args.e2e_chunk)
+                                     args.e2e_chunk, args.e2e_qchunk)
         e2e_equal = bool(torch.equal(o_h, runners["vfa"].o.cpu()) and torch.equal(lse_h, runners["vfa"].lse.cpu()))
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
@@ -444,7 +444,7 @@ def main_ours(args):
                            "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
                            "d2h_bytes_per_step": d2h, "bitwise_equal_to_device_run": e2e_equal,
                            "api": "paper_2604_12798_b200.attention_forward on page-locked host tensors (library-pipelined H2D / kernels / D2H)",
-                           "chunk_kv_heads": args.e2e_chunk}
+                           "chunk_kv_heads": args.e2e_chunk, "chunk_q_heads": args.e2e_qchunk}
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -529,6 +529,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="KV heads per pipelined host chunk")
+    ap.add_argument("--e2e-qchunk", type=int, default=2, help="query heads per pipelined sub-chunk (0: all)")
     ap.add_argument("--cpu-core-seconds", type=float, default=24.0)
     ap.add_argument("--cpu-core-seconds-ref", type=float, default=2.5,
                     help="per-step wall seconds of the reference arm (x cores)")

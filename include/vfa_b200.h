@@ -125,21 +125,24 @@ VFA_API int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void
             void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
             unsigned char* skip_trace, void* stream);
 
-/* Bytes of device scratch vfa_fwd_host needs (a ring of per-chunk Q/K/V/O/LSE/workspace
- * slots), or 0 if the parameters or chunking are invalid. */
-VFA_API size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads);
+/* Bytes of device scratch vfa_fwd_host needs (up to four K/V group slots and eight query
+ * sub-chunk slots), or 0 if the parameters or the chunking are invalid. */
+VFA_API size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads, int chunk_q_heads);
 
 /* End-to-end forward from HOST memory (the reference's own calling convention: arrays in,
  * arrays out). q/k/v/o are dense host bf16 [B,H,L,D] (strides in *p are ignored), lse a
  * dense host float32 [B,Hq,Lq] (nullable); page-locked host memory gives full overlap.
- * The problem is pipelined in chunks of (one batch, chunk_kv_heads KV heads + their GQA
- * query heads): H2D copy, attention kernels and D2H copy of consecutive chunks overlap on
- * library-owned streams. stats/status are device buffers (nullable) accumulated over all
- * chunks with whole-problem row indices. `stream` is made to wait for the last copy, so a
- * synchronize on it means o/lse are in host memory. krepr_precomputed must be 0. */
+ * The problem is pipelined in K/V groups (one batch, chunk_kv_heads KV heads, copied once)
+ * and query sub-chunks (chunk_q_heads consecutive query heads of a group; 0 = the whole
+ * group; a value below the GQA group requires chunk_kv_heads = 1): H2D copies, attention
+ * kernels and D2H copies of consecutive sub-chunks overlap on library-owned streams.
+ * stats/status are device buffers (nullable) accumulated over all chunks with whole-problem
+ * row indices. `stream` is made to wait for the last copy, so a synchronize on it means
+ * o/lse are in host memory. krepr_precomputed must be 0. */
 VFA_API int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host,
-                 void* o_host, float* lse_host, void* scratch, size_t scratch_bytes,
-                 long long* stats, unsigned int* status, int chunk_kv_heads, void* stream);
+                         void* o_host, float* lse_host, void* scratch, size_t scratch_bytes,
+                         long long* stats, unsigned int* status, int chunk_kv_heads, int chunk_q_heads,
+                         void* stream);
 
 /* Key-block representations only (precompute_kreprs): k bf16 [B,Hkv,Lk,D] ->
  * out bf16 contiguous [B, Hkv, n_blocks, D], n_blocks = tc1 or Lk/k_block. */

@@ -76,9 +76,10 @@ def bind(path: str):
     lib.vfa_workspace_bytes.restype = ctypes.c_size_t
     lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     lib.vfa_fwd.restype = ctypes.c_int
-    lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int]
+    lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int, ctypes.c_int]
     lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
-    lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, vp]
+    lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, ctypes.c_int,
+                                 vp]
     lib.vfa_fwd_host.restype = ctypes.c_int
     lib.vfa_krepr.argtypes = [P, vp, vp, vp]
     lib.vfa_krepr.restype = ctypes.c_int

@@ -447,11 +447,14 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
                            scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True,
                            tc1=None, n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None,
                            lse=None,
-                           check=True, stream=None, device=None, chunk_kv_heads=1, softmax_split=0):
+                           check=True, stream=None, device=None, chunk_kv_heads=1, chunk_q_heads=2,
+                           softmax_split=0):
     """The forward on HOST tensors (bf16 [B, Hq, Lq, d] / [B, Hkv, Lk, d], contiguous;
     page-locked for full overlap) -> host (O bf16, LSE fp32, info), through the C ABI's
     vfa_fwd_host: chunks of `chunk_kv_heads` KV heads are copied in, computed and copied
-    out on overlapping streams, so the PCIe transfers hide behind the attention kernels.
+    out on overlapping streams, so the PCIe transfers hide behind the attention kernels;
+    each KV head's K/V is copied once and its query heads go in sub-chunks of chunk_q_heads
+    (when chunk_kv_heads == 1 and it divides the GQA group; else whole groups).
     The result is in host memory when this returns (check=True) or once `stream` (default:
     the current stream of `device`) is synchronized (check=False)."""
     lib = _lib.load()
@@ -480,7 +483,9 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)
-    nbytes = int(lib.vfa_host_scratch_bytes(ctypes.byref(p), int(chunk_kv_heads)))
+    group = q.shape[1] // k.shape[1]
+    cq = int(chunk_q_heads) if (chunk_kv_heads == 1 and chunk_q_heads and group % chunk_q_heads == 0) else 0
+    nbytes = int(lib.vfa_host_scratch_bytes(ctypes.byref(p), int(chunk_kv_heads), cq))
     if nbytes == 0:
         raise ValueError(f"chunk_kv_heads={chunk_kv_heads} must divide heads_kv={k.shape[1]}")
     with torch.cuda.device(dev):
@@ -490,7 +495,7 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
         st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         rc = lib.vfa_fwd_host(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr(), scratch.data_ptr(), nbytes, stats.data_ptr(),
-                              status.data_ptr(), int(chunk_kv_heads), ctypes.c_void_p(st))
+                              status.data_ptr(), int(chunk_kv_heads), cq, ctypes.c_void_p(st))
     if rc:
         _raise_for(rc)
     info = {"stats": stats, "status": status, "skip_trace": None, "workspace": None}

@@ -246,44 +246,65 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
 }
 
 // ---------------------------------------------------------------- host-resident pipeline
-// vfa_fwd_host: the problem is cut into chunks of (one batch, `ck` KV heads with their GQA
-// query heads). Chunk c is copied host->device on the H2D stream into scratch slot c % S,
-// computed on compute stream c % 2 (so one chunk's causal tail overlaps the next chunk's
-// head), and its O / LSE copied back on the D2H stream, so PCIe transfers in both
-// directions overlap the attention kernels.
+// vfa_fwd_host: the problem is cut into K/V groups (one batch, `ck` KV heads) and each group
+// into query sub-chunks (`nqs` consecutive query heads of the group). A group's K and V are
+// copied host->device once into one of two K/V slots (and its key-block representations
+// computed there); each sub-chunk's Q is copied into one of three Q/O
+// slots, computed on compute stream c % 2 (one sub-chunk's causal tail overlaps the next
+// one's head) and its O / LSE copied back on the D2H stream. PCIe transfers in both
+// directions overlap the attention kernels; small sub-chunks keep the exposed head (first
+// copy) and tail (last kernel + last copy-back) of the pipeline short.
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-struct ChunkGeom {
-  int64_t ck, nq, chunks, slots;
-  size_t q_bytes, kv_bytes, lse_bytes, ws_bytes, slot_bytes;
-  VfaParams cp;  // the per-chunk problem (dense device layout)
+struct HostPlan {
+  int64_t ck = 0, nqs = 0, subs = 0, groups = 0, chunks = 0, kv_slots = 0, q_slots = 0;
+  size_t q_bytes = 0, kv_bytes = 0, lse_bytes = 0, ws_bytes = 0, kv_slot_bytes = 0, q_slot_bytes = 0;
+  bool minit = false;
+  VfaParams cp{};  // the per-sub-chunk problem (dense device layout)
 };
 
-ChunkGeom chunk_geom(const VfaParams* p, int chunk_kv_heads) {
-  ChunkGeom g{};
-  g.ck = chunk_kv_heads;
+// chunk_q_heads = 0: all query heads of the group; otherwise it must divide the GQA group
+// and requires chunk_kv_heads == 1 (the sub-chunk's query heads are then contiguous).
+bool host_plan(const VfaParams* p, int chunk_kv_heads, int chunk_q_heads, HostPlan* out) {
+  if (chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads || chunk_q_heads < 0) return false;
   const int64_t group = p->heads_q / p->heads_kv;
-  g.nq = g.ck * group;
-  g.chunks = p->batch * (p->heads_kv / g.ck);
-  g.slots = g.chunks < 3 ? g.chunks : 3;
+  HostPlan g;
+  g.ck = chunk_kv_heads;
+  if (chunk_q_heads == 0 || chunk_q_heads >= group) {
+    g.nqs = g.ck * group;
+  } else {
+    if (group % chunk_q_heads || g.ck != 1) return false;
+    g.nqs = chunk_q_heads;
+  }
+  g.subs = g.ck * group / g.nqs;
+  g.groups = p->batch * (p->heads_kv / g.ck);
+  g.chunks = g.groups * g.subs;
+  // enough slots that the copy stream never waits on a slot in steady state (the copy-in
+  // runs ahead of the kernels by up to ~2 groups; HBM is plentiful, PCIe is the bottleneck)
+  g.kv_slots = g.groups < 4 ? g.groups : 4;
+  g.q_slots = g.chunks < 8 ? g.chunks : 8;
+  g.minit = (p->variant == VFA_VARIANT_VFA || p->variant == VFA_VARIANT_VSA) && p->use_m_init;
   g.cp = *p;
   g.cp.batch = 1;
-  g.cp.heads_q = g.nq;
+  g.cp.heads_q = g.nqs;
   g.cp.heads_kv = g.ck;
+  g.cp.krepr_precomputed = g.minit ? 1 : 0;  // computed once per K/V group on the copy stream
   const int64_t D = p->head_dim;
-  const int64_t qs[3] = {g.nq * p->seq_q * D, p->seq_q * D, D};
+  const int64_t qs[3] = {g.nqs * p->seq_q * D, p->seq_q * D, D};
   const int64_t ks[3] = {g.ck * p->seq_k * D, p->seq_k * D, D};
   for (int i = 0; i < 3; ++i) {
     g.cp.q_stride[i] = g.cp.o_stride[i] = qs[i];
     g.cp.k_stride[i] = g.cp.v_stride[i] = ks[i];
   }
-  g.q_bytes = static_cast<size_t>(g.nq * p->seq_q * D * 2);
+  g.q_bytes = static_cast<size_t>(g.nqs * p->seq_q * D * 2);
   g.kv_bytes = static_cast<size_t>(g.ck * p->seq_k * D * 2);
-  g.lse_bytes = static_cast<size_t>(g.nq * p->seq_q * 4);
+  g.lse_bytes = static_cast<size_t>(g.nqs * p->seq_q * 4);
   g.ws_bytes = vfa_workspace_bytes(&g.cp);
-  g.slot_bytes = 2 * align_up(g.q_bytes) + 2 * align_up(g.kv_bytes) + align_up(g.lse_bytes) + align_up(g.ws_bytes);
-  return g;
+  g.kv_slot_bytes = 2 * align_up(g.kv_bytes) + align_up(g.ws_bytes);
+  g.q_slot_bytes = 2 * align_up(g.q_bytes) + align_up(g.lse_bytes);
+  *out = g;
+  return true;
 }
 
 struct HostStreams {
@@ -312,29 +333,33 @@ int host_streams(HostStreams** out) {
 
 extern "C" {
 
-size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads) {
-  if (!p || vfa_check_params(p) != VFA_OK || chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads) return 0;
-  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
-  return static_cast<size_t>(g.slots) * g.slot_bytes + kAlign;
+size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads, int chunk_q_heads) {
+  HostPlan g;
+  if (!p || vfa_check_params(p) != VFA_OK || !host_plan(p, chunk_kv_heads, chunk_q_heads, &g)) return 0;
+  return static_cast<size_t>(g.kv_slots) * g.kv_slot_bytes + static_cast<size_t>(g.q_slots) * g.q_slot_bytes + kAlign;
 }
 
 int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, const void* v_host, void* o_host,
                  float* lse_host, void* scratch, size_t scratch_bytes, long long* stats, unsigned int* status,
-                 int chunk_kv_heads, void* stream) {
+                 int chunk_kv_heads, int chunk_q_heads, void* stream) {
   int rc = vfa_check_params(p);
   if (rc) return rc;
   if (!q_host || !k_host || !v_host || !o_host) return fail(VFA_ERR_DATA, "NULL host pointer");
-  if (chunk_kv_heads < 1 || p->heads_kv % chunk_kv_heads)
-    return fail(VFA_ERR_CONFIG, "chunk_kv_heads must divide heads_kv");
+  HostPlan g;
+  if (!host_plan(p, chunk_kv_heads, chunk_q_heads, &g))
+    return fail(VFA_ERR_CONFIG,
+                "chunk_kv_heads must divide heads_kv; chunk_q_heads must be 0 or divide the GQA group "
+                "(with chunk_kv_heads = 1)");
   if (p->krepr_precomputed) return fail(VFA_ERR_CONFIG, "vfa_fwd_host computes the representations itself");
-  const size_t need = vfa_host_scratch_bytes(p, chunk_kv_heads);
+  const size_t need = vfa_host_scratch_bytes(p, chunk_kv_heads, chunk_q_heads);
   if (!scratch || scratch_bytes < need) return fail(VFA_ERR_DATA, "scratch too small (vfa_host_scratch_bytes)");
-  const ChunkGeom g = chunk_geom(p, chunk_kv_heads);
   HostStreams* hs = nullptr;
   rc = host_streams(&hs);
   if (rc) return rc;
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(scratch) + kAlign - 1) & ~uintptr_t(kAlign - 1));
+  uint8_t* kv_base = base;
+  uint8_t* q_base = base + g.kv_slots * g.kv_slot_bytes;
 
   std::vector<cudaEvent_t> ev;
   auto new_event = [&]() -> cudaEvent_t {
@@ -357,42 +382,62 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
 
   const int64_t D = p->head_dim, group = p->heads_q / p->heads_kv;
   const int64_t per_b = p->heads_kv / g.ck;
-  std::vector<cudaEvent_t> slot_free(static_cast<size_t>(g.slots), nullptr);
-  for (int64_t c = 0; c < g.chunks; ++c) {
-    const int64_t b = c / per_b, kv0 = (c % per_b) * g.ck, h0 = kv0 * group;
-    const int64_t s = c % g.slots;
-    uint8_t* sl = base + s * g.slot_bytes;
-    uint8_t* dq = sl;
-    uint8_t* dk = dq + align_up(g.q_bytes);
+  std::vector<cudaEvent_t> kv_free(static_cast<size_t>(g.kv_slots), nullptr);
+  std::vector<cudaEvent_t> q_free(static_cast<size_t>(g.q_slots), nullptr);
+  int64_t c = 0;  // global sub-chunk counter
+  for (int64_t gi = 0; gi < g.groups; ++gi) {
+    const int64_t b = gi / per_b, kv0 = (gi % per_b) * g.ck;
+    uint8_t* kvs = kv_base + (gi % g.kv_slots) * g.kv_slot_bytes;
+    uint8_t* dk = kvs;
     uint8_t* dv = dk + align_up(g.kv_bytes);
-    uint8_t* dout = dv + align_up(g.kv_bytes);
-    float* dlse = reinterpret_cast<float*>(dout + align_up(g.q_bytes));
-    uint8_t* dws = reinterpret_cast<uint8_t*>(dlse) + align_up(g.lse_bytes);
-    const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
+    uint8_t* dws = dv + align_up(g.kv_bytes);
     const size_t koff = static_cast<size_t>((b * p->heads_kv + kv0) * p->seq_k * D) * 2;
-    const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
-    // H2D (after the slot's previous chunk has been copied out)
-    if (slot_free[s]) cudaStreamWaitEvent(hs->h2d, slot_free[s], 0);
+    // K/V of the group (after every sub-chunk that used this slot has been copied out)
+    if (kv_free[gi % g.kv_slots]) cudaStreamWaitEvent(hs->h2d, kv_free[gi % g.kv_slots], 0);
     cudaMemcpyAsync(dk, static_cast<const uint8_t*>(k_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
     cudaMemcpyAsync(dv, static_cast<const uint8_t*>(v_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
-    cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, g.q_bytes, cudaMemcpyHostToDevice, hs->h2d);
-    cudaEvent_t in = new_event(), done = new_event(), out = new_event();
-    if (!in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
-    cudaEventRecord(in, hs->h2d);
-    // compute
-    cudaStream_t cs = hs->comp[c & 1];
-    cudaStreamWaitEvent(cs, in, 0);
-    rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, cs, false,
-                      static_cast<long long>(loff));
-    if (rc) return cleanup(), rc;
-    cudaEventRecord(done, cs);
-    // D2H
-    cudaStreamWaitEvent(hs->d2h, done, 0);
-    cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
-    if (lse_host)
-      cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
-    cudaEventRecord(out, hs->d2h);
-    slot_free[s] = out;
+    cudaEvent_t kv_in = new_event();
+    if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+    cudaEventRecord(kv_in, hs->h2d);
+    if (g.minit) {
+      // representations once per group, on the compute stream of its first sub-chunk (a kernel
+      // on the copy stream would stall the copies behind the running attention kernels)
+      cudaStream_t cs0 = hs->comp[c & 1];
+      cudaStreamWaitEvent(cs0, kv_in, 0);
+      rc = launch_krepr(&g.cp, dk, dws, cs0);
+      if (rc) return cleanup(), rc;
+      kv_in = new_event();
+      if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+      cudaEventRecord(kv_in, cs0);
+    }
+    for (int64_t si = 0; si < g.subs; ++si, ++c) {
+      const int64_t h0 = kv0 * group + si * g.nqs;
+      uint8_t* qsl = q_base + (c % g.q_slots) * g.q_slot_bytes;
+      uint8_t* dq = qsl;
+      uint8_t* dout = dq + align_up(g.q_bytes);
+      float* dlse = reinterpret_cast<float*>(dout + align_up(g.q_bytes));
+      const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
+      const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
+      if (q_free[c % g.q_slots]) cudaStreamWaitEvent(hs->h2d, q_free[c % g.q_slots], 0);
+      cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, g.q_bytes, cudaMemcpyHostToDevice, hs->h2d);
+      cudaEvent_t q_in = new_event(), done = new_event(), out = new_event();
+      if (!q_in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+      cudaEventRecord(q_in, hs->h2d);
+      cudaStream_t cs = hs->comp[c & 1];
+      cudaStreamWaitEvent(cs, kv_in, 0);
+      cudaStreamWaitEvent(cs, q_in, 0);
+      rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, cs, false,
+                        static_cast<long long>(loff));
+      if (rc) return cleanup(), rc;
+      cudaEventRecord(done, cs);
+      cudaStreamWaitEvent(hs->d2h, done, 0);
+      cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
+      if (lse_host) cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
+      cudaEventRecord(out, hs->d2h);
+      q_free[c % g.q_slots] = out;
+      // the D2H stream has waited for every sub-chunk's kernel of this group by now
+      if (si + 1 == g.subs) kv_free[gi % g.kv_slots] = out;
+    }
   }
   cudaEvent_t exit_ev = new_event();
   if (!exit_ev) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
@@ -407,12 +452,17 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
 int vfa_schedule(int i, int q_block, int k_block, int t_c, int causal, int n_sink, int n_local, int reorder,
                  int variant, int* order_out, unsigned char* special_out, int cap) {
   if (i < 1 || q_block < 1 || k_block < 1 || t_c < 1) return -VFA_ERR_CONFIG;
+  // the device's unit_schedule: FA / BLASST-FA4 / rowskip ascending; BLASST may reorder
+  // (1 sink + 1 local); every block of the FA-like variants is exact
+  const bool seq = variant == VFA_VARIANT_FA || variant == VFA_VARIANT_BLASST_FA4 || variant == VFA_VARIANT_BLASST_ROWSKIP;
+  const bool all_exact = seq || variant == VFA_VARIANT_BLASST;
+  if (variant >= VFA_VARIANT_BLASST) n_sink = n_local = 1;
   vfa::TileSchedule s = vfa::make_schedule(i, q_block, k_block, t_c, causal != 0, n_sink, n_local,
-                                           variant != VFA_VARIANT_FA && reorder != 0, variant == VFA_VARIANT_FA);
+                                           !seq && reorder != 0, seq);
   for (int pos = 0; pos < s.vmax && pos < cap; ++pos) {
     int j = vfa::sched_block(s, pos);
     if (order_out) order_out[pos] = j;
-    if (special_out) special_out[pos] = vfa::sched_is_special(s, j) ? 1 : 0;
+    if (special_out) special_out[pos] = (all_exact || vfa::sched_is_special(s, j)) ? 1 : 0;
   }
   return s.vmax;
 }

@@ -414,17 +414,22 @@ def test_dropin_api_mirrors_reference():
     assert c3.rowmax_reductions == stats.blocks_visited
 
 
-@pytest.mark.parametrize("variant,chunk,b", [("vfa", 1, 1), ("fa", 2, 1), ("vsa", 1, 2), ("vfa", 4, 2)])
-def test_host_pipeline_bitwise_equals_device_path(variant, chunk, b):
+@pytest.mark.parametrize("variant,chunk,qchunk,b", [("vfa", 1, 2, 1), ("fa", 2, 0, 1), ("vsa", 1, 1, 2),
+                                                     ("vfa", 4, 0, 2), ("blasst_fa4", 1, 0, 1)])
+def test_host_pipeline_bitwise_equals_device_path(variant, chunk, qchunk, b):
     # vfa_fwd_host (chunked H2D / kernels / D2H) computes exactly what vfa_fwd computes
     from paper_2604_12798_b200 import attention_forward, stats_dict
     L, Hq, Hkv = 1024, 8, 4
     q, k, v = _rand((b, Hq, L, 128), 101), _rand((b, Hkv, L, 128), 102), _rand((b, Hkv, L, 128), 103)
-    kw = dict(variant=variant, causal=True, lam=1e-2 if variant == "vsa" else None)
+    kw = dict(variant=variant, causal=True, lam=1e-2 if variant != "vfa" else None)
+    if qchunk == 1:  # one query head per kernel launch runs the 4-way softmax split: match it
+        kw["softmax_split"] = 4
+    if variant == "blasst_fa4":
+        kw["tau"] = 2.0
     o1, l1, i1, st1 = _run_gpu(q, k, v, **kw)
     qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
     from paper_2604_12798_b200 import attention_forward_host
-    o2, l2, i2 = attention_forward_host(qh, kh, vh, chunk_kv_heads=chunk, **kw)
+    o2, l2, i2 = attention_forward_host(qh, kh, vh, chunk_kv_heads=chunk, chunk_q_heads=qchunk, **kw)
     assert o2.device.type == "cpu" and l2.device.type == "cpu"
     assert torch.equal(o1.cpu(), o2) and torch.equal(l1.cpu(), l2)
     assert stats_dict(i2) == st1
@@ -447,5 +452,5 @@ def test_host_pipeline_reports_whole_problem_row():
     q[1, 1], k[1, 1], v[1, 1] = qb, kb, vb
     with pytest.raises(NormalizerUnderflowError) as ei:
         attention_forward_host(q, k, v, variant="vfa", kind=m["kind"], causal=m["causal"],
-                               k_block=m["k_block"], chunk_kv_heads=1)
+                               k_block=m["k_block"], chunk_kv_heads=1, chunk_q_heads=1)
     assert ei.value.row == (1 * H + 1) * L + int(m["error"].split(":")[1])

@@ -168,12 +168,16 @@ def test_entry_points_fail_loudly_without_library(monkeypatch, tmp_path):
 
 
 def test_host_scratch_bytes(lib):
-    p = _params()  # B=1, Hq=4, Hkv=2, L=1024, d=128
-    one = lib.vfa_host_scratch_bytes(ctypes.byref(p), 1)
-    two = lib.vfa_host_scratch_bytes(ctypes.byref(p), 2)
-    # a slot holds Q + O (2 query heads) + K + V (1 KV head) + LSE + the representation workspace
-    slot = 2 * (2 * 1024 * 128 * 2) + 2 * (1024 * 128 * 2) + 2 * 1024 * 4
-    assert one >= 2 * slot and two >= slot
-    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 3) == 0  # 3 does not divide Hkv = 2
-    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 0) == 0
-    assert lib.vfa_host_scratch_bytes(ctypes.byref(_params(k_block=96)), 1) == 0
+    p = _params()  # B=1, Hq=4, Hkv=2 (GQA group 2), L=1024, d=128
+    one = lib.vfa_host_scratch_bytes(ctypes.byref(p), 1, 0)
+    two = lib.vfa_host_scratch_bytes(ctypes.byref(p), 2, 0)
+    sub = lib.vfa_host_scratch_bytes(ctypes.byref(p), 1, 1)
+    # K/V slots (2 x [K, V, representations] of one KV head) + Q/O/LSE slots (2 query heads)
+    kv_slot = 2 * (1024 * 128 * 2)
+    q_slot = 2 * (2 * 1024 * 128 * 2) + 2 * 1024 * 4
+    assert one >= 2 * kv_slot + 2 * q_slot  # 2 groups -> 2 K/V slots, 2 chunks -> 2 Q slots
+    assert two >= kv_slot * 2 and sub < one * 2
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 3, 0) == 0  # 3 does not divide Hkv = 2
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 0, 0) == 0
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 2, 1) == 0  # query sub-chunks need 1 KV head
+    assert lib.vfa_host_scratch_bytes(ctypes.byref(_params(k_block=96)), 1, 0) == 0
