@@ -230,7 +230,7 @@ class Runner:
     def attn(self, stream):
         rc = self.lib.vfa_fwd(self.ctypes.byref(self.p), self.q.data_ptr(), self.k.data_ptr(),
                               self.v.data_ptr(), self.o.data_ptr(), self.lse.data_ptr(), self.ws.data_ptr(),
-                              self.ws_bytes, self.stats.data_ptr(), self.status.data_ptr(), None,
+                              self.ws_bytes, self.stats.data_ptr(), self.status.data_ptr(), None, None,
                               self.ctypes.c_void_p(stream))
         assert rc == 0, self.lib.vfa_last_error()
 

@@ -120,10 +120,13 @@ VFA_API size_t vfa_workspace_bytes(const VfaParams* p);
  * [B,Hq,Lq] (nullable). workspace: >= vfa_workspace_bytes. stats: int64[VFA_STAT_COUNT]
  * (nullable). status: uint32[VFA_STATUS_COUNT] (nullable). skip_trace: uint8
  * [B, Hq, Lq/128, Lk/k_block] (nullable): per visit position, 1 = processed,
- * 2 = skipped, 0 = not visited. stream: cudaStream_t (NULL = legacy default). */
+ * 2 = skipped, 0 = not visited. stab_block: int32 [B, Hq, Lq] (nullable): the StateTrace
+ * stabilization position of every row (src/analysis.py:39-78) -- the 1-based key block of
+ * the visit after which the running max equals its final value. stream: cudaStream_t
+ * (NULL = legacy default). */
 VFA_API int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
-            void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-            unsigned char* skip_trace, void* stream);
+                    void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                    unsigned char* skip_trace, int* stab_block, void* stream);
 
 /* Bytes of device scratch vfa_fwd_host needs (up to four K/V group slots and eight query
  * sub-chunk slots), or 0 if the parameters or the chunking are invalid. */

@@ -231,6 +231,10 @@ class HeadResult:
     error: Exception | None = None
     elided: int = 0       # BLASST-FA4: processed blocks whose rescale was elided
     rows_masked: int = 0  # BLASST rowskip: suppressed row slots (skipped blocks count all rows)
+    # StateTrace stabilization position per row (src/analysis.py:39-78): the block of the
+    # first visit whose running-max snapshot equals the final max = the last visit that
+    # raised it (the first visit if none did)
+    stab: np.ndarray | None = None
 
 
 VARIANTS = ("fa", "vfa", "vsa", "blasst", "blasst_fa4", "blasst_rowskip")
@@ -286,7 +290,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
     t_r, t_c = nq // qb, nk // kb
     out = np.full((nq, d), np.nan)
     lse = np.full(nq, np.nan)
-    res = HeadResult(out=out, lse=lse)
+    res = HeadResult(out=out, lse=lse, stab=np.zeros(nq, dtype=np.int64))
     kreprs = precompute_kreprs(k, kb, kind, tc1) if use_m_init else None
 
     for i in (range(1, t_r + 1) if q_blocks is None else q_blocks):
@@ -308,6 +312,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
         l = np.zeros(qb)
         o = np.zeros((qb, d))
         dec = []
+        stab = np.full(qb, visit[0], dtype=np.int64)
         for j in visit:
             s = tile_scores(q, k, scale, causal, i, j, qb, kb)
             v_j = v[(j - 1) * kb: j * kb]
@@ -332,7 +337,9 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
                 p_t = np.exp(_exp_args(s_kept, m_new))
                 l = f * l + _rowsum(p_t)
                 o = f[:, None] * o + p_t @ v_j
-                m = np.where(keep, m_new, m)
+                m_next = np.where(keep, m_new, m)
+                stab[m_next > m] = j
+                m = m_next
                 res.special += 1
                 res.rows_masked += qb - int(keep.sum())
                 continue
@@ -361,6 +368,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
                 f = _rescale_factor(m, m_new)
                 l = f * l + _rowsum(p_t)
                 o = f[:, None] * o + p_t @ v_j
+                stab[m_new > m] = j
                 m = m_new
                 res.special += 1
             else:
@@ -373,6 +381,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
                 res.frozen += 1
         if record_decisions:
             res.decisions.append(dec)
+        res.stab[(i - 1) * qb: i * qb] = stab
         zero = l == 0.0  # src/core.py:101-109
         if zero.any():
             row = int(np.argmax(zero))

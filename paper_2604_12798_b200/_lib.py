@@ -74,7 +74,7 @@ def bind(path: str):
     lib.vfa_check_params.restype = ctypes.c_int
     lib.vfa_workspace_bytes.argtypes = [P]
     lib.vfa_workspace_bytes.restype = ctypes.c_size_t
-    lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp, vp]
     lib.vfa_fwd.restype = ctypes.c_int
     lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int, ctypes.c_int]
     lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t

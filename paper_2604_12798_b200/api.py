@@ -15,8 +15,10 @@ Same names, keyword arguments, validation errors and numerical exceptions; the
 compute runs in libvfa_b200.so (hand-written sm_100a kernels) on bf16 CUDA
 tensors. Differences that follow from running on the GPU: O is returned as a bf16
 torch tensor on the device (shape of q), the LSE is returned as well (`.lse`),
-`trace` is None (no per-visit m snapshots), and the OverflowMonitor counts come
-from device counters when monitor=True (exp_arg_max is not tracked).
+`trace` is a DeviceTrace (the per-row stabilization positions the reference's
+StateTrace feeds into stabilization_positions, recorded by the kernel instead of per-visit
+m snapshots), and the OverflowMonitor counts come from device counters when monitor=True
+(exp_arg_max is not tracked).
 """
 
 from __future__ import annotations
@@ -366,7 +368,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                       kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
                       n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None, lse=None,
                       check=True, skip_trace=False, stream=None, workspace=None,
-                      krepr_precomputed=False, softmax_split=0):
+                      krepr_precomputed=False, softmax_split=0, stab_trace=False):
     """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
 
     Returns (out, lse, info) with info = {"stats": int64 device tensor | dict,
@@ -379,6 +381,9 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     sink/local-first visit order (VFA / VSA; for blasst it is order='sink_local', so pass
     reorder=False for the reference's default sequential blasst). lam: skip threshold of the
     skipping variants; tau: blasst_fa4 rescale-elision threshold (SkipConfig.tau).
+    stab_trace: also return info["stab_block"], int32 [B, Hq, Lq]: per row the key block after
+    whose visit the running max held its final value (the StateTrace stabilization position,
+    src/analysis.py:39-78), see DeviceTrace / stabilization_positions.
     softmax_split: 0 (per-variant default), 2 or 4 threads per row of a query tile (a layout
     choice: results are within tolerance of each other, bitwise-stable for a fixed split).
     """
@@ -389,8 +394,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     if not tau >= 0:
         raise ValueError(f"tau must be >= 0, got {tau}")
     if all(isinstance(x, torch.Tensor) and x.device.type == "cpu" for x in (q, k, v)):
-        if skip_trace or krepr_precomputed or workspace is not None:
-            raise ValueError("skip_trace / krepr_precomputed / workspace need device-resident inputs")
+        if skip_trace or stab_trace or krepr_precomputed or workspace is not None:
+            raise ValueError("skip_trace / stab_trace / krepr_precomputed / workspace need device-resident inputs")
         return attention_forward_host(q, k, v, variant=variant, causal=causal, q_block=q_block,
                                       k_block=k_block, scale=scale, kind=kind, qkind=qkind,
                                       reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
@@ -430,14 +435,16 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     if skip_trace:
         trace = torch.empty((q.shape[0], q.shape[1], q.shape[2] // 128, k.shape[2] // k_block),
                             dtype=torch.uint8, device=dev)
+    stab = torch.empty(q.shape[:3], dtype=torch.int32, device=dev) if stab_trace else None
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     with torch.cuda.device(dev):
         rc = lib.vfa_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                          lse.data_ptr(), ws.data_ptr(), ws_bytes, stats.data_ptr(), status.data_ptr(),
-                         trace.data_ptr() if trace is not None else None, ctypes.c_void_p(st))
+                         trace.data_ptr() if trace is not None else None,
+                         stab.data_ptr() if stab is not None else None, ctypes.c_void_p(st))
     if rc:
         _raise_for(rc)
-    info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws}
+    info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws, "stab_block": stab}
     if check:
         check_status(status)
     return out, lse, info
@@ -535,9 +542,61 @@ def _run(p: AttentionProblem, variant, **kw):
                                        q_block=p.blocks.q_block, k_block=p.blocks.k_block,
                                        scale=p.scale, **kw)
     st = stats_dict(info)
+    if info.get("stab_block") is not None:
+        st["stab_block"] = info["stab_block"].view(*p.q.shape[:-1]) if two_d else info["stab_block"]
     if two_d:
         out, lse = out.view(*p.q.shape), lse.view(p.q.shape[0])
     return out, lse, st
+
+
+@dataclass
+class DeviceTrace:
+    """Device-side stand-in for the reference's StateTrace (src/core.py:35-54).
+
+    The reference records a running-max snapshot after every visit; the one consumer on the
+    forward path, stabilization_positions (src/analysis.py:39-78), needs only the block after
+    which each row's max held its final value, which the kernel records directly
+    (`positions`, 1-based key blocks, shape [..., Nq]) together with each query block's local
+    key block -- so the analysis runs at any context length.
+    """
+
+    q_block: int
+    positions: torch.Tensor
+    local_blocks: list
+
+    @classmethod
+    def from_run(cls, p: "AttentionProblem", stab) -> "DeviceTrace":
+        b = p.blocks
+        local = [min((i * b.q_block - 1) // b.k_block + 1, b.t_c) for i in range(1, b.t_r + 1)]
+        return cls(q_block=b.q_block, positions=stab, local_blocks=local)
+
+
+@dataclass
+class StabilizationReport:
+    """src/analysis.py:30-37."""
+
+    positions: np.ndarray
+    frac_sink: float
+    frac_local: float
+    frac_other: float
+
+    def frac_sink_or_local(self) -> float:
+        return self.frac_sink + self.frac_local
+
+
+def stabilization_positions(trace: DeviceTrace) -> StabilizationReport:
+    """Fractions of rows whose running max stabilised in the sink block, the local block or
+    elsewhere (src/analysis.py:39-78), from a DeviceTrace of one or more heads."""
+    pos = trace.positions.to(torch.int64).cpu().numpy()
+    nq = pos.shape[-1]
+    qb = trace.q_block
+    local = np.repeat(np.asarray(trace.local_blocks, dtype=np.int64), qb)[:nq]
+    sink = pos == 1
+    loc = (pos == local) & (local != 1)
+    n = pos.size
+    return StabilizationReport(positions=pos, frac_sink=float(sink.sum()) / n,
+                               frac_local=float(loc.sum()) / n,
+                               frac_other=float((~sink & (pos != local)).sum()) / n)
 
 
 def _counters(st, p: AttentionProblem, variant: str) -> OpCounters:
@@ -555,13 +614,13 @@ def _monitor(st, monitor: bool) -> OverflowMonitor:
 def fa_forward(p: AttentionProblem, order_hook=None):
     """Baseline online softmax, rescale on every block (src/fa.py:28-61).
 
-    Returns (O, counters, trace=None) with `.lse`. order_hook (a test-only
+    Returns (O, counters, DeviceTrace) with `.lse`. order_hook (a test-only
     permutation hook in the reference) is not supported on the GPU path.
     """
     if order_hook is not None:
         raise ValueError("order_hook is not supported by the GPU fa_forward")
-    out, lse, st = _run(p, "fa")
-    return ForwardResult((out, _counters(st, p, "fa"), None), lse, st)
+    out, lse, st = _run(p, "fa", stab_trace=True)
+    return ForwardResult((out, _counters(st, p, "fa"), DeviceTrace.from_run(p, st["stab_block"])), lse, st)
 
 
 def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True,
@@ -569,7 +628,7 @@ def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True
                 monitor: bool = False, *, n_sink: int = 1, n_local: int = 1):
     """Frozen-max pass with m-initialisation (src/vfa.py:156-223).
 
-    Returns (O, counters, trace=None, overflow_monitor) with `.lse`.
+    Returns (O, counters, DeviceTrace, overflow_monitor) with `.lse`.
     """
     if kind not in _lib.KEY_REPRS:
         raise ValueError(f"unknown key representation {kind!r}")
@@ -578,8 +637,9 @@ def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True
     if tc1 is not None and not (1 <= tc1 <= p.t_c):
         raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
     out, lse, st = _run(p, "vfa", kind=kind, reorder=reorder, use_m_init=use_m_init, qkind=qkind,
-                        tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor)
-    return ForwardResult((out, _counters(st, p, "vfa"), None, _monitor(st, monitor)), lse, st)
+                        tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor, stab_trace=True)
+    trace = DeviceTrace.from_run(p, st["stab_block"])
+    return ForwardResult((out, _counters(st, p, "vfa"), trace, _monitor(st, monitor)), lse, st)
 
 
 def vsa_forward(p: AttentionProblem, cfg: SkipConfig, kind: str = "sabsmax", qkind: str = "row_wise",

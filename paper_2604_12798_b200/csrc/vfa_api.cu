@@ -98,7 +98,8 @@ void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
 
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base);
+                 unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
+                 long long row_base);
 
 }  // namespace
 
@@ -154,13 +155,13 @@ int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream) {
 
 int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
             void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-            unsigned char* skip_trace, void* stream) {
+            unsigned char* skip_trace, int* stab_block, void* stream) {
   int rc = vfa_check_params(p);
   if (rc) return rc;
   if (!q || !k || !v || !o) return fail(VFA_ERR_DATA, "NULL tensor pointer");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
     return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
-  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, skip_trace,
+  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, skip_trace, stab_block,
                       static_cast<cudaStream_t>(stream), true, 0);
 }
 
@@ -171,7 +172,8 @@ namespace {
 // caller accumulates several launches into one status word, e.g. vfa_fwd_host's chunks).
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
-                 unsigned char* skip_trace, cudaStream_t st, bool zero_counters, long long row_base) {
+                 unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
+                 long long row_base) {
   int rc = VFA_OK;
   // m-initialisation belongs to the frozen-max variants; FA and the BLASST family start at -inf
   const bool minit = (p->variant == VFA_VARIANT_VFA || p->variant == VFA_VARIANT_VSA) && p->use_m_init;
@@ -235,6 +237,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.stats = reinterpret_cast<unsigned long long*>(stats);
   a.status = status;
   a.skip_trace = skip_trace;
+  a.stab = stab_block;
   a.row_base = row_base;
   a.trace = g_debug_trace;
 
@@ -426,8 +429,8 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       cudaStream_t cs = hs->comp[c & 1];
       cudaStreamWaitEvent(cs, kv_in, 0);
       cudaStreamWaitEvent(cs, q_in, 0);
-      rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, cs, false,
-                        static_cast<long long>(loff));
+      rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, nullptr, cs,
+                        false, static_cast<long long>(loff));
       if (rc) return cleanup(), rc;
       cudaEventRecord(done, cs);
       cudaStreamWaitEvent(hs->d2h, done, 0);

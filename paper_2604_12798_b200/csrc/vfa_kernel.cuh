@@ -85,6 +85,7 @@ struct FwdArgs {
   unsigned long long* stats;
   unsigned int* status;
   unsigned char* skip_trace;
+  int* stab;  // per row: key block (1-based) of the visit where the running max last rose
   long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
@@ -531,11 +532,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float cs = a.c_scale;
       float m2[NT], l[NT];  // running max (log2 units of scaled scores; identical in all parts)
       uint32_t xpar[NT];    // and this part's share of the normalizer, per served tile
+      // StateTrace stabilization (src/analysis.py:39-78): the block of the visit after which
+      // the running max equals its final value = the last visit that raised it (or the first
+      // visit when nothing raised it); the first record's block otherwise
+      int stab[NT];
 #pragma unroll
       for (int ti = 0; ti < NT; ++ti) {
         m2[ti] = -INFINITY;
         l[ti] = 0.f;
         xpar[ti] = 0;
+        stab[ti] = sched_block(sched, 0);
       }
       uint32_t over32 = 0, over16 = 0;
       uint32_t pv_ph = 0;  // bit ti: pv_done phase (SB 2)
@@ -656,6 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // suppressed row keeps factor 1 and its max, and adds zero mass (src/sparse.py:241-247)
               const bool upd = (MODE != kBLR) || keep;
               f = (!upd || m2n == -INFINITY) ? 1.0f : ex2_approx(m2[ti] - m2n);
+              if (upd && m2n > m2[ti]) stab[ti] = j;
               if (upd) m2[ti] = m2n;
               if (!upd) {
 #pragma unroll
@@ -779,6 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
         const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
         if (part == 0 && a.lse) a.lse[lrow] = (m2[ti] + __log2f(lsum)) * kLn2;
+        if (part == 0 && a.stab) a.stab[lrow] = stab[ti];
         if (a.status) {
           if (part == 0 && lsum == 0.f) {
             if (m2[ti] == -INFINITY) {

@@ -88,12 +88,12 @@ def run_case(name, spec, data, causal, variant, **kw):
            "k_block": spec.k_block, "n_sink": _SCHED["n_sink"], "n_local": _SCHED["n_local"]}
     err = ""
     out = np.full(q.shape, np.nan)
-    counters = stats = mon = None
+    counters = stats = mon = trace = None
     try:
         if variant == "fa":
-            out, counters, _ = vfa_lab.fa_forward(p)
+            out, counters, trace = vfa_lab.fa_forward(p)
         elif variant == "vfa":
-            out, counters, _, mon = vfa_lab.vfa_forward(p, **kw)
+            out, counters, trace, mon = vfa_lab.vfa_forward(p, **kw)
         elif variant == "vsa":
             lam = kw.pop("lam")
             out, counters, stats, mon = vfa_lab.vsa_forward(p, SkipConfig(lam=lam), **kw)
@@ -129,6 +129,12 @@ def run_case(name, spec, data, causal, variant, **kw):
         # its sha256 (the oracle must reproduce it bit-for-bit)
         f"{name}/out": out.astype(np.float32), f"{name}/lse": lse,
     })
+    if trace is not None:
+        # StateTrace -> stabilization positions per row (src/analysis.py:39-78)
+        rep = vfa_lab.stabilization_positions(trace)
+        arrays[f"{name}/stab"] = rep.positions.astype(np.int32)
+        rec["stab.frac_sink"], rec["stab.frac_local"], rec["stab.frac_other"] = (
+            rep.frac_sink, rep.frac_local, rep.frac_other)
     rec["out_sha256"] = hashlib.sha256(np.ascontiguousarray(out, dtype=np.float64).tobytes()).hexdigest()
     if counters is not None:
         for f, val in counters.as_dict().items():

@@ -38,3 +38,9 @@ def case_bits(name):
     arrays, meta = _load()
     m = meta[name]
     return tuple(arrays[m[f"in_{t}"]] for t in "qkv")
+
+
+def case_stab(name):
+    """Reference stabilization positions per row (None if the case has no StateTrace)."""
+    arrays, _ = _load()
+    return arrays.get(f"{name}/stab")

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import torch
 
-from golden_io import case, case_bits, case_names
+from golden_io import case, case_bits, case_names, case_stab
 from oracle import vfa_oracle as vo
 
 pytestmark = pytest.mark.gpu
@@ -143,6 +143,13 @@ def test_golden_vectors(name):
             assert st["nonfinite_rows"] > 0
         return
     _compare(out[0, 0], lse_g[0, 0], out32.astype(np.float64), lse, name)
+    stab = case_stab(name)
+    if stab is not None:
+        # device StateTrace stabilization positions vs the reference's (fp32 vs float64 maxima:
+        # a row whose two largest block maxima tie within fp32 rounding may differ)
+        _, _, info2 = attention_forward(qb, kb, vb, check=False, stab_trace=True, **kw)
+        got = info2["stab_block"][0, 0].cpu().numpy()
+        assert (got != stab).mean() <= 0.01, (name, (got != stab).sum())
     if "stats.blocks_visited" in m:
         assert st["visited"] == m["stats.blocks_visited"]
         assert st["skipped"] == m["stats.blocks_skipped"]
@@ -402,7 +409,9 @@ def test_dropin_api_mirrors_reference():
     p = AttentionProblem(q, k, v, blocks=BlockSpec(L, L, d, 128, 128), causal=True)
     out, counters, trace, mon = vfa_forward(p)
     r = vo.forward_head(qf, kf, vf, variant="vfa", causal=True, q_block=128, k_block=128)
-    assert out.shape == (L, d) and trace is None
+    from paper_2604_12798_b200 import DeviceTrace
+    assert out.shape == (L, d) and isinstance(trace, DeviceTrace)
+    assert np.array_equal(trace.positions.cpu().numpy(), r.stab) or (trace.positions.cpu().numpy() != r.stab).mean() < 0.01
     assert vo.max_rel_err(_f64(out), r.out) <= O_REL
     t_r = L // 128
     assert counters.rowmax_reductions == sum(min(2, i) for i in range(1, t_r + 1))
@@ -454,3 +463,23 @@ def test_host_pipeline_reports_whole_problem_row():
         attention_forward_host(q, k, v, variant="vfa", kind=m["kind"], causal=m["causal"],
                                k_block=m["k_block"], chunk_kv_heads=1, chunk_q_heads=1)
     assert ei.value.row == (1 * H + 1) * L + int(m["error"].split(":")[1])
+
+
+def test_device_trace_stabilization_api():
+    # reference-shaped: fa_forward returns a trace that stabilization_positions consumes
+    # (tests/test_acceptance.py:171-183 pattern, on the golden planted-middle-peak problem)
+    from paper_2604_12798_b200 import (AttentionProblem, BlockSpec, fa_forward, stabilization_positions,
+                                       vfa_forward)
+    name = "vsa_midpeak_lam1e-2"
+    m, q, k, v, _, _ = case(name)
+    qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda() for x in case_bits(name))
+    L, d = qb.shape
+    p = AttentionProblem(qb, kb, vb, blocks=BlockSpec(L, L, d, 128, m["k_block"]), causal=True)
+    _, _, trace = fa_forward(p)
+    rep = stabilization_positions(trace)
+    r = vo.forward_head(q, k, v, variant="fa", causal=True, q_block=128, k_block=m["k_block"])
+    assert (rep.positions != r.stab).mean() <= 0.01
+    assert abs(rep.frac_sink + rep.frac_local + rep.frac_other - 1.0) < 1e-12
+    _, _, vtrace, _ = vfa_forward(p)
+    rv = vo.forward_head(q, k, v, variant="vfa", causal=True, q_block=128, k_block=m["k_block"])
+    assert (vtrace.positions.cpu().numpy() != rv.stab).mean() <= 0.01

@@ -181,3 +181,17 @@ def test_host_scratch_bytes(lib):
     assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 0, 0) == 0
     assert lib.vfa_host_scratch_bytes(ctypes.byref(p), 2, 1) == 0  # query sub-chunks need 1 KV head
     assert lib.vfa_host_scratch_bytes(ctypes.byref(_params(k_block=96)), 1, 0) == 0
+
+
+@pytest.mark.parametrize("name", [n for n in case_names() if "stab.frac_sink" in case(n)[0]])
+def test_stabilization_report_matches_reference(name):
+    # api.stabilization_positions on the reference's own positions reproduces its fractions
+    import torch
+    from golden_io import case_stab
+    from paper_2604_12798_b200.api import BlockSpec, DeviceTrace, stabilization_positions
+    m, q, *_ = case(name)
+    b = BlockSpec(q.shape[0], q.shape[0], q.shape[1], m["q_block"], m["k_block"])
+    local = [min((i * b.q_block - 1) // b.k_block + 1, b.t_c) for i in range(1, b.t_r + 1)]
+    rep = stabilization_positions(DeviceTrace(b.q_block, torch.from_numpy(case_stab(name)), local))
+    assert rep.frac_sink == m["stab.frac_sink"] and rep.frac_local == m["stab.frac_local"]
+    assert rep.frac_other == m["stab.frac_other"]

@@ -11,7 +11,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from golden_io import case, case_names
+from golden_io import case, case_names, case_stab
 from oracle import vfa_oracle as vo
 
 
@@ -55,6 +55,9 @@ def test_oracle_bitwise_equals_reference(name):
     if "mon.count_over_f32" in m:
         assert r.monitor.count_over_f32 == m["mon.count_over_f32"]
         assert r.monitor.count_over_f16 == m["mon.count_over_f16"]
+    stab = case_stab(name)
+    if stab is not None:  # StateTrace -> stabilization_positions (src/analysis.py:39-78)
+        assert np.array_equal(r.stab, stab)
 
 
 def test_sabsmax_known_answers():
