@@ -96,7 +96,7 @@ typedef struct VfaParams {
   int32_t k_block;      /* BlockSpec.k_block: 64 or 128 */
   int32_t variant;      /* VFA_VARIANT_* */
   int32_t kind;         /* VFA_KREPR_* */
-  int32_t qkind;        /* 0 = row_wise (the only query representation on the GPU path) */
+  int32_t qkind;        /* QUERY_REPRS (src/vfa.py:40): 0 row_wise, 1 q_absmax, 2 q_sabsmax, 3 q_mean */
   int32_t reorder;      /* vfa_forward(reorder=...); BLASST: 1 = order 'sink_local' */
   int32_t use_m_init;   /* vfa_forward(use_m_init=...) */
   int32_t tc1;          /* representations for key blocks 1..tc1; 0 = all (src/vfa.py:79-88) */
@@ -150,6 +150,11 @@ VFA_API int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_h
 /* Key-block representations only (precompute_kreprs): k bf16 [B,Hkv,Lk,D] ->
  * out bf16 contiguous [B, Hkv, n_blocks, D], n_blocks = tc1 or Lk/k_block. */
 VFA_API int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream);
+
+/* Incremental representations for an append-only K cache:
+ * recomputes only key blocks [first_block, n_blocks) of `out` (layout of vfa_krepr), e.g. the
+ * blocks that new tokens filled or extended; blocks before first_block are left untouched. */
+VFA_API int vfa_krepr_range(const VfaParams* p, const void* k, void* out, int first_block, void* stream);
 
 /* Host mirror of the device tile scheduler (build_schedule, src/vfa.py:146-153,
  * generalised to n_sink/n_local). i is the 1-based query block. Writes up to `cap`

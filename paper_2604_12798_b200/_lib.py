@@ -35,7 +35,7 @@ STATUS_COUNT = 4
 # every symbol include/vfa_b200.h declares
 EXPORTS = ("vfa_check_params", "vfa_workspace_bytes", "vfa_fwd", "vfa_krepr", "vfa_schedule",
            "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace",
-           "vfa_host_scratch_bytes", "vfa_fwd_host")
+           "vfa_host_scratch_bytes", "vfa_fwd_host", "vfa_krepr_range")
 
 
 class VfaParams(ctypes.Structure):
@@ -82,6 +82,8 @@ def bind(path: str):
                                  vp]
     lib.vfa_fwd_host.restype = ctypes.c_int
     lib.vfa_krepr.argtypes = [P, vp, vp, vp]
+    lib.vfa_krepr_range.argtypes = [P, vp, vp, ctypes.c_int, vp]
+    lib.vfa_krepr_range.restype = ctypes.c_int
     lib.vfa_krepr.restype = ctypes.c_int
     lib.vfa_schedule.argtypes = [ctypes.c_int] * 9 + [ctypes.POINTER(ctypes.c_int),
                                                      ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int]

@@ -706,8 +706,14 @@ def blasst_rowskip_forward(p: AttentionProblem, cfg: SkipConfig):
     return ForwardResult((out, c, _skip_stats(st, b.q_block, row_slots=True)), lse, st)
 
 
-def precompute_kreprs(p: AttentionProblem, kind: str, tc1: int | None = None) -> torch.Tensor:
-    """Key-block representations on the GPU (src/vfa.py:79-88): bf16 [..., n_blocks, d]."""
+def precompute_kreprs(p: AttentionProblem, kind: str, tc1: int | None = None, *, out=None,
+                      first_block: int = 0) -> torch.Tensor:
+    """Key-block representations on the GPU (src/vfa.py:79-88): bf16 [..., n_blocks, d].
+
+    Incremental use for an append-only K cache: pass the previous result as
+    `out` and the 0-based first block whose keys changed as `first_block`; only blocks from
+    there on are recomputed (vfa_krepr_range).
+    """
     if kind not in _lib.KEY_REPRS:
         raise ValueError(f"unknown key representation {kind!r}")
     tc1 = p.t_c if tc1 is None else tc1
@@ -718,11 +724,19 @@ def precompute_kreprs(p: AttentionProblem, kind: str, tc1: int | None = None) ->
     prm = _params(q, k, k, q, variant="vfa", causal=p.causal, q_block=p.blocks.q_block,
                   k_block=p.blocks.k_block, scale=p.scale, kind=kind, qkind="row_wise", reorder=True,
                   use_m_init=True, tc1=tc1, n_sink=1, n_local=1, lam=None, monitor=False)
-    out = torch.empty((k.shape[0], k.shape[1], tc1, k.shape[3]), dtype=torch.bfloat16, device=k.device)
+    shape = (k.shape[0], k.shape[1], tc1, k.shape[3])
+    if out is None:
+        if first_block:
+            raise ValueError("first_block > 0 needs the previous representations as `out`")
+        out = torch.empty(shape, dtype=torch.bfloat16, device=k.device)
+    else:
+        out = out if out.dim() == 4 else out.view(1, 1, *out.shape)
+        if tuple(out.shape) != shape or out.dtype != torch.bfloat16 or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous bf16 tensor of shape {shape}")
     lib = _lib.load()
     with torch.cuda.device(k.device):
-        rc = lib.vfa_krepr(ctypes.byref(prm), k.data_ptr(), out.data_ptr(),
-                           ctypes.c_void_p(torch.cuda.current_stream(k.device).cuda_stream))
+        rc = lib.vfa_krepr_range(ctypes.byref(prm), k.data_ptr(), out.data_ptr(), int(first_block),
+                                 ctypes.c_void_p(torch.cuda.current_stream(k.device).cuda_stream))
     if rc:
         _raise_for(rc)
     return out if p.k.dim() == 4 else out[0, 0]

@@ -70,21 +70,44 @@ int64_t n_reprs(const VfaParams* p) {
   return (p->tc1 > 0 && p->tc1 < tc) ? p->tc1 : tc;
 }
 
-int launch_krepr(const VfaParams* p, const void* k, void* out, cudaStream_t st) {
-  const int nblk = static_cast<int>(n_reprs(p));
-  dim3 grid((nblk + 3) / 4, static_cast<unsigned>(p->heads_kv), static_cast<unsigned>(p->batch));
-  if (p->head_dim == 128)
-    vfa::krepr_kernel<128><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
-                                                p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
-                                                p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
+// Block representations of `rows`-row blocks of x [B, H, L, D] (strides sb, sh, sr) for blocks
+// [jb0, nblk): out [B, H, nblk, D] bf16 contiguous.
+int launch_block_repr(const void* x, int64_t B, int64_t H, const int64_t* strides, int D, int rows, int nblk,
+                      int kind, void* out, int jb0, cudaStream_t st) {
+  if (nblk <= jb0) return VFA_OK;
+  dim3 grid((nblk - jb0 + 3) / 4, static_cast<unsigned>(H), static_cast<unsigned>(B));
+  const auto* xp = static_cast<const __nv_bfloat16*>(x);
+  auto* op = static_cast<__nv_bfloat16*>(out);
+  if (D == 128)
+    vfa::krepr_kernel<128><<<grid, 128, 0, st>>>(xp, strides[0], strides[1], strides[2], static_cast<int>(H), rows,
+                                                nblk, kind, op, jb0);
   else
-    vfa::krepr_kernel<64><<<grid, 128, 0, st>>>(static_cast<const __nv_bfloat16*>(k), p->k_stride[0],
-                                               p->k_stride[1], p->k_stride[2], static_cast<int>(p->heads_kv),
-                                               p->k_block, nblk, p->kind, static_cast<__nv_bfloat16*>(out));
+    vfa::krepr_kernel<64><<<grid, 128, 0, st>>>(xp, strides[0], strides[1], strides[2], static_cast<int>(H), rows,
+                                               nblk, kind, op, jb0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("krepr launch: ") + cudaGetErrorString(e));
   return VFA_OK;
 }
+
+int launch_krepr(const VfaParams* p, const void* k, void* out, cudaStream_t st, int jb0 = 0) {
+  return launch_block_repr(k, p->batch, p->heads_kv, p->k_stride, static_cast<int>(p->head_dim), p->k_block,
+                           static_cast<int>(n_reprs(p)), p->kind, out, jb0, st);
+}
+
+// block-wise qkind (src/vfa.py:69-76): the query tile's representation kind as a block_repr kind
+int qkind_as_block_kind(int qkind) {
+  return qkind == 1 ? VFA_KREPR_K_ABSMAX_UNSIGNED : (qkind == 2 ? VFA_KREPR_SABSMAX : VFA_KREPR_K_MEAN);
+}
+
+// workspace layout: [key representations][query representations][per-tile seeds] (the last two
+// only for the block-wise query representations)
+size_t ws_krepr_bytes(const VfaParams* p) {
+  return static_cast<size_t>(p->batch * p->heads_kv * n_reprs(p) * p->head_dim * 2 + 255) / 256 * 256;
+}
+size_t ws_qrepr_bytes(const VfaParams* p) {
+  return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * p->head_dim * 2 + 255) / 256 * 256;
+}
+size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * 4); }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
@@ -111,7 +134,7 @@ int vfa_check_params(const VfaParams* p) {
     return fail(VFA_ERR_CONFIG, "variant must be 0 (fa), 1 (vfa), 2 (vsa), 3 (blasst), 4 (blasst_fa4) or 5 (blasst_rowskip)");
   if (p->kind < VFA_KREPR_SABSMAX || p->kind > VFA_KREPR_K_ABSMAX_UNSIGNED)
     return fail(VFA_ERR_CONFIG, "unknown key representation");
-  if (p->qkind != 0) return fail(VFA_ERR_CONFIG, "only the row_wise query representation runs on the GPU path");
+  if (p->qkind < 0 || p->qkind > 3) return fail(VFA_ERR_CONFIG, "unknown query representation");
   if (p->q_block != 128) return fail(VFA_ERR_CONFIG, "q_block must be 128 (tcgen05 M = 128)");
   if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
   if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
@@ -143,7 +166,17 @@ int vfa_check_params(const VfaParams* p) {
 
 size_t vfa_workspace_bytes(const VfaParams* p) {
   if (!p || vfa_check_params(p) != VFA_OK) return 0;
-  return static_cast<size_t>(p->batch * p->heads_kv * n_reprs(p) * p->head_dim * 2) + 256;
+  size_t n = ws_krepr_bytes(p) + 256;
+  if (p->qkind != 0) n += ws_qrepr_bytes(p) + ws_m0_bytes(p);
+  return n;
+}
+
+int vfa_krepr_range(const VfaParams* p, const void* k, void* out, int first_block, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!k || !out) return fail(VFA_ERR_DATA, "NULL pointer");
+  if (first_block < 0 || first_block > n_reprs(p)) return fail(VFA_ERR_CONFIG, "first_block out of range");
+  return launch_krepr(p, k, out, static_cast<cudaStream_t>(stream), first_block);
 }
 
 int vfa_krepr(const VfaParams* p, const void* k, void* out, void* stream) {
@@ -201,6 +234,31 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   } else {
     mr = mk;
   }
+  const float* m0_tile = nullptr;
+  if (minit && p->qkind != 0) {
+    // block-wise query representation: per query tile, seed = max_j qrepr . krepr_j
+    uint8_t* qrep = static_cast<uint8_t*>(workspace) + ws_krepr_bytes(p);
+    float* m0 = reinterpret_cast<float*>(qrep + ws_qrepr_bytes(p));
+    const int tr = static_cast<int>(p->seq_q / 128);
+    rc = launch_block_repr(q, p->batch, p->heads_q, p->q_stride, D, 128, tr, qkind_as_block_kind(p->qkind), qrep, 0,
+                           st);
+    if (rc) return rc;
+    dim3 grid((tr + 3) / 4, static_cast<unsigned>(p->heads_q), static_cast<unsigned>(p->batch));
+    const auto* qr = reinterpret_cast<const __nv_bfloat16*>(qrep);
+    const auto* kr = static_cast<const __nv_bfloat16*>(workspace);
+    const int tc = static_cast<int>(n_key_blocks(p));
+    if (D == 128)
+      vfa::minit_block_kernel<128><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
+                                                         static_cast<int>(p->heads_kv), tr, static_cast<int>(nrep),
+                                                         BC, tc, p->causal ? 1 : 0, m0);
+    else
+      vfa::minit_block_kernel<64><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
+                                                        static_cast<int>(p->heads_kv), tr, static_cast<int>(nrep), BC,
+                                                        tc, p->causal ? 1 : 0, m0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("m-init seed launch: ") + cudaGetErrorString(e));
+    m0_tile = m0;
+  }
   if (zero_counters) reset_counters(stats, status, st);
   if (skip_trace)
     cudaMemsetAsync(skip_trace, 0,
@@ -238,6 +296,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.status = status;
   a.skip_trace = skip_trace;
   a.stab = stab_block;
+  a.m0_tile = m0_tile;
   a.row_base = row_base;
   a.trace = g_debug_trace;
 

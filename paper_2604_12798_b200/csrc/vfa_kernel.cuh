@@ -86,6 +86,7 @@ struct FwdArgs {
   unsigned int* status;
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
+  const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
   long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
@@ -190,7 +191,7 @@ __device__ __forceinline__ TileSchedule unit_schedule(const FwdArgs& a, int qt, 
 // number of m-init chunks (BC representations per chunk)
 template <int MODE>
 __device__ __forceinline__ int minit_chunks(const FwdArgs& a, const TileSchedule& s, int BC, int* nrep) {
-  if ((MODE != kVFA && MODE != kVSA) || !a.use_m_init) {
+  if ((MODE != kVFA && MODE != kVSA) || !a.use_m_init || a.m0_tile != nullptr) {
     *nrep = 0;
     return 0;
   }
@@ -602,6 +603,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ti = 0; ti < NT; ++ti) m2[ti] = exchange_max(ti, tile0 + ti, mx[ti]) * cs;
       }
+      if ((MODE == kVFA || MODE == kVSA) && a.use_m_init && a.m0_tile != nullptr) {
+        // block-wise query representation (src/vfa.py:104-106): one seed for the whole tile
+#pragma unroll
+        for (int ti = 0; ti < NT; ++ti)
+          m2[ti] = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + unit.h0 + tile0 + ti) * a.Tr + unit.qt] * cs;
+      }
 
       const float2 cs2 = make_float2(cs, cs);
       // block-class counts beyond the closed form (skip / elision / row-mask variants only)
@@ -838,13 +845,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------------------------
 // Key-block representations (src/vfa.py:47-88): one warp per key block, lane owns
 // D/32 consecutive columns; sabsmax keeps the first row on ties (strict >).
+// Also computes the block-wise query representations (src/vfa.py:69-76) over 128-row query
+// tiles (q_sabsmax = sabsmax, q_absmax = k_absmax_unsigned, q_mean = k_mean), and, with
+// jb0 > 0, refreshes only blocks [jb0, nblk) (append-only K cache).
 template <int D>
 __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restrict__ k, long long sb, long long sh,
                                                     long long sr, int Hkv, int BC, int nblk, int kind,
-                                                    __nv_bfloat16* __restrict__ out) {
+                                                    __nv_bfloat16* __restrict__ out, int jb0 = 0) {
   constexpr int CPL = D / 32;  // columns per lane (2 or 4)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jb = blockIdx.x * 4 + warp;
+  const int jb = jb0 + blockIdx.x * 4 + warp;
   const int kvh = blockIdx.y, b = blockIdx.z;
   if (jb >= nblk) return;
   const __nv_bfloat16* base = k + b * sb + kvh * sh + static_cast<long long>(jb) * BC * sr + lane * CPL;
@@ -896,6 +906,39 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
     float r = kind == VFA_KREPR_SABSMAX ? val[c] : (kind == VFA_KREPR_K_MEAN ? best[c] / BC : best[c]);
     dst[c] = __float2bfloat16_rn(r);
   }
+}
+
+// Block-wise m-init seed (src/vfa.py:104-106): per query tile i, max over the visible key
+// representations j <= min(vmax_i, nrep) of qrepr_i . krepr_j (raw, unscaled; fp32 dot).
+// One warp per (batch, query head, tile); lane owns D/32 dimensions.
+template <int D>
+__global__ void __launch_bounds__(128) minit_block_kernel(const __nv_bfloat16* __restrict__ qrep,
+                                                          const __nv_bfloat16* __restrict__ krep, int Hq, int Hkv,
+                                                          int Tr, int nrep, int BC, int Tc, int causal,
+                                                          float* __restrict__ m0) {
+  constexpr int CPL = D / 32;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int h = blockIdx.y, b = blockIdx.z;
+  if (w >= Tr) return;
+  const int i = w + 1;  // 1-based query tile
+  const int vmax = causal ? min((i * kBR - 1) / BC + 1, Tc) : Tc;
+  const int cap = vmax < nrep ? vmax : nrep;
+  const int kvh = h / (Hq / Hkv);
+  float qv[CPL];
+  const __nv_bfloat16* qp = qrep + ((static_cast<size_t>(b) * Hq + h) * Tr + w) * D + lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) qv[c] = __bfloat162float(qp[c]);
+  const __nv_bfloat16* kp = krep + (static_cast<size_t>(b) * Hkv + kvh) * nrep * D + lane * CPL;
+  float best = -INFINITY;
+  for (int j = 0; j < cap; ++j) {
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc = fmaf(qv[c], __bfloat162float(kp[static_cast<size_t>(j) * D + c]), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    best = fmaxf(best, acc);
+  }
+  if (lane == 0) m0[(static_cast<size_t>(b) * Hq + h) * Tr + w] = best;
 }
 
 }  // namespace vfa

@@ -168,6 +168,11 @@ def main():
                   dict(kind="k_max", reorder=False)))
     cases.append(("vfa_d128_causal_noinit", s, gen_gaussian(s, 5), True, "vfa", dict(use_m_init=False)))
     cases.append(("vfa_d128_causal_tc1", s, gen_gaussian(s, 6), True, "vfa", dict(tc1=2)))
+    # block-wise query representations for the m-init seed (src/vfa.py:69-76, 104-106)
+    for qk in ("q_absmax", "q_sabsmax", "q_mean"):
+        cases.append((f"vfa_d128_causal_{qk}", s, gen_gaussian(s, 14), True, "vfa", dict(qkind=qk)))
+    cases.append(("vfa_d128_noncausal_q_sabsmax_kmax", s, gen_gaussian(s, 15), False, "vfa",
+                  dict(qkind="q_sabsmax", kind="k_max")))
     s = BlockSpec(1024, 1024, 64, 128, 128)
     sd = gen_structured(s, 7, "middle_peak", 8.0)
     cases.append(("vsa_midpeak_lam1e-2", s, (sd.q, sd.k, sd.v), True, "vsa", dict(lam=1e-2)))

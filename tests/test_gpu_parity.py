@@ -110,7 +110,7 @@ def test_vfa_options(kind, opts):
 def _golden_kw(m):
     kw = dict(variant=m["variant"], causal=m["causal"], q_block=128, k_block=m["k_block"],
               n_sink=m["n_sink"], n_local=m["n_local"])
-    for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau"):
+    for key in ("kind", "qkind", "reorder", "use_m_init", "tc1", "lam", "tau"):
         if key in m:
             kw[key] = m[key]
     if m.get("order") == "sink_local":
@@ -483,3 +483,55 @@ def test_device_trace_stabilization_api():
     _, _, vtrace, _ = vfa_forward(p)
     rv = vo.forward_head(q, k, v, variant="vfa", causal=True, q_block=128, k_block=m["k_block"])
     assert (vtrace.positions.cpu().numpy() != rv.stab).mean() <= 0.01
+
+
+@pytest.mark.parametrize("qkind", ["q_absmax", "q_sabsmax", "q_mean"])
+@pytest.mark.parametrize("variant", ["vfa", "vsa"])
+def test_blockwise_query_repr_m_init(qkind, variant):
+    # block-wise m-init seeds (src/vfa.py:104-106) on the GPU against the oracle, GQA + batch
+    from paper_2604_12798_b200.api import NormalizerUnderflowError
+    B, Hq, Hkv, L, d = 2, 4, 2, 1024, 128
+    q, k, v = _rand((B, Hq, L, d), 151), _rand((B, Hkv, L, d), 152), _rand((B, Hkv, L, d), 153)
+    kw = dict(variant=variant, causal=True, qkind=qkind)
+    if variant == "vsa":
+        kw["lam"] = 1e-3
+    errors = [vo.forward_head(_f64(q[b, h]), _f64(k[b, h // 2]), _f64(v[b, h // 2]), q_block=128,
+                              k_block=128, raise_errors=False, **kw).error
+              for b in range(B) for h in range(Hq)]
+    if any(e is not None for e in errors):
+        # a block-wise absmax seed overestimates every row's max; VSA then skips every block
+        # of some query tile and the normalizer underflows -- the reference raises, so must we
+        assert variant == "vsa" and qkind != "q_mean"
+        from paper_2604_12798_b200 import attention_forward
+        with pytest.raises(NormalizerUnderflowError):
+            attention_forward(q, k, v, **kw)
+        return
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), q_block=128, k_block=128, **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    if variant == "vfa":
+        assert (st["special"], st["frozen"], st["visited"]) == (ref_st["special"], ref_st["frozen"],
+                                                                ref_st["visited"])
+
+
+def test_incremental_krepr_range_matches_full():
+    # append-only K cache: recomputing only the tail blocks reproduces the full representations
+    import ctypes
+    from paper_2604_12798_b200 import _lib
+    from paper_2604_12798_b200.api import _params
+    lib = _lib.load()
+    k = _rand((1, 2, 2048, 128), 161)
+    p = _params(k.new_empty((1, 2, 2048, 128)), k, k, k, variant="vfa", causal=True, q_block=128, k_block=128,
+                scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
+                n_sink=1, n_local=1, lam=None, monitor=False)
+    full = torch.empty((1, 2, 16, 128), dtype=torch.bfloat16, device="cuda")
+    part = torch.zeros_like(full)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.vfa_krepr(ctypes.byref(p), k.data_ptr(), full.data_ptr(), st) == 0
+    k2 = k.clone()
+    k2[:, :, 1500:] = _rand((1, 2, 548, 128), 162)  # tokens appended after position 1500
+    assert lib.vfa_krepr(ctypes.byref(p), k.data_ptr(), part.data_ptr(), st) == 0
+    assert lib.vfa_krepr_range(ctypes.byref(p), k2.data_ptr(), part.data_ptr(), 1500 // 128, st) == 0
+    assert lib.vfa_krepr(ctypes.byref(p), k2.data_ptr(), full.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(part, full)

@@ -59,7 +59,7 @@ def _params(**kw):
 
 
 @pytest.mark.parametrize("field,value,code", [
-    ("variant", 7, 2), ("kind", 9, 2), ("qkind", 2, 2), ("q_block", 64, 2), ("k_block", 96, 2),
+    ("variant", 7, 2), ("kind", 9, 2), ("qkind", 4, 2), ("q_block", 64, 2), ("k_block", 96, 2),
     ("head_dim", 96, 2), ("seq_q", 1000, 3), ("seq_k", 1000, 3), ("heads_q", 3, 3), ("tc1", 99, 2),
     ("n_sink", -1, 2), ("tau", -1.0, 2), ("softmax_split", 3, 2), ("variant", 6, 2),
 ])
@@ -131,7 +131,7 @@ def test_op_counters_integer_equal_reference(name):
     m, q, k, v, _, _ = case(name)
     if "counters.blocks_processed" not in m or m["error"]:
         pytest.skip("no counters recorded")
-    kw = {key: m[key] for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau", "order") if key in m}
+    kw = {key: m[key] for key in ("kind", "qkind", "reorder", "use_m_init", "tc1", "lam", "tau", "order") if key in m}
     r = vo.forward_head(q, k, v, variant=m["variant"], causal=m["causal"], q_block=m["q_block"],
                         k_block=m["k_block"], n_sink=m["n_sink"], n_local=m["n_local"], **kw)
     st = dict(visited=r.visited, skipped=r.skipped, special=r.special, frozen=r.frozen,

@@ -19,7 +19,7 @@ def _kw(m):
     kw = dict(variant=m["variant"], causal=m["causal"], q_block=m["q_block"],
               k_block=m["k_block"], n_sink=m["n_sink"], n_local=m["n_local"],
               raise_errors=False)
-    for key in ("kind", "reorder", "use_m_init", "tc1", "lam", "tau", "order"):
+    for key in ("kind", "qkind", "reorder", "use_m_init", "tc1", "lam", "tau", "order"):
         if key in m:
             kw[key] = m[key]
     return kw
