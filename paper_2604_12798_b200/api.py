@@ -192,9 +192,21 @@ class SkipStats:
     def block_sparsity(self) -> float:
         return self.blocks_skipped / self.blocks_visited if self.blocks_visited else 0.0
 
+    @property
+    def row_sparsity(self) -> float:
+        return self.rows_masked / self.row_slots if self.row_slots else 0.0
+
+    @property
+    def rescale_skip_rate(self) -> float:
+        return self.rescales_elided / self.blocks_processed if self.blocks_processed else 0.0
+
     def as_dict(self) -> dict:
-        d = {f.name: getattr(self, f.name) for f in fields(self)}
+        """src/sparse.py:84-96 (the reference reports these fields)."""
+        d = {f.name: getattr(self, f.name) for f in fields(self) if f.name not in ("processed_special",
+                                                                                 "processed_frozen")}
         d["block_sparsity"] = self.block_sparsity
+        d["row_sparsity"] = self.row_sparsity
+        d["rescale_skip_rate"] = self.rescale_skip_rate
         return d
 
 

@@ -535,3 +535,43 @@ def test_incremental_krepr_range_matches_full():
     assert lib.vfa_krepr(ctypes.byref(p), k2.data_ptr(), full.data_ptr(), st) == 0
     torch.cuda.synchronize()
     assert torch.equal(part, full)
+
+
+@pytest.mark.parametrize("variant,extra", [("vfa", {}), ("blasst_fa4", dict(lam=1e-3, tau=2.0)),
+                                           ("vsa", dict(lam=1e-2))])
+def test_vft1_run_backend_matches_reference_report(variant, extra, tmp_path):
+    # `run` on a VFT1 dump through the GPU backend: counters / stats integer-equal to the
+    # report the reference CLI wrote for the same dump (tests/golden/make_vft1.py), O vs oracle
+    import json
+    import os
+
+    from paper_2604_12798_b200 import runner, vft1
+    fix = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "vft1")
+    ref = json.load(open(os.path.join(fix, f"ref_run_{variant}.json")))
+    rep = runner.run(fix, variant=variant, q_block=128, k_block=64, causal=True, out=tmp_path / "o.vft",
+                     report=tmp_path / "r.json", **extra)
+    assert json.load(open(tmp_path / "r.json"))["values"]["output_shape"] == [256, 64]
+    assert rep["counters"] == ref["counters"]
+    if ref["stats"] is not None:
+        assert rep["stats"] == ref["stats"]
+    q, k, v = runner.load_tensors(fix)
+    kw = {"lam": extra.get("lam"), "tau": extra.get("tau", 0.0)} if variant != "vfa" else {}
+    r = vo.forward_head(q, k, v, variant=variant, causal=True, q_block=128, k_block=64, **kw)
+    o = vft1.read_matrix(tmp_path / "o.vft")
+    assert vo.max_rel_err(o, r.out) <= O_REL
+    cmp = runner.compare(fix, "fa", variant=variant, q_block=128, k_block=64, causal=True, **extra)
+    assert cmp["values"]["max_rel_diff"] <= 5e-2 and set(cmp["values"]["counter_delta"]) == set(ref["counters"])
+
+
+def test_module_cli_run(tmp_path):
+    import os
+    import subprocess
+    import sys
+    fix = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "vft1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "paper_2604_12798_b200", "run", "--data", fix, "--variant", "vfa",
+                        "--causal", "--report", str(tmp_path / "r.json")], cwd=root, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([sys.executable, "-m", "paper_2604_12798_b200", "run", "--data", str(tmp_path),
+                        "--variant", "vfa"], cwd=root, capture_output=True, text=True)
+    assert r.returncode == 3  # missing q.vft -> DataError (src/cli.py:69-72)
