@@ -634,7 +634,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool skipped = false;
           bool rescale = false;  // this block rescales O by f (exact update, not skipped / elided)
           float f = 1.0f;
-          if (MODE != kVFA || special) {
+          if (MODE == kVSA && !special) {
+            // ---- VSA frozen block: only the skip test (src/sparse.py:296-304). A row is below
+            //      the threshold iff every part's maximum is (m~ = max over parts, and a part
+            //      holding m~ > m fails the test), so one CTA-wide AND over the part maxima
+            //      decides without exchanging row maxima; the frozen max is not updated.
+            float pm = -INFINITY;
+#pragma unroll
+            for (int e = 0; e < CP; e += 2) pm = fmax3(pm, v[e], v[e + 1]);
+            const float pm2 = pm * cs;
+            const bool below = (pm2 - fmaxf(m2[ti], pm2) < a.log2_lambda) ||
+                               (pm2 == -INFINITY && m2[ti] == -INFINITY && a.log2_lambda != -INFINITY);
+            skipped = named_bar_and(1 + t, SPLIT * kBR, below);
+            if (skipped) ++n_skipped;
+          } else if (MODE != kVFA || special) {
             // ---- exact-update / skip-test block: rowmax over the full row (all parts,
             //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
             float mt = -INFINITY;
