@@ -264,6 +264,21 @@ __device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o1
   }
 }
 
+// Max of N (a multiple of 8) consecutive values: four independent FMNMX3 chains (max is exact
+// in any order, so the result does not depend on the reduction shape).
+template <int N>
+__device__ __forceinline__ float part_max(const float* v) {
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < N; e += 8) {
+    m0 = fmax3(m0, v[e], v[e + 1]);
+    m1 = fmax3(m1, v[e + 2], v[e + 3]);
+    m2 = fmax3(m2, v[e + 4], v[e + 5]);
+    m3 = fmax3(m3, v[e + 6], v[e + 7]);
+  }
+  return fmax3(fmaxf(m0, m1), m2, m3);
+}
+
 // W consecutive columns (masked entries already -inf): P = exp2(s*cs - m2) -> W/2 packed
 // bf16x2 words; row sums into two independent packed accumulators (halves the FADD2 chain).
 template <int W, bool MON, int kPoly>
@@ -639,9 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             //      the threshold iff every part's maximum is (m~ = max over parts, and a part
             //      holding m~ > m fails the test), so one CTA-wide AND over the part maxima
             //      decides without exchanging row maxima; the frozen max is not updated.
-            float pm = -INFINITY;
-#pragma unroll
-            for (int e = 0; e < CP; e += 2) pm = fmax3(pm, v[e], v[e + 1]);
+            const float pm = part_max<CP>(v);
             const float pm2 = pm * cs;
             const bool below = (pm2 - fmaxf(m2[ti], pm2) < a.log2_lambda) ||
                                (pm2 == -INFINITY && m2[ti] == -INFINITY && a.log2_lambda != -INFINITY);
@@ -650,10 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (MODE != kVFA || special) {
             // ---- exact-update / skip-test block: rowmax over the full row (all parts,
             //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
-            float mt = -INFINITY;
-#pragma unroll
-            for (int e = 0; e < CP; e += 2) mt = fmax3(mt, v[e], v[e + 1]);
-            mt = exchange_max(ti, t, mt);
+            const float mt = exchange_max(ti, t, part_max<CP>(v));
             const float mt2 = mt * cs;
             const float m2n = fmaxf(m2[ti], mt2);
             bool keep = true;  // rowskip: this row takes part in the update

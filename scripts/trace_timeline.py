@@ -21,11 +21,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--variant", default="vfa")
 ap.add_argument("--k-block", type=int, default=128)
 ap.add_argument("--n-local", type=int, default=1)
+ap.add_argument("--sink", type=float, default=0.0, help="planted-sink boost (C3 data); 0 = Gaussian")
+ap.add_argument("--lam", type=float, default=1e-2)
 a = ap.parse_args()
 cfg = CONFIGS["c2"]
 dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
-r = Runner(q, k, v, a.variant, lam=1e-2 if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
+if a.sink:
+    from scripts.sweeps import planted_sink
+    planted_sink(q, k, a.sink, a.k_block)
+r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
 T = cfg["L"] // a.k_block
 buf = torch.zeros(T * 16, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
