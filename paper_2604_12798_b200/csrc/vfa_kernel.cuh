@@ -103,9 +103,18 @@ constexpr int kTraceSlots = 16;
   do {                                                                                       \
     if ((args).trace != nullptr && blockIdx.x == 0) (args).trace[(pos) * kTraceSlots + (slot)] = clock64(); \
   } while (0)
+// per-CTA phase stamps after CTA 0's per-visit slots: entry, first S seen, last P done, exit
+#define VFA_TRACE_UNIT(args, slot)                                                           \
+  do {                                                                                       \
+    if ((args).trace != nullptr)                                                             \
+      (args).trace[(args).Tc * kTraceSlots + blockIdx.x * 4 + (slot)] = clock64();           \
+  } while (0)
 #else
 #define VFA_TRACE_EVENT(args, pos, slot) \
   do {                                   \
+  } while (0)
+#define VFA_TRACE_UNIT(args, slot) \
+  do {                             \
   } while (0)
 #endif
 
@@ -328,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = tid & 31;
 
   if (tid == 0) {
+    VFA_TRACE_UNIT(a, 0);
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&ctl->q_full[t], 1);
       for (int b = 0; b < SB; ++b) {
@@ -640,6 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int b = g % SB;
           wait_s(t, g);
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
+          if (r == 0 && part == 0 && t == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
           float v[CP];
           load_part(t, b, v);
           if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
@@ -774,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int c = 0; c < NCH; ++c) mbar_arrive(&ctl->p_full[t][b][c]);
           }
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
+          if (r == 0 && part == 0 && pos == N - 1 && t == NQ - 1) VFA_TRACE_UNIT(a, 2);
         }
       }
       const int n_exact = all_exact(MODE) ? N : sched.n_spec;  // exact-update blocks per tile
@@ -859,6 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) VFA_TRACE_UNIT(a, 3);
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(ctl->tmem_base);

@@ -32,7 +32,8 @@ if a.sink:
     planted_sink(q, k, a.sink, a.k_block)
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
 T = cfg["L"] // a.k_block
-buf = torch.zeros(T * 16, dtype=torch.int64, device=dev)
+units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
+buf = torch.zeros(T * 16 + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)
 r.attn(sh)  # warm-up
@@ -41,7 +42,16 @@ r.krepr(sh)
 r.attn(sh)
 torch.cuda.synchronize()
 r.lib.vfa_debug_trace(None)
-tr = buf.cpu().numpy().reshape(T, 16).astype(np.float64)
+allbuf = buf.cpu().numpy()
+ut = allbuf[T * 16:].reshape(units, 4).astype(np.float64)
+ok = (ut > 0).all(axis=1)
+ut = ut[ok]
+dur = ut[:, 3] - ut[:, 0]
+pro = ut[:, 1] - ut[:, 0]
+epi = ut[:, 3] - ut[:, 2]
+print(f"units {ok.sum()}: mean cycles {dur.mean():.0f}; prologue (entry -> first S) {pro.mean():.0f} "
+      f"({pro.sum() / dur.sum():.1%}), epilogue (last P -> exit) {epi.mean():.0f} ({epi.sum() / dur.sum():.1%})")
+tr = allbuf[: T * 16].reshape(T, 16).astype(np.float64)
 n = int((tr[:, 1] > 0).sum())
 tr = tr[:n]
 t0 = tr[tr > 0].min()
