@@ -301,9 +301,17 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: VFA_BENCH_SHARE_GPU=1 puts every rank on GPU 0 over gloo, to exercise the sharded
+    # path (shard plan, max-over-ranks timing, gather + bitwise verification) on a 1-GPU box
+    share = os.environ.get("VFA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(dev)
     if rank == 0:
@@ -321,7 +329,7 @@ def main_ours(args):
     shard = kv_head_shard(rank, world, Hq, Hkv)
     q_full, k_full, v_full = make_inputs(cfg, dev)
     q, k, v = shard_inputs(q_full, k_full, v_full, shard)
-    if world > 1:
+    if world > 1 and rank != 0:  # rank 0 keeps the full problem for the post-timing verification
         del q_full, k_full, v_full
     flops_total = causal_flops(B, Hq, L, d)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > L2

@@ -45,6 +45,10 @@ def gather_heads(x, world: int):
     import torch.distributed as dist
     if world == 1:
         return x
+    if dist.get_backend() == "gloo" and x.is_cuda:  # gloo gathers host tensors
+        parts = [torch.empty_like(x, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, x.contiguous().cpu())
+        return torch.cat(parts, 1).to(x.device)
     parts = [torch.empty_like(x) for _ in range(world)]
     dist.all_gather(parts, x.contiguous())
     return torch.cat(parts, 1)
