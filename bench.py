@@ -42,6 +42,8 @@ CONFIGS = {
                B=1, Hq=32, Hkv=8, L=32768, d=128),
     "c4": dict(workload="long-context prefill bf16 causal L=128K (BASELINE configs[3])",
                B=1, Hq=32, Hkv=8, L=131072, d=128),
+    # a small problem for the test suite's multi-rank runs (not a benchmark line)
+    "tiny": dict(workload="test problem", B=1, Hq=8, Hkv=4, L=2048, d=128),
 }
 
 
@@ -429,7 +431,8 @@ def main_ours(args):
                        "variant": "vfa", "key_repr": "sabsmax", "n_sink": args.n_sink, "n_local": args.n_local,
                        "parallelism": f"kv-head sharding x{world}" if world > 1 else "single GPU",
                        "flops_per_step": flops_total,
-                       "l2": "inputs 384 MiB > 126 MB L2, and L2 flushed (256 MiB write) between timed steps",
+                       "l2": f"inputs {(B * Hq * L * d + 2 * B * Hkv * L * d) * 2 / 2**20:.0f} MiB, and L2 flushed "
+                             "(256 MiB write) between timed steps",
                        "timing": "variants fa/vfa/vsa interleaved step by step; value = the vfa steps"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

@@ -575,3 +575,22 @@ def test_module_cli_run(tmp_path):
     r = subprocess.run([sys.executable, "-m", "paper_2604_12798_b200", "run", "--data", str(tmp_path),
                         "--variant", "vfa"], cwd=root, capture_output=True, text=True)
     assert r.returncode == 3  # missing q.vft -> DataError (src/cli.py:69-72)
+
+
+def test_bench_sharded_path_two_ranks():
+    # bench.py under torchrun with 2 ranks sharing GPU 0 (gloo): KV-head shards, max-over-ranks
+    # timing, NCCL-style gather + bitwise verification against the single-GPU run
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VFA_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29611", "bench.py", "--gpus", "2",
+                        "--config", "tiny", "--steps", "2", "--warmup", "3", "--no-cpu", "--e2e-steps", "1"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["verified_vs_single_gpu"] is True
+    assert line["e2e"]["bitwise_equal_to_device_run"] is True
