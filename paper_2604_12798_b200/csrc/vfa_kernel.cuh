@@ -900,6 +900,7 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
     best[c] = kind == VFA_KREPR_K_MEAN ? 0.f : -INFINITY;
     val[c] = 0.f;
   }
+#pragma unroll 8
   for (int row = 0; row < BC; ++row) {
     float x[CPL];
     if constexpr (CPL == 4) {
