@@ -594,3 +594,24 @@ def test_bench_sharded_path_two_ranks():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["verified_vs_single_gpu"] is True
     assert line["e2e"]["bitwise_equal_to_device_run"] is True
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa", "blasst", "blasst_fa4", "blasst_rowskip"])
+@pytest.mark.parametrize("geom", [dict(B=2, Hq=6, Hkv=3, Lq=512, Lk=768, causal=False),
+                                  dict(B=1, Hq=3, Hkv=1, Lq=768, Lk=768, causal=True),
+                                  dict(B=1, Hq=4, Hkv=4, Lq=384, Lk=384, causal=True, k_block=64)])
+def test_every_variant_on_mixed_geometries(variant, geom):
+    # batch, odd GQA groups (one query tile per CTA), Lq != Lk, Bc = 64 for every variant
+    g = dict(geom)
+    B, Hq, Hkv, Lq, Lk = g.pop("B"), g.pop("Hq"), g.pop("Hkv"), g.pop("Lq"), g.pop("Lk")
+    q, k, v = _rand((B, Hq, Lq, 64), 171), _rand((B, Hkv, Lk, 64), 172), _rand((B, Hkv, Lk, 64), 173)
+    kw = dict(variant=variant, q_block=128, k_block=g.pop("k_block", 128), **g)
+    if variant not in ("fa", "vfa"):
+        kw["lam"] = 1e-2
+    if variant == "blasst_fa4":
+        kw["tau"] = 1.0
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    okw = dict(kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **okw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    assert st["visited"] == ref_st["visited"]

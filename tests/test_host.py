@@ -195,3 +195,24 @@ def test_stabilization_report_matches_reference(name):
     rep = stabilization_positions(DeviceTrace(b.q_block, torch.from_numpy(case_stab(name)), local))
     assert rep.frac_sink == m["stab.frac_sink"] and rep.frac_local == m["stab.frac_local"]
     assert rep.frac_other == m["stab.frac_other"]
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "blasst", "blasst_fa4", "blasst_rowskip"])
+@pytest.mark.parametrize("reorder", [True, False])
+def test_host_schedule_mirror_matches_oracle(variant, reorder):
+    # vfa_schedule (the device scheduler's host mirror) == the oracle's visit order / exact set
+    from paper_2604_12798_b200 import build, tile_schedule
+    build.build()
+    qb, kb, tc = 128, 64, 16
+    for i in range(1, 9):
+        order, special = tile_schedule(i, qb, kb, tc, True, reorder=reorder, variant=variant)
+        vmax = vo.visible_key_blocks(i, qb, kb, tc, True)
+        local = vo.local_key_block(i, qb, kb, tc)
+        if variant == "fa" or variant in ("blasst_fa4", "blasst_rowskip") or (variant == "blasst" and not reorder):
+            ref_order, ref_special = tuple(range(1, vmax + 1)), frozenset(range(1, vmax + 1))
+        elif variant == "blasst":
+            ref_order, _ = vo.build_schedule(i, vmax, local, True)
+            ref_special = frozenset(range(1, vmax + 1))
+        else:
+            ref_order, ref_special = vo.build_schedule(i, vmax, local, reorder)
+        assert order == tuple(ref_order) and special == frozenset(ref_special), (variant, i)
