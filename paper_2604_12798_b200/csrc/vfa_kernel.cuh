@@ -94,6 +94,9 @@ struct FwdArgs {
 #ifndef VFA_SB_MAX
 #define VFA_SB_MAX 2  // S buffers per tile (tuning experiments: 1 disables double buffering)
 #endif
+#ifndef VFA_SB_NQ1
+#define VFA_SB_NQ1 1  // double-buffer S for every mode when a CTA serves one query tile
+#endif
 
 // debug timeline slots per visited block (CTA 0 only, builds with -DVFA_TRACE): softmax t:
 // S ready, P done; MMA t: P observed, next QK issued
@@ -140,7 +143,7 @@ struct Cfg {
   // never waits on the PV -> QK latency of the previous block. Used for the all-exact modes
   // only: measured faster for FA at BC = 64, slower for VFA / VSA (profiles/ab_r01_sb.txt).
   static constexpr int kSB =
-      (NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && all_exact(MODE)) ? 2 : 1;
+      (NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && (all_exact(MODE) || (NQ == 1 && VFA_SB_NQ1))) ? 2 : 1;
   static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
     return static_cast<uint32_t>(kSB == 2 ? (t * 2 + b) * BC : t * 128);
   }
