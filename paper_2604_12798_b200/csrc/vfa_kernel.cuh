@@ -231,10 +231,14 @@ constexpr int kPolyOverride = -1;
 #endif
 // Element pairs (of every 8) whose exp2 runs on the FMA pipe (degree-4 polynomial) instead
 // of MUFU.EX2. Under the B200's 1 kW power cap the 13-instruction polynomial costs more
-// energy (lower clocks) than it saves in MUFU time: measured best is 0 for both softmax
-// splits (profiles/ab_r01_poly.txt); the polynomial stays as a tuning knob. Kept identical
-// for every split so P (hence O) does not depend on the split.
-__host__ __device__ constexpr int poly_pairs() { return kPolyOverride >= 0 ? kPolyOverride : 0; }
+// energy (lower clocks) than it saves in MUFU time at head dim 128: measured best is 0 for
+// both softmax splits (profiles/ab_r01_poly.txt). Kept identical for every split and mode so
+// P (hence O) does not depend on the split or the variant.
+// At head dim 64 (half the MMA work per exponential; the GPU is not power-capped) one pair
+// in eight on the FMA pipe is measured +4 % at Bc 128 (profiles/ab_r01_poly.txt).
+__host__ __device__ constexpr int poly_pairs(int d, int bc) {
+  return kPolyOverride >= 0 ? kPolyOverride : (d == 64 && bc == 128 ? 1 : 0);
+}
 // softmax column split per mode (see the softmax role): measured best per variant
 #ifndef VFA_SPLIT_FA
 #define VFA_SPLIT_FA 2
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int OP = C::kOP;
   constexpr int NCH = C::kNCH;
   constexpr int CW = C::kCW;
-  constexpr int kPoly = poly_pairs();
+  constexpr int kPoly = poly_pairs(D, BC);
   constexpr int SB = C::kSB;
   using CtlT = Ctl<NS, NQ, SB>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
