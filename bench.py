@@ -201,7 +201,7 @@ def make_inputs(cfg, dev, seed=1234):
 class Runner:
     """Pre-allocated launcher for one variant over one (sharded) problem."""
 
-    def __init__(self, q, k, v, variant, lam=None, k_block=128, n_sink=1, n_local=1, lib=None):
+    def __init__(self, q, k, v, variant, lam=None, k_block=128, n_sink=1, n_local=1, lib=None, cta_pair=0):
         import ctypes
 
         import torch
@@ -215,6 +215,7 @@ class Runner:
                          scale=None, kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True,
                          tc1=None, n_sink=n_sink, n_local=n_local, lam=lam, monitor=False)
         self.p.krepr_precomputed = 1
+        self.p.cta_pair = cta_pair
         self.ws_bytes = int(self.lib.vfa_workspace_bytes(ctypes.byref(self.p)))
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=q.device)
         self.stats = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=q.device)

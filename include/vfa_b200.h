@@ -108,6 +108,9 @@ typedef struct VfaParams {
   int32_t softmax_split; /* threads sharing one row of a query tile: 0 = per-variant default,
                            2 = per-tile warp sets, 4 = all softmax warps serve both tiles */
   double tau;           /* BLASST-FA4 rescale elision: max increase <= tau * ln 2 (SkipConfig.tau) */
+  int32_t cta_pair;     /* 0 = default, 1 = one CTA per unit, 2 = CTA pairs (even GQA group, d = 128):
+                           the unit's two query heads on two SMs sharing K/V through M = 256 MMAs */
+  int32_t reserved;
 } VfaParams;
 
 /* Host-only validation (no GPU needed). Returns VFA_OK or VFA_ERR_CONFIG / VFA_ERR_DATA. */

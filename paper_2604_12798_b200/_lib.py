@@ -54,6 +54,7 @@ class VfaParams(ctypes.Structure):
         ("lam", ctypes.c_double),
         ("krepr_precomputed", ctypes.c_int32), ("softmax_split", ctypes.c_int32),
         ("tau", ctypes.c_double),
+        ("cta_pair", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
 

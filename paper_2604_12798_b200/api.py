@@ -340,7 +340,7 @@ def _strides(x):
 
 
 def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind, reorder,
-            use_m_init, tc1, n_sink, n_local, lam, monitor, softmax_split=0, tau=0.0):
+            use_m_init, tc1, n_sink, n_local, lam, monitor, softmax_split=0, tau=0.0, cta_pair=0):
     if kind not in _lib.KEY_REPRS:
         raise ValueError(f"unknown key representation {kind!r}")
     if qkind not in _lib.QUERY_REPRS:
@@ -366,6 +366,7 @@ def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind
     p.lam = float(lam) if lam is not None else 0.0
     p.tau = float(tau)
     p.softmax_split = int(softmax_split)
+    p.cta_pair = int(cta_pair)
     return p
 
 
@@ -380,7 +381,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                       kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
                       n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None, lse=None,
                       check=True, skip_trace=False, stream=None, workspace=None,
-                      krepr_precomputed=False, softmax_split=0, stab_trace=False):
+                      krepr_precomputed=False, softmax_split=0, stab_trace=False, cta_pair=0):
     """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
 
     Returns (out, lse, info) with info = {"stats": int64 device tensor | dict,
@@ -396,6 +397,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     stab_trace: also return info["stab_block"], int32 [B, Hq, Lq]: per row the key block after
     whose visit the running max held its final value (the StateTrace stabilization position,
     src/analysis.py:39-78), see DeviceTrace / stabilization_positions.
+    cta_pair: 0 (default), 1 (one CTA per unit) or 2 (the unit's two query heads on a CTA pair
+    sharing each K/V tile through M = 256 tcgen05 MMAs; even GQA groups, d = 128).
     softmax_split: 0 (per-variant default), 2 or 4 threads per row of a query tile (a layout
     choice: results are within tolerance of each other, bitwise-stable for a fixed split).
     """
@@ -412,7 +415,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                                       k_block=k_block, scale=scale, kind=kind, qkind=qkind,
                                       reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
                                       n_local=n_local, lam=lam, tau=tau, monitor=monitor, out=out, lse=lse,
-                                      check=check, stream=stream, softmax_split=softmax_split)
+                                      check=check, stream=stream, softmax_split=softmax_split,
+                                      cta_pair=cta_pair)
     lib = _lib.load()
     for name, x in (("q", q), ("k", k), ("v", v)):
         if not isinstance(x, torch.Tensor) or x.dtype != torch.bfloat16 or x.device.type != "cuda":
@@ -427,7 +431,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
                 tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
-                softmax_split=softmax_split, tau=tau)
+                softmax_split=softmax_split, tau=tau, cta_pair=cta_pair)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)
@@ -467,7 +471,7 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
                            tc1=None, n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None,
                            lse=None,
                            check=True, stream=None, device=None, chunk_kv_heads=1, chunk_q_heads=2,
-                           softmax_split=0):
+                           softmax_split=0, cta_pair=0):
     """The forward on HOST tensors (bf16 [B, Hq, Lq, d] / [B, Hkv, Lk, d], contiguous;
     page-locked for full overlap) -> host (O bf16, LSE fp32, info), through the C ABI's
     vfa_fwd_host: chunks of `chunk_kv_heads` KV heads are copied in, computed and copied
@@ -498,7 +502,7 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
                 tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
-                softmax_split=softmax_split, tau=tau)
+                softmax_split=softmax_split, tau=tau, cta_pair=cta_pair)
     rc = lib.vfa_check_params(ctypes.byref(p))
     if rc:
         _raise_for(rc)

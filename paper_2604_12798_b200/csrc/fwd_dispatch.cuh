@@ -9,11 +9,11 @@
 
 namespace vfa_host {
 
-template <int D, int BC, int NQ, int MODE, int SPLIT>
+template <int D, int BC, int NQ, int MODE, int SPLIT, int PAIR = 1>
 int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
-  using C = vfa::Cfg<D, BC, NQ, SPLIT, MODE>;
-  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT>;
+  using C = vfa::Cfg<D, BC, NQ, SPLIT, MODE, PAIR>;
+  auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT, PAIR>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -28,8 +28,27 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
   }
   const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
   if (units <= 0) return VFA_OK;
-  kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if constexpr (PAIR == 2) {
+    // one cluster of two CTAs per unit (the unit's two query heads, one per CTA)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+    cfg.blockDim = dim3(vfa::kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mr, args);
+    if (e == cudaSuccess) e = cudaGetLastError();
+  } else {
+    kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return VFA_OK;
 }
@@ -54,6 +73,10 @@ template <int MODE>
 int launch_mode(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                 const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
   const int D = static_cast<int>(p->head_dim), BC = p->k_block;
+  if (a.pair == 2) {  // CTA pairs (d = 128): one query tile per CTA, K/V shared by M = 256 MMAs
+    if (BC == 128) return launch_fwd<128, 128, 1, MODE, 4, 2>(p, mq, mk, mv, mr, a, st);
+    return launch_fwd<128, 64, 1, MODE, 4, 2>(p, mq, mk, mv, mr, a, st);
+  }
 #define VFA_NQ(DD, BB)                                                                          \
   return nq == 2 ? dispatch_split<DD, BB, 2, MODE>(p, mq, mk, mv, mr, a, st)                    \
                  : dispatch_split<DD, BB, 1, MODE>(p, mq, mk, mv, mr, a, st)

@@ -111,6 +111,13 @@ size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+// CTA pairs off by default: measured slower than one CTA per unit (profiles/ab_r01_pair.txt);
+// cta_pair = 2 selects them per call
+#ifndef VFA_PAIR_DEFAULT
+#define VFA_PAIR_DEFAULT 0
+#endif
+bool default_pair(int variant) { return VFA_PAIR_DEFAULT != 0 && variant >= 0; }
+
 void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
   if (stats) cudaMemsetAsync(stats, 0, sizeof(long long) * VFA_STAT_COUNT, st);
   if (status) {
@@ -141,6 +148,7 @@ int vfa_check_params(const VfaParams* p) {
   if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
   if (p->softmax_split != 0 && p->softmax_split != 2 && p->softmax_split != 4)
     return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 2 or 4");
+  if (p->cta_pair < 0 || p->cta_pair > 2) return fail(VFA_ERR_CONFIG, "cta_pair must be 0 (auto), 1 (off) or 2 (on)");
   if (p->variant >= VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
   if (!(p->tau >= 0.0)) return fail(VFA_ERR_CONFIG, "tau must be >= 0");  // src/sparse.py:52-53 (NaN rejected)
   if (p->batch < 1 || p->heads_q < 1 || p->heads_kv < 1 || p->seq_q < 1 || p->seq_k < 1)
@@ -218,14 +226,19 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   const int D = static_cast<int>(p->head_dim), BC = p->k_block;
   const int group = static_cast<int>(p->heads_q / p->heads_kv);
   const int nq = (group % 2 == 0) ? 2 : 1;
+  // CTA pairs (cta_pair = 2, or auto): the unit's two query heads on two SMs sharing each K/V
+  // tile through M = 256 MMAs; needs an even GQA group and d = 128
+  const bool pair_ok = nq == 2 && D == 128;
+  const int pair = (pair_ok && (p->cta_pair == 2 || (p->cta_pair == 0 && default_pair(p->variant)))) ? 2 : 1;
 
   CUtensorMap mq, mk, mv, mr;
   if (!make_map(&mq, q, p->batch, p->heads_q, p->seq_q, D, p->q_stride[0], p->q_stride[1], p->q_stride[2], 128) ||
-      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2], BC) ||
+      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2],
+                BC / pair) ||
       !make_map(&mv, v, p->batch, p->heads_kv, p->seq_k, D, p->v_stride[0], p->v_stride[1], p->v_stride[2], BC))
     return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (minit) {
-    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, BC))
+    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, BC / pair))
       return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed (krepr)");
     if (!p->krepr_precomputed) {
       rc = launch_krepr(p, k, workspace, st);
@@ -274,6 +287,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.Tr = static_cast<int>(p->seq_q / 128);
   a.Tc = static_cast<int>(n_key_blocks(p));
   a.heads_per_unit = nq;
+  a.pair = pair;
   a.units_per_kvh = a.Tr * (group / nq);
   const double scale = p->scale > 0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(D));
   a.c_scale = static_cast<float>(scale * 1.4426950408889634);

@@ -87,6 +87,7 @@ struct FwdArgs {
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
   const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
+  int pair;            // host: 2 = launched as CTA pairs (one query tile per CTA), else 1
   long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
@@ -121,10 +122,14 @@ constexpr int kTraceSlots = 16;
   } while (0)
 #endif
 
-template <int D, int BC, int NQ, int SPLIT, int MODE>
+// PAIR == 2: a CTA pair (cluster of 2) shares every K/V tile through M = 256 tcgen05 MMAs
+// (cta_group::2): each CTA holds ONE query tile (NQ == 1 locally), half of each K tile's rows
+// and half of each V tile's columns, so a K/V stage is half as large and S can be double
+// buffered in TMEM.
+template <int D, int BC, int NQ, int SPLIT, int MODE, int PAIR = 1>
 struct Cfg {
   static constexpr int kQBytes = kBR * D * 2;
-  static constexpr int kKVBytes = BC * D * 2;
+  static constexpr int kKVBytes = BC * D * 2 / PAIR;
   static constexpr int kDCh = D / 64;  // 64-column (128-byte) swizzle chunks
   // softmax column split: each row of a tile is shared by SPLIT threads (one per warpgroup)
   static constexpr int kCP = BC / SPLIT;             // S columns per part
@@ -158,6 +163,7 @@ struct Cfg {
 
 template <int NS, int NQ, int SB>
 struct __align__(16) Ctl {
+  uint32_t skip2[SB][2];       // CTA pair: each CTA's skip decision, gathered in the leader
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
@@ -317,12 +323,13 @@ __device__ __forceinline__ void p_chunk(const float* v, float2 cs2, float2 nmu2,
 }
 
 // ------------------------------------------------------------------------------------
-template <int D, int BC, int NQ, int MODE, int SPLIT>
+template <int D, int BC, int NQ, int MODE, int SPLIT, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
-  using C = Cfg<D, BC, NQ, SPLIT, MODE>;
+  using C = Cfg<D, BC, NQ, SPLIT, MODE, PAIR>;
+  static_assert(PAIR == 1 || (NQ == 1 && SPLIT == 4 && D == 128), "CTA pairs: one local tile, d = 128");
   constexpr int NS = C::kStages;
   constexpr int CP = C::kCP;
   constexpr int OP = C::kOP;
@@ -342,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  const uint32_t crank = PAIR == 2 ? cluster_ctarank() : 0;  // CTA rank in the pair (0 = leader)
 
   if (tid == 0) {
     VFA_TRACE_UNIT(a, 0);
@@ -349,9 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&ctl->q_full[t], 1);
       for (int b = 0; b < SB; ++b) {
         mbar_init(&ctl->s_full[t][b], 1);
-        mbar_init(&ctl->s_free[t][b], C::kWarpsPerTile);
-        mbar_init(&ctl->p_full[t][b][0], C::kWarpsPerTile);
-        mbar_init(&ctl->p_full[t][b][1], C::kWarpsPerTile);
+        // a pair's leader barriers count the softmax warps of both CTAs
+        mbar_init(&ctl->s_free[t][b], C::kWarpsPerTile * PAIR);
+        mbar_init(&ctl->p_full[t][b][0], C::kWarpsPerTile * PAIR);
+        mbar_init(&ctl->p_full[t][b][1], C::kWarpsPerTile * PAIR);
       }
       mbar_init(&ctl->pv_done[t], 1);
       mbar_init(&ctl->o_final[t], 1);
@@ -368,17 +377,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmR);
   }
-  if (warp == kMmaWarp) tmem_alloc<C::kTmemCols>(&ctl->tmem_base);
+  if (warp == kMmaWarp) {
+    if constexpr (PAIR == 2)
+      tmem_alloc_pair<C::kTmemCols>(&ctl->tmem_base);
+    else
+      tmem_alloc<C::kTmemCols>(&ctl->tmem_base);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR == 2) cluster_sync_all();  // peer barriers initialised before any remote op
   tc_fence_after();
+  // the query head of local tile t (a pair's CTAs each hold one of the unit's two heads)
+  auto head_of = [&](const Unit& u, int t) { return u.h0 + (PAIR == 2 ? static_cast<int>(crank) : t); };
+  (void)head_of;
+  // softmax -> MMA hand-offs arrive on the MMA-issuing CTA's barrier (the leader of a pair).
+  // The TMEM data they publish is ordered by tcgen05.fence::* around the barrier, so the
+  // follower's remote arrive is relaxed; only the arrive that also publishes a generic store
+  // (the skip flag, `release_store`) pays a cluster-scope release.
+  auto arrive_mma = [&](uint64_t* bar, bool release_store = false) {
+    if constexpr (PAIR == 2) {
+      if (crank == 0)
+        mbar_arrive(bar);
+      else if (release_store)
+        mbar_arrive_cluster(mapa_shared(bar, 0));
+      else
+        mbar_arrive_cluster_relaxed(mapa_shared(bar, 0));
+    } else {
+      (void)release_store;
+      mbar_arrive(bar);
+    }
+  };
+  (void)arrive_mma;
   // Each role re-derives its work description after its setmaxnreg so that nothing
   // computed before the role split has to stay live (or spill) across it.
   // Sequence g = 0 .. G-1: nchunks m-init chunks (S = Q . Krepr^T), then the N visited
   // key blocks in schedule order (S = Q . K^T).
 #define VFA_ROLE_SETUP()                                                       \
   const uint32_t tbase = ctl->tmem_base;                                       \
-  const Unit unit = decode_unit(a, blockIdx.x);                                \
+  const Unit unit = decode_unit(a, PAIR == 2 ? (blockIdx.x >> 1) : blockIdx.x); \
   const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);              \
   const int N = sched.vmax;                                                    \
   int nrep = 0;                                                                \
@@ -395,21 +431,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t pol_q = policy_evict_first();
         const uint64_t pol_kv = policy_evict_last();
         for (int t = 0; t < NQ; ++t) {
-          mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
+          if constexpr (PAIR == 2) {
+            // both CTAs' Q tiles count on the leader's barrier (the pair MMA reads both)
+            if (crank == 0) mbar_arrive_expect_tx(&ctl->q_full[t], 2 * C::kQBytes);
 #pragma unroll
-          for (int c = 0; c < C::kDCh; ++c)
-            tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
-                        unit.h0 + t, unit.b, pol_q);
+            for (int c = 0; c < C::kDCh; ++c)
+              tma_load_4d_pair(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+                               head_of(unit, t), unit.b, pol_q);
+          } else {
+            mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
+#pragma unroll
+            for (int c = 0; c < C::kDCh; ++c)
+              tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+                          head_of(unit, t), unit.b, pol_q);
+          }
         }
         int stage = 0;
         uint32_t phase = 0;
-        auto load_tile = [&](const CUtensorMap* map, int row) {
+        // K-like tiles (keys, key representations): all D columns of BC / PAIR rows; a pair's
+        // CTA r loads rows [r*BC/2, (r+1)*BC/2). V tiles: all BC rows of D / PAIR columns.
+        auto load_tile = [&](const CUtensorMap* map, int row, bool is_v) {
           mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
           uint8_t* dst = sKV + stage * C::kKVBytes;
+          if constexpr (PAIR == 2) {
+            if (crank == 0) mbar_arrive_expect_tx(&ctl->kv_full[stage], 2 * C::kKVBytes);
+            if (is_v) {
+              tma_load_4d_pair(dst, map, &ctl->kv_full[stage], static_cast<int>(crank) * 64, row, unit.kvh, unit.b,
+                               pol_kv);
+            } else {
 #pragma unroll
-          for (int c = 0; c < C::kDCh; ++c)
-            tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
+              for (int c = 0; c < C::kDCh; ++c)
+                tma_load_4d_pair(dst + c * (BC / 2) * 128, map, &ctl->kv_full[stage], c * 64,
+                                 row + static_cast<int>(crank) * (BC / 2), unit.kvh, unit.b, pol_kv);
+            }
+          } else {
+            (void)is_v;
+            mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
+#pragma unroll
+            for (int c = 0; c < C::kDCh; ++c)
+              tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
+          }
           if (++stage == NS) {
             stage = 0;
             phase ^= 1;
@@ -418,25 +479,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the MMA warp's consumption order: op(0 .. SB-1); per g: [V(g)], op(g+SB)
         auto load_s_operand = [&](int g) {
           if (g < nchunks)
-            load_tile(&tmR, g * BC);
+            load_tile(&tmR, g * BC, false);
           else
-            load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
+            load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC, false);
         };
         for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
         for (int g = 0; g < G; ++g) {
-          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC, true);
           if (g + SB < G) load_s_operand(g + SB);
         }
       }
-    } else if (warp == kMmaWarp) {
+    } else if (warp == kMmaWarp && (PAIR == 1 || crank == 0)) {
       // ============================ MMA issuer ============================
+      // (a CTA pair's MMAs are all issued by the leader, M = 256 over both CTAs' tiles)
       // The whole warp runs the issue loop (warp-uniform state in uniform registers); one
       // elected lane issues each tcgen05 instruction. Per element g and query tile t:
       // PV_t(g) then QK_t(g+1), so each tile's next S is issued as soon as its own P is
       // consumed and the two query tiles ping-pong (anti-phase) on the tensor pipe.
       VFA_ROLE_SETUP();
-      constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
-      constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t kIdescQK = make_idesc_bf16(128 * PAIR, BC, false, false);
+      constexpr uint32_t kIdescPV = make_idesc_bf16(128 * PAIR, D, false, true);
+      // pair: commits arrive on both CTAs' barriers (same offset)
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (PAIR == 2) {
+          if (elect_one()) mma_commit_pair(bar);
+          __syncwarp();
+        } else {
+          commit_elect(bar);
+        }
+      };
       // UMMA smem descriptors: hi word constant (SBO = 1024 B, version 1, SWIZZLE_128B),
       // lo word = (address >> 4) | LBO << 16. Addresses < 256 KiB so the start field never carries.
       constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
@@ -464,10 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
-          const uint32_t ok = ((kk >> 2) * (BC * 128) + (kk & 3) * 32) >> 4;
-          if (elect_one())
-            mma_ss(tbase + C::s_off(t, b), (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq),
-                   (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok), kIdescQK, kk > 0 ? 1u : 0u);
+          const uint32_t ok = ((kk >> 2) * ((BC / PAIR) * 128) + (kk & 3) * 32) >> 4;
+          const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq);
+          const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok);
+          if (elect_one()) {
+            if constexpr (PAIR == 2)
+              mma_ss_pair(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+            else
+              mma_ss(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+          }
           __syncwarp();
         }
       };
@@ -481,9 +557,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k2 = 0; k2 < CW / 16; ++k2) {
             const int kk = pp * (CP / 16) + c * (CW / 16) + k2;  // K-step (16 key rows of V)
             const uint32_t pcol = pp * CP + c * (CW / 2) + k2 * 8;
-            if (elect_one())
-              mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol,
-                     (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4)), kIdescPV, first ? 0u : 1u);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
+            if (elect_one()) {
+              if constexpr (PAIR == 2)
+                mma_ts_pair(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, first ? 0u : 1u);
+              else
+                mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, first ? 0u : 1u);
+            }
             __syncwarp();
             first = false;
           }
@@ -499,12 +579,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
         }
         issue_qk(t, b, st);
-        commit_elect(&ctl->s_full[t][b]);
+        commit(&ctl->s_full[t][b]);
       };
       for (int g = 0; g < SB && g < G; ++g) {
         const int st = acquire();
         for (int t = 0; t < NQ; ++t) issue_s_tile(g, t, st);
-        commit_elect(&ctl->kv_empty[st]);
+        commit(&ctl->kv_empty[st]);
       }
       for (int g = 0; g < G; ++g) {
         const bool main_blk = g >= nchunks;
@@ -522,18 +602,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool skip = false;
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-              mbar_wait(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
+              if constexpr (PAIR == 2 && skips(MODE))  // pairs with the follower's release
+                mbar_wait_cluster(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
+              else
+                mbar_wait(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
               tc_fence_after();
               if (c == 0) {
                 if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
-                skip = skips(MODE) && (ctl->skip[t][b] != 0);
+                if constexpr (PAIR == 2)  // the pair's PV is skipped only if both tiles skip
+                  skip = skips(MODE) && ctl->skip2[b][0] != 0 && ctl->skip2[b][1] != 0;
+                else
+                  skip = skips(MODE) && (ctl->skip[t][b] != 0);
               }
               if (!skip) issue_pv_chunk(t, b, vs, c, first);
             }
             p_ph ^= 1u << (t * SB + b);
             if (!skip) o_init |= 1u << t;
-            if (signal_pv) commit_elect(&ctl->pv_done[t]);
-            if (t == NQ - 1) commit_elect(&ctl->kv_empty[vs]);
+            if (signal_pv) commit(&ctl->pv_done[t]);
+            if (t == NQ - 1) commit(&ctl->kv_empty[vs]);
           }
           if (next_s) {
             if (t == 0) ks = acquire();
@@ -541,9 +627,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 5 + 2 * t);
           }
         }
-        if (ks >= 0) commit_elect(&ctl->kv_empty[ks]);
+        if (ks >= 0) commit(&ctl->kv_empty[ks]);
       }
-      for (int t = 0; t < NQ; ++t) commit_elect(&ctl->o_final[t]);
+      for (int t = 0; t < NQ; ++t) commit(&ctl->o_final[t]);
     }
   } else {
     // ============================ softmax WGs ============================
@@ -629,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (e < valid) mx[ti] = fmaxf(mx[ti], v[e]);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl->s_free[t][ch % SB]);
+            if (lane == 0) arrive_mma(&ctl->s_free[t][ch % SB]);
           }
         }
 #pragma unroll
@@ -639,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // block-wise query representation (src/vfa.py:104-106): one seed for the whole tile
 #pragma unroll
         for (int ti = 0; ti < NT; ++ti)
-          m2[ti] = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + unit.h0 + tile0 + ti) * a.Tr + unit.qt] * cs;
+          m2[ti] = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + head_of(unit, tile0 + ti)) * a.Tr + unit.qt] * cs;
       }
 
       const float2 cs2 = make_float2(cs, cs);
@@ -747,10 +833,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (SB == 1 && rescale) rescale_o();
           // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
           if (r == 0 && part == 0) {
-            if (skips(MODE)) ctl->skip[t][b] = skipped ? 1u : 0u;
+            if (skips(MODE)) {
+              if constexpr (PAIR == 2)  // the leader's MMA warp needs both CTAs' decisions
+                st_cluster_u32(mapa_shared(&ctl->skip2[b][crank], 0), skipped ? 1u : 0u);
+              else
+                ctl->skip[t][b] = skipped ? 1u : 0u;
+            }
             if (a.skip_trace) {
               const size_t idx =
-                  ((static_cast<size_t>(unit.b) * a.Hq + unit.h0 + t) * a.Tr + unit.qt) * a.Tc + pos;
+                  ((static_cast<size_t>(unit.b) * a.Hq + head_of(unit, t)) * a.Tr + unit.qt) * a.Tc + pos;
               a.skip_trace[idx] = skipped ? 2 : 1;
             }
           }
@@ -773,7 +864,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&ctl->p_full[t][b][c]);
+                if (lane == 0) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && warp == 0 && c == 0);
               }
             }
             l[ti] = __fadd_rn(l[ti], __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
@@ -784,12 +875,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (rescale) rescale_o();
           }
+          if constexpr (PAIR == 2) {
+            if (skipped) {  // the pair's PV still runs if the other tile keeps the block: P = 0
+              uint32_t z[CW / 2];
+#pragma unroll
+              for (int e = 0; e < CW / 2; ++e) z[e] = 0u;
+#pragma unroll
+              for (int c = 0; c < NCH; ++c) {
+                if constexpr (CW == 32) tmem_st16(tS(t, b) + c * 16, z);
+                else tmem_st8(tS(t, b) + c * 8, z);
+              }
+            }
+          }
           if (skipped || defer) {
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0)
-              for (int c = 0; c < NCH; ++c) mbar_arrive(&ctl->p_full[t][b][c]);
+              for (int c = 0; c < NCH; ++c) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && warp == 0 && c == 0);
           }
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
           if (r == 0 && part == 0 && pos == N - 1 && t == NQ - 1) VFA_TRACE_UNIT(a, 2);
@@ -804,7 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int ti = 0; ti < NT; ++ti) {
         const int t = tile0 + ti;
-        const int h = unit.h0 + t;
+        const int h = head_of(unit, t);
         ctl->xl[t][part][r] = l[ti];
         named_bar_sync(1 + t, SPLIT * kBR);
         float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
@@ -878,10 +981,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR == 2) cluster_sync_all();  // the peer may still be reading our smem / TMEM
   if (tid == 0) VFA_TRACE_UNIT(a, 3);
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(ctl->tmem_base);
+    if constexpr (PAIR == 2)
+      tmem_dealloc_pair<C::kTmemCols>(ctl->tmem_base);
+    else
+      tmem_dealloc<C::kTmemCols>(ctl->tmem_base);
   }
 }
 

@@ -19,13 +19,14 @@ ap.add_argument("--k-block", type=int, default=128)
 ap.add_argument("--head-dim", type=int, default=128)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--n-local", type=int, default=1)
+ap.add_argument("--pair", type=int, default=0)
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 cfg["d"] = a.head_dim
 dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block,
-           n_local=a.n_local)
+           n_local=a.n_local, cta_pair=a.pair)
 sh = torch.cuda.current_stream().cuda_stream
 for _ in range(a.iters):
     r.krepr(sh)

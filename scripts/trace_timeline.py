@@ -23,6 +23,7 @@ ap.add_argument("--k-block", type=int, default=128)
 ap.add_argument("--n-local", type=int, default=1)
 ap.add_argument("--sink", type=float, default=0.0, help="planted-sink boost (C3 data); 0 = Gaussian")
 ap.add_argument("--lam", type=float, default=1e-2)
+ap.add_argument("--pair", type=int, default=0, help="cta_pair (2 = CTA pairs)")
 a = ap.parse_args()
 cfg = CONFIGS["c2"]
 dev = torch.device("cuda", 0)
@@ -30,9 +31,10 @@ q, k, v = make_inputs(cfg, dev)
 if a.sink:
     from scripts.sweeps import planted_sink
     planted_sink(q, k, a.sink, a.k_block)
-r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local)
+r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local,
+           cta_pair=a.pair)
 T = cfg["L"] // a.k_block
-units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
+units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2) * (2 if a.pair == 2 else 1)
 buf = torch.zeros(T * 16 + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)

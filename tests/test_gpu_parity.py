@@ -615,3 +615,58 @@ def test_every_variant_on_mixed_geometries(variant, geom):
     ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **okw)
     _compare(out, lse, ref_o, ref_lse, str(kw))
     assert st["visited"] == ref_st["visited"]
+
+
+
+PAIR_VARIANTS = [("fa", {}), ("vfa", {}), ("vsa", dict(lam=1e-2)), ("blasst", dict(lam=1e-2)),
+                 ("blasst_fa4", dict(lam=1e-2, tau=1.0)), ("blasst_rowskip", dict(lam=1e-2))]
+
+
+@pytest.mark.parametrize("variant,extra", PAIR_VARIANTS, ids=[v for v, _ in PAIR_VARIANTS])
+@pytest.mark.parametrize("bc", [64, 128])
+@pytest.mark.parametrize("causal", [True, False])
+def test_cta_pair_against_oracle(variant, extra, bc, causal):
+    # cta_group::2 path: the unit's two query heads on a CTA pair, K/V tiles split between the
+    # two SMs' shared memory and consumed by M = 256 MMAs issued by the leader CTA. Planted
+    # sink so that the skipping variants skip / elide / mask.
+    B, Hq, Hkv, L, d = 1, 4, 2, 640, 128
+    q, k, v = _rand((B, Hq, L, d), 211), _rand((B, Hkv, L, d), 212), _rand((B, Hkv, L, d), 213)
+    if variant not in ("fa", "vfa"):
+        amp = float(np.sqrt(8.0 * np.sqrt(d)))
+        q[..., 0] = amp
+        k[..., 0] = 0
+        k[:, :, :bc, 0] = amp
+    kw = dict(variant=variant, causal=causal, q_block=128, k_block=bc, **extra)
+    okw = dict(kw)
+    if variant.startswith("blasst"):
+        kw["reorder"] = False
+    out, lse, _, st = _run_gpu(q, k, v, cta_pair=2, **kw)
+    qf, kf, vf = _f64(q), _f64(k), _f64(v)
+    o_ref, l_ref = np.empty(out.shape), np.empty(lse.shape)
+    visited = 0
+    for h in range(Hq):
+        r = vo.forward_head(qf[0, h], kf[0, h // 2], vf[0, h // 2], **okw)
+        o_ref[0, h], l_ref[0, h] = r.out, r.lse
+        visited += r.visited
+    _compare(out, lse, o_ref, l_ref, f"{kw} pair")
+    assert st["visited"] == visited
+    # the pair and single-CTA paths take identical skip decisions
+    out1, lse1, _, st1 = _run_gpu(q, k, v, cta_pair=1, softmax_split=4, **kw)
+    assert st == st1
+    if variant == "vfa":  # frozen max: same per-row arithmetic in both layouts
+        assert torch.equal(out, out1) and torch.equal(lse, lse1)
+
+
+def test_cta_pair_falls_back_where_ineligible():
+    # odd GQA groups and d = 64 cannot pair: cta_pair = 2 runs the single-CTA kernel there
+    for (hq, hkv, d) in [(3, 1, 128), (2, 1, 64)]:
+        q, k, v = _rand((1, hq, 256, d), 221), _rand((1, hkv, 256, d), 222), _rand((1, hkv, 256, d), 223)
+        o2, l2, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True, cta_pair=2)
+        o1, l1, _, _ = _run_gpu(q, k, v, variant="vfa", causal=True, cta_pair=1)
+        assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+def test_cta_pair_rejects_bad_value():
+    q, k, v = _rand((1, 2, 128, 128), 231), _rand((1, 1, 128, 128), 232), _rand((1, 1, 128, 128), 233)
+    with pytest.raises(ValueError):
+        _run_gpu(q, k, v, variant="vfa", causal=True, cta_pair=3)

@@ -40,8 +40,8 @@ def test_library_exports_every_header_symbol(lib):
 def test_params_struct_layout_matches_header():
     from paper_2604_12798_b200._lib import VfaParams
     # 6 int64 + 12 int64 strides + double + 12 int32 + double + 2 int32
-    # + softmax_split (int32) and tau (double)
-    assert ctypes.sizeof(VfaParams) == 6 * 8 + 12 * 8 + 8 + 12 * 4 + 8 + 2 * 4 + 8
+    # + softmax_split (int32), tau (double), cta_pair + reserved (int32)
+    assert ctypes.sizeof(VfaParams) == 6 * 8 + 12 * 8 + 8 + 12 * 4 + 8 + 2 * 4 + 8 + 2 * 4
 
 
 def _params(**kw):
