@@ -20,6 +20,7 @@ ap.add_argument("--head-dim", type=int, default=128)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--n-local", type=int, default=1)
 ap.add_argument("--pair", type=int, default=0)
+ap.add_argument("--stats-out", default=None, help="write the pass's block-class counts here (JSON)")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 cfg["d"] = a.head_dim
@@ -33,3 +34,8 @@ for _ in range(a.iters):
     r.attn(sh)
 torch.cuda.synchronize()
 print(a.variant, r.stats_dict())
+if a.stats_out:
+    import json
+    with open(a.stats_out, "w") as f:
+        json.dump(dict(variant=a.variant, d=a.head_dim, k_block=a.k_block, n_local=a.n_local, B=cfg["B"],
+                       Hq=cfg["Hq"], Hkv=cfg["Hkv"], L=cfg["L"], stats=r.stats_dict()), f)
