@@ -20,14 +20,19 @@ ap.add_argument("--head-dim", type=int, default=128)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--n-local", type=int, default=1)
 ap.add_argument("--pair", type=int, default=0)
+ap.add_argument("--lib", default=None, help="experiment build (libvfa_b200_<name>.so) instead of the product library")
 ap.add_argument("--stats-out", default=None, help="write the pass's block-class counts here (JSON)")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 cfg["d"] = a.head_dim
 dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
+lib = None
+if a.lib:
+    from paper_2604_12798_b200 import _lib
+    lib = _lib.bind(os.path.abspath(a.lib))
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block,
-           n_local=a.n_local, cta_pair=a.pair)
+           n_local=a.n_local, cta_pair=a.pair, lib=lib)
 sh = torch.cuda.current_stream().cuda_stream
 for _ in range(a.iters):
     r.krepr(sh)
