@@ -449,7 +449,7 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     status = torch.empty(_lib.STATUS_COUNT, dtype=torch.int32, device=dev)
     trace = None
     if skip_trace:
-        trace = torch.empty((q.shape[0], q.shape[1], q.shape[2] // 128, k.shape[2] // k_block),
+        trace = torch.empty((q.shape[0], q.shape[1], q.shape[2] // q_block, k.shape[2] // k_block),
                             dtype=torch.uint8, device=dev)
     stab = torch.empty(q.shape[:3], dtype=torch.int32, device=dev) if stab_trace else None
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream

@@ -105,9 +105,9 @@ size_t ws_krepr_bytes(const VfaParams* p) {
   return static_cast<size_t>(p->batch * p->heads_kv * n_reprs(p) * p->head_dim * 2 + 255) / 256 * 256;
 }
 size_t ws_qrepr_bytes(const VfaParams* p) {
-  return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * p->head_dim * 2 + 255) / 256 * 256;
+  return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / p->q_block) * p->head_dim * 2 + 255) / 256 * 256;
 }
-size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * 4); }
+size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / p->q_block) * 4); }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
@@ -142,7 +142,10 @@ int vfa_check_params(const VfaParams* p) {
   if (p->kind < VFA_KREPR_SABSMAX || p->kind > VFA_KREPR_K_ABSMAX_UNSIGNED)
     return fail(VFA_ERR_CONFIG, "unknown key representation");
   if (p->qkind < 0 || p->qkind > 3) return fail(VFA_ERR_CONFIG, "unknown query representation");
-  if (p->q_block != 128) return fail(VFA_ERR_CONFIG, "q_block must be 128 (tcgen05 M = 128)");
+  // a 128-row tcgen05 tile holds one reference query block; q_block < 128 leaves rows idle
+  // (same schedule / statistics as the reference at that block size, 128 / q_block x the work)
+  if (p->q_block != 128 && p->q_block != 64 && p->q_block != 32 && p->q_block != 16)
+    return fail(VFA_ERR_CONFIG, "q_block must be 16, 32, 64 or 128 (tcgen05 M = 128 tiles)");
   if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
   if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
   if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
@@ -228,7 +231,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   const int nq = (group % 2 == 0) ? 2 : 1;
   // CTA pairs (cta_pair = 2, or auto): the unit's two query heads on two SMs sharing each K/V
   // tile through M = 256 MMAs; needs an even GQA group and d = 128
-  const bool pair_ok = nq == 2 && D == 128;
+  const bool pair_ok = nq == 2 && D == 128 && p->q_block == 128;
   const int pair = (pair_ok && (p->cta_pair == 2 || (p->cta_pair == 0 && default_pair(p->variant)))) ? 2 : 1;
 
   CUtensorMap mq, mk, mv, mr;
@@ -252,8 +255,8 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
     // block-wise query representation: per query tile, seed = max_j qrepr . krepr_j
     uint8_t* qrep = static_cast<uint8_t*>(workspace) + ws_krepr_bytes(p);
     float* m0 = reinterpret_cast<float*>(qrep + ws_qrepr_bytes(p));
-    const int tr = static_cast<int>(p->seq_q / 128);
-    rc = launch_block_repr(q, p->batch, p->heads_q, p->q_stride, D, 128, tr, qkind_as_block_kind(p->qkind), qrep, 0,
+    const int tr = static_cast<int>(p->seq_q / p->q_block);
+    rc = launch_block_repr(q, p->batch, p->heads_q, p->q_stride, D, p->q_block, tr, qkind_as_block_kind(p->qkind), qrep, 0,
                            st);
     if (rc) return rc;
     dim3 grid((tr + 3) / 4, static_cast<unsigned>(p->heads_q), static_cast<unsigned>(p->batch));
@@ -262,12 +265,12 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
     const int tc = static_cast<int>(n_key_blocks(p));
     if (D == 128)
       vfa::minit_block_kernel<128><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
-                                                         static_cast<int>(p->heads_kv), tr, static_cast<int>(nrep),
-                                                         BC, tc, p->causal ? 1 : 0, m0);
+                                                         static_cast<int>(p->heads_kv), tr, p->q_block,
+                                                         static_cast<int>(nrep), BC, tc, p->causal ? 1 : 0, m0);
     else
       vfa::minit_block_kernel<64><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
-                                                        static_cast<int>(p->heads_kv), tr, static_cast<int>(nrep), BC,
-                                                        tc, p->causal ? 1 : 0, m0);
+                                                        static_cast<int>(p->heads_kv), tr, p->q_block,
+                                                        static_cast<int>(nrep), BC, tc, p->causal ? 1 : 0, m0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("m-init seed launch: ") + cudaGetErrorString(e));
     m0_tile = m0;
@@ -275,7 +278,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   if (zero_counters) reset_counters(stats, status, st);
   if (skip_trace)
     cudaMemsetAsync(skip_trace, 0,
-                    static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / 128) * n_key_blocks(p)), st);
+                    static_cast<size_t>(p->batch * p->heads_q * (p->seq_q / p->q_block) * n_key_blocks(p)), st);
 
   vfa::FwdArgs a;
   a.B = static_cast<int>(p->batch);
@@ -284,7 +287,8 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.Lq = static_cast<int>(p->seq_q);
   a.Lk = static_cast<int>(p->seq_k);
   a.group = group;
-  a.Tr = static_cast<int>(p->seq_q / 128);
+  a.Tr = static_cast<int>(p->seq_q / p->q_block);
+  a.qrows = p->q_block;
   a.Tc = static_cast<int>(n_key_blocks(p));
   a.heads_per_unit = nq;
   a.pair = pair;

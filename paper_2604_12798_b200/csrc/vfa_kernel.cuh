@@ -75,6 +75,8 @@ constexpr bool skips(int m) { return m == kVSA || m == kBL || m == kBL4 || m == 
 struct FwdArgs {
   int B, Hq, Hkv, Lq, Lk, group, Tr, Tc;
   int units_per_kvh, heads_per_unit;
+  int qrows;          // query rows per reference block (q_block | 128): a 128-row MMA tile holds
+                      // query block qt's qrows rows; the rest are idle lanes (never stored)
   float c_scale;      // softmax scale * log2(e)
   float log2_lambda;  // skip threshold in log2 units (-inf: no skipping)
   float tau;          // BLASST-FA4 elision threshold: max increase tau*ln2 (natural) = tau (log2)
@@ -202,7 +204,7 @@ __device__ __forceinline__ TileSchedule unit_schedule(const FwdArgs& a, int qt, 
   // FA / BLASST-FA4 / rowskip: ascending, all exact; BLASST: the VFA visit order when
   // reorder (order='sink_local', src/sparse.py:133) but every block exact
   constexpr bool kSeq = MODE == kFA || MODE == kBL4 || MODE == kBLR;
-  return make_schedule(qt + 1, kBR, BC, a.Tc, a.causal != 0, a.n_sink, a.n_local, kSeq ? false : (a.reorder != 0),
+  return make_schedule(qt + 1, a.qrows, BC, a.Tc, a.causal != 0, a.n_sink, a.n_local, kSeq ? false : (a.reorder != 0),
                        kSeq);
 }
 
@@ -436,13 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (crank == 0) mbar_arrive_expect_tx(&ctl->q_full[t], 2 * C::kQBytes);
 #pragma unroll
             for (int c = 0; c < C::kDCh; ++c)
-              tma_load_4d_pair(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+              tma_load_4d_pair(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * a.qrows,
                                head_of(unit, t), unit.b, pol_q);
           } else {
             mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
 #pragma unroll
             for (int c = 0; c < C::kDCh; ++c)
-              tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+              tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * a.qrows,
                           head_of(unit, t), unit.b, pol_q);
           }
         }
@@ -647,7 +649,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int r = tid & 127;
       VFA_ROLE_SETUP();
       const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const int R = unit.qt * kBR + r;  // absolute query row
+      const int R = unit.qt * a.qrows + r;  // absolute query row
+      // rows past the reference block (q_block < 128) compute on the next block's queries and are
+      // discarded: they vote "skippable" / "elidable", count nothing and store nothing
+      const bool live = r < a.qrows;
       const float cs = a.c_scale;
       float m2[NT], l[NT];  // running max (log2 units of scaled scores; identical in all parts)
       uint32_t xpar[NT];    // and this part's share of the normalizer, per served tile
@@ -734,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int pos = 0; pos < N; ++pos) {
         const int j = sched_block(sched, pos);
         const bool special = all_exact(MODE) || sched_is_special(sched, j);
-        const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
+        const bool mask = sched_needs_mask(unit.qt + 1, j, a.qrows, BC, a.causal != 0);
         const int lim = R - (j - 1) * BC - part * CP;  // this part's columns > lim are masked
 #pragma unroll
         for (int ti = 0; ti < NT; ++ti) {
@@ -761,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float pm = part_max<CP>(v);
             const float pm2 = pm * cs;
             const bool below = (pm2 - fmaxf(m2[ti], pm2) < a.log2_lambda) ||
-                               (pm2 == -INFINITY && m2[ti] == -INFINITY && a.log2_lambda != -INFINITY);
+                               (pm2 == -INFINITY && m2[ti] == -INFINITY && a.log2_lambda != -INFINITY) || !live;
             skipped = named_bar_and(1 + t, SPLIT * kBR, below);
             if (skipped) ++n_skipped;
           } else if (MODE != kVFA || special) {
@@ -773,21 +778,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool keep = true;  // rowskip: this row takes part in the update
             if (MODE == kBLR) {
               // row-granular threshold (src/sparse.py:223-227): NaN (dead row) is not kept
-              keep = (a.log2_lambda == -INFINITY) || (mt2 - m2n >= a.log2_lambda);
+              keep = live && ((a.log2_lambda == -INFINITY) || (mt2 - m2n >= a.log2_lambda));
               skipped = named_bar_and(1 + t, SPLIT * kBR, !keep);
             } else if (skips(MODE)) {
               const bool below = (mt2 - m2n < a.log2_lambda) ||
-                                 (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
+                                 (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY) || !live;
               skipped = named_bar_and(1 + t, SPLIT * kBR, below);
             }
             bool elide = false;
             if (MODE == kBL4 && !skipped) {
               // rescale elision (src/sparse.py:187-193): every row had a finite max and none rose
               // by more than tau*ln2 -> keep the old max, factor exactly 1
-              elide = named_bar_and(1 + t, SPLIT * kBR, m2[ti] != -INFINITY && m2n - m2[ti] <= a.tau);
+              elide = named_bar_and(1 + t, SPLIT * kBR, (m2[ti] != -INFINITY && m2n - m2[ti] <= a.tau) || !live);
               n_elided += elide ? 1 : 0;
             }
-            if (MODE == kBLR) n_rows_masked += (skipped || !keep) ? 1 : 0;
+            if (MODE == kBLR && live) n_rows_masked += (skipped || !keep) ? 1 : 0;
             if (skipped) {
               ++n_skipped;
               n_skipped_special += special ? 1 : 0;
@@ -931,16 +936,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             finite = finite && isfinite(o0) && isfinite(o1);
             u[e >> 1] = pack_bf16x2(o0, o1);
           }
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
-          dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+          if (live) {  // (the TMEM load above is warp-collective: idle lanes take part)
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+            dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+          }
         }
         const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
         const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
-        if (part == 0 && a.lse) a.lse[lrow] = (m2[ti] + __log2f(lsum)) * kLn2;
-        if (part == 0 && a.stab) a.stab[lrow] = stab[ti];
+        finite = finite || !live;
+        if (part == 0 && live && a.lse) a.lse[lrow] = (m2[ti] + __log2f(lsum)) * kLn2;
+        if (part == 0 && live && a.stab) a.stab[lrow] = stab[ti];
         if (a.status) {
-          if (part == 0 && lsum == 0.f) {
+          if (part == 0 && live && lsum == 0.f) {
             if (m2[ti] == -INFINITY) {
               atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
               atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
@@ -959,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (any_nonfinite) atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
       if (a.stats) {
-        if (a.monitor) {
+        if (a.monitor && live) {
           atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
           atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
         }
@@ -1065,14 +1073,14 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
 template <int D>
 __global__ void __launch_bounds__(128) minit_block_kernel(const __nv_bfloat16* __restrict__ qrep,
                                                           const __nv_bfloat16* __restrict__ krep, int Hq, int Hkv,
-                                                          int Tr, int nrep, int BC, int Tc, int causal,
+                                                          int Tr, int QR, int nrep, int BC, int Tc, int causal,
                                                           float* __restrict__ m0) {
   constexpr int CPL = D / 32;
   const int w = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
   if (w >= Tr) return;
   const int i = w + 1;  // 1-based query tile
-  const int vmax = causal ? min((i * kBR - 1) / BC + 1, Tc) : Tc;
+  const int vmax = causal ? min((i * QR - 1) / BC + 1, Tc) : Tc;  // QR = q_block
   const int cap = vmax < nrep ? vmax : nrep;
   const int kvh = h / (Hq / Hkv);
   float qv[CPL];

@@ -22,8 +22,8 @@ from . import api, vft1
 
 EXIT_OK, EXIT_CONFIG, EXIT_DATA, EXIT_NUMERICAL = 0, 2, 3, 4
 VARIANTS = ("fa", "vfa", "blasst", "blasst_swa", "blasst_fa4", "blasst_rowskip", "vsa")  # src/cli.py:60-67
-# the reference's run defaults (src/cli.py:83-105) except q_block: tcgen05 tiles are 128 rows
-DEFAULTS = {"q_block": 128, "k_block": 64, "causal": False, "variant": "fa", "repr": "sabsmax",
+# the reference's run defaults (src/cli.py:83-105)
+DEFAULTS = {"q_block": 64, "k_block": 64, "causal": False, "variant": "fa", "repr": "sabsmax",
             "q_repr": "row_wise", "lambda": None, "tau": 0.0, "reorder": True, "m_init": True,
             "monitor": False, "tc1": None}
 

@@ -217,6 +217,21 @@ def main():
     cases.append(("blasst_fa4_k64_tau2_sink", s, sink, True, "blasst_fa4", dict(lam=1e-2, tau=2.0)))
     cases.append(("blasst_rowskip_k64_midpeak_lam1e-2", s, mp, True, "blasst_rowskip", dict(lam=1e-2)))
 
+    # query blocks smaller than the GPU's 128-row MMA tile (the reference CLI defaults to 64/64):
+    # the GPU holds one reference block per tile, so schedules and statistics are the reference's
+    s = BlockSpec(512, 512, 64, 64, 64)
+    cases.append(("fa_q64k64_causal", s, gen_gaussian(s, 16), True, "fa", {}))
+    cases.append(("vfa_q64k64_causal_s1l2", s, gen_gaussian(s, 17), True, "vfa", dict(n_local=2)))
+    s = BlockSpec(512, 512, 128, 32, 64)
+    cases.append(("vfa_q32k64_d128_causal", s, gen_gaussian(s, 18), True, "vfa", {}))
+    s = BlockSpec(256, 256, 64, 16, 64)
+    cases.append(("vfa_q16k64_noncausal_q_mean", s, gen_gaussian(s, 19), False, "vfa", dict(qkind="q_mean")))
+    s = BlockSpec(1024, 1024, 64, 64, 128)
+    cases.append(("vsa_sink_q64_lam1e-2", s, sink, True, "vsa", dict(lam=1e-2)))
+    cases.append(("blasst_rowskip_sink_q64_lam1e-3", s, sink, True, "blasst_rowskip", dict(lam=1e-3)))
+    s = BlockSpec(1024, 1024, 64, 32, 64)
+    cases.append(("blasst_fa4_sink_q32_lam1e-3_tau8", s, sink, True, "blasst_fa4", dict(lam=1e-3, tau=8.0)))
+
     arrays, meta = {}, []
     for name, spec, data, causal, variant, kw in cases:
         a, rec = run_case(name, spec, data, causal, variant, **dict(kw))

@@ -108,7 +108,7 @@ def test_vfa_options(kind, opts):
 
 
 def _golden_kw(m):
-    kw = dict(variant=m["variant"], causal=m["causal"], q_block=128, k_block=m["k_block"],
+    kw = dict(variant=m["variant"], causal=m["causal"], q_block=m["q_block"], k_block=m["k_block"],
               n_sink=m["n_sink"], n_local=m["n_local"])
     for key in ("kind", "qkind", "reorder", "use_m_init", "tc1", "lam", "tau"):
         if key in m:
@@ -121,8 +121,6 @@ def _golden_kw(m):
 @pytest.mark.parametrize("name", [n for n in case_names()])
 def test_golden_vectors(name):
     m, q, k, v, out32, lse = case(name)
-    if m["q_block"] != 128:
-        pytest.skip("q_block 64 runs on the CPU oracle only (tcgen05 M = 128)")
     from paper_2604_12798_b200 import attention_forward, stats_dict
     from paper_2604_12798_b200.api import NormalizerUnderflowError
     qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda()[None, None]
@@ -174,7 +172,7 @@ def test_blasst_golden_counters_integer_equal(name):
     m, q, k, v, out32, lse = case(name)
     qb, kb, vb = (torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16).cuda() for x in case_bits(name))
     L, d = qb.shape
-    p = AttentionProblem(qb, kb, vb, blocks=BlockSpec(L, L, d, 128, m["k_block"]), causal=m["causal"])
+    p = AttentionProblem(qb, kb, vb, blocks=BlockSpec(L, L, d, m["q_block"], m["k_block"]), causal=m["causal"])
     if m["variant"] == "blasst":
         out, c, stats = blasst_forward(p, SkipConfig(lam=m["lam"]), order=m.get("order", "sequential"))
     elif m["variant"] == "blasst_fa4":
@@ -392,7 +390,7 @@ def test_validation_errors_raise_like_reference():
     with pytest.raises(ValueError):
         attention_forward(q, q, q, variant="vfa", kind="median")
     with pytest.raises(ValueError):
-        attention_forward(q, q, q, variant="vfa", q_block=64)
+        attention_forward(q, q, q, variant="vfa", q_block=48)
     k = _rand((1, 1, 128, 128), 2)
     with pytest.raises(ValueError):
         attention_forward(q, k, k, variant="fa", causal=True)  # causal needs Nq == Nk
@@ -670,3 +668,63 @@ def test_cta_pair_rejects_bad_value():
     q, k, v = _rand((1, 2, 128, 128), 231), _rand((1, 1, 128, 128), 232), _rand((1, 1, 128, 128), 233)
     with pytest.raises(ValueError):
         _run_gpu(q, k, v, variant="vfa", causal=True, cta_pair=3)
+
+
+SMALLQ = [(v, qb) for v in ("fa", "vfa", "vsa", "blasst", "blasst_fa4", "blasst_rowskip") for qb in (16, 32, 64)]
+
+
+@pytest.mark.parametrize("variant,qb", SMALLQ)
+@pytest.mark.parametrize("causal", [True, False])
+def test_small_query_blocks_against_oracle(variant, qb, causal):
+    # q_block < 128 (the reference CLI default is 64): each 128-row MMA tile holds one reference
+    # query block, so the schedule, special / frozen classes and skip decisions are the
+    # reference's at that block size; the idle rows never reach O, LSE or the statistics
+    B, Hq, Hkv, L, d, bc = 1, 4, 2, 512, 64, 64
+    q, k, v = _rand((B, Hq, L, d), 241), _rand((B, Hkv, L, d), 242), _rand((B, Hkv, L, d), 243)
+    extra = {}
+    if variant not in ("fa", "vfa"):
+        amp = float(np.sqrt(8.0 * np.sqrt(d)))
+        q[..., 0] = amp
+        k[..., 0] = 0
+        k[:, :, :bc, 0] = amp
+        extra = dict(lam=1e-2, tau=4.0) if variant == "blasst_fa4" else dict(lam=1e-2)
+    kw = dict(variant=variant, causal=causal, q_block=qb, k_block=bc, **extra)
+    if variant.startswith("blasst"):
+        kw["reorder"] = False
+    out, lse, _, st = _run_gpu(q, k, v, monitor=True, **kw)
+    okw = {key: val for key, val in kw.items() if key != "reorder"}
+    qf, kf, vf = _f64(q), _f64(k), _f64(v)
+    o_ref, l_ref = np.empty(out.shape), np.empty(lse.shape)
+    ref = {"visited": 0, "skipped": 0, "special": 0, "frozen": 0, "elided": 0, "rows_masked": 0}
+    tight = True
+    for h in range(Hq):
+        r = vo.forward_head(qf[0, h], kf[0, h // 2], vf[0, h // 2], record_decisions=True, **okw)
+        o_ref[0, h], l_ref[0, h] = r.out, r.lse
+        for key in ref:
+            ref[key] += getattr(r, key)
+        tight &= all(mg > 1e-3 for blk in r.decisions for (_, _, mg) in blk)
+    _compare(out, lse, o_ref, l_ref, str(kw))
+    assert st["visited"] == ref["visited"]
+    if variant in ("fa", "vfa"):
+        assert (st["special"], st["frozen"]) == (ref["special"], ref["frozen"])
+    if tight:
+        assert st["skipped"] == ref["skipped"]
+        assert st["rows_masked"] == ref["rows_masked"]
+    assert st["count_over_f32"] == 0
+
+
+def test_small_query_blocks_host_pipeline_and_trace():
+    # q_block 64 through the chunked host path (bitwise = device path) and the device
+    # StateTrace / skip trace geometry (one entry per reference query block)
+    from paper_2604_12798_b200 import attention_forward
+    q, k, v = _rand((1, 4, 512, 128), 251), _rand((1, 2, 512, 128), 252), _rand((1, 2, 512, 128), 253)
+    kw = dict(variant="vfa", causal=True, q_block=64, k_block=128)
+    o1, l1, _ = attention_forward(q, k, v, **kw)
+    o2, l2, _ = attention_forward(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory(), **kw)
+    assert torch.equal(o1.cpu(), o2) and torch.equal(l1.cpu(), l2)
+    _, _, info = attention_forward(q, k, v, stab_trace=True, skip_trace=True, **kw)
+    assert info["stab_block"].shape == (1, 4, 512)
+    qf, kf, vf = _f64(q), _f64(k), _f64(v)
+    r = vo.forward_head(qf[0, 0], kf[0, 0], vf[0, 0], **kw)
+    got = info["stab_block"][0, 0].cpu().numpy()
+    assert (got != r.stab).mean() <= 0.01

@@ -59,7 +59,7 @@ def _params(**kw):
 
 
 @pytest.mark.parametrize("field,value,code", [
-    ("variant", 7, 2), ("kind", 9, 2), ("qkind", 4, 2), ("q_block", 64, 2), ("k_block", 96, 2),
+    ("variant", 7, 2), ("kind", 9, 2), ("qkind", 4, 2), ("q_block", 48, 2), ("k_block", 96, 2),
     ("head_dim", 96, 2), ("seq_q", 1000, 3), ("seq_k", 1000, 3), ("heads_q", 3, 3), ("tc1", 99, 2),
     ("n_sink", -1, 2), ("tau", -1.0, 2), ("softmax_split", 3, 2), ("variant", 6, 2),
 ])
