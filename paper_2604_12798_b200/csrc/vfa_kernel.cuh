@@ -97,6 +97,9 @@ struct FwdArgs {
 #ifndef VFA_SB_MAX
 #define VFA_SB_MAX 2  // S buffers per tile (tuning experiments: 1 disables double buffering)
 #endif
+#ifndef VFA_Q_TMEM
+#define VFA_Q_TMEM 1
+#endif
 #ifndef VFA_SB_NQ1
 #define VFA_SB_NQ1 1  // double-buffer S for every mode when a CTA serves one query tile
 #endif
@@ -152,10 +155,17 @@ struct Cfg {
   static constexpr int kSB =
       (NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && (all_exact(MODE) || (NQ == 1 && VFA_SB_NQ1))) ? 2 : 1;
   static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
-    return static_cast<uint32_t>(kSB == 2 ? (t * 2 + b) * BC : t * 128);
+    return static_cast<uint32_t>(kSB == 2 ? (t * 2 + b) * BC : t * BC);
   }
-  static constexpr int kOBase = kSB == 2 ? NQ * 2 * BC : NQ * 128;
-  static constexpr int kColsUsed = kOBase + NQ * D;
+  static constexpr int kOBase = kSB == 2 ? NQ * 2 * BC : NQ * BC;
+  static constexpr int kColsUsed0 = kOBase + NQ * D;
+  // Q resident in TMEM (D/2 columns per tile, bf16 pairs) where it fits, for BC = 64: QK^T then
+  // runs A-from-TMEM, reading only K from shared memory. With both operands in shared memory an
+  // N = 64 MMA is shared-memory bound (48 instead of 32 cycles, profiles/ubench_mma_rate_r01.txt);
+  // at N = 128 both modes run at the 64-cycle floor.
+  static constexpr bool kQT = PAIR == 1 && BC == 64 && VFA_Q_TMEM && kColsUsed0 + NQ * D / 2 <= 512;
+  static constexpr int kQBase = kColsUsed0;
+  static constexpr int kColsUsed = kColsUsed0 + (kQT ? NQ * D / 2 : 0);
   static constexpr uint32_t kTmemCols = kColsUsed <= 256 ? 256 : 512;
   static_assert(kColsUsed <= 512, "TMEM over-subscribed");
   static_assert(kStages >= 3, "not enough shared memory for a K/V ring");
@@ -519,6 +529,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t kv_lo = smem_u32(sKV) >> 4;
       for (int t = 0; t < NQ; ++t) mbar_wait(&ctl->q_full[t], 0);
       tc_fence_after();
+      if constexpr (C::kQT) {
+        // Q_t -> TMEM (lane = row, 8 columns per 16-element K-step); executes ahead of the MMAs
+        // issued after it by this thread (in-order tcgen05 pipe)
+#pragma unroll
+        for (int t = 0; t < NQ; ++t)
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+            const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + t * (C::kQBytes >> 4) + kLboK + oq);
+            if (elect_one()) tmem_cp_128x256b(tbase + C::kQBase + t * (D / 2) + kk * 8, da);
+            __syncwarp();
+          }
+      }
       int stage = 0;
       uint32_t phase = 0;
       auto acquire = [&]() -> int {
@@ -543,6 +566,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) {
             if constexpr (PAIR == 2)
               mma_ss_pair(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+            else if constexpr (C::kQT)
+              mma_ts(tbase + C::s_off(t, b), tbase + C::kQBase + t * (D / 2) + kk * 8, db, kIdescQK, kk > 0 ? 1u : 0u);
             else
               mma_ss(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
           }
@@ -616,8 +641,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                   skip = skips(MODE) && (ctl->skip[t][b] != 0);
               }
+              if (c == NCH - 1 && lane == 0) VFA_TRACE_EVENT(a, pos, 8 + 2 * t);
               if (!skip) issue_pv_chunk(t, b, vs, c, first);
             }
+            if (lane == 0) VFA_TRACE_EVENT(a, pos, 9 + 2 * t);
             p_ph ^= 1u << (t * SB + b);
             if (!skip) o_init |= 1u << t;
             if (signal_pv) commit(&ctl->pv_done[t]);
@@ -625,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (next_s) {
             if (t == 0) ks = acquire();
+            if (main_blk && t == 0 && lane == 0) VFA_TRACE_EVENT(a, pos, 12);
             issue_s_tile(g + SB, t, ks);
             if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 5 + 2 * t);
           }

@@ -14,7 +14,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2604_12798_b200 import _lib, build  # noqa: E402
 
-_lib.LIB_PATH = build.build(trace=True)  # the -DVFA_TRACE variant of the library
+# the -DVFA_TRACE variant of the library (VFA_TRACE_LIB: an experiment build made with
+# build.build(trace=True, defines=(name, flags)))
+_lib.LIB_PATH = os.environ.get("VFA_TRACE_LIB") or build.build(trace=True)
 from bench import CONFIGS, Runner, make_inputs  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -71,6 +73,12 @@ for t in (0, 1):
           f" p90 {np.nanpercentile(busy[sl], 90):.0f}); softmax waits for S {np.nanmedian(wait_s[sl]):.0f};"
           f" MMA sees P after {np.nanmedian(seen[sl]):.0f}; S ready {np.nanmedian(qk_to_s[sl]):.0f} after QK issue;"
           f" period {np.nanmedian(np.diff(s_ready)[sl]):.0f}")
-print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK]")
+print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK,"
+      " mma0 lastP, mma0 PVdone, mma1 lastP, mma1 PVdone, K acq]")
 for i in range(20, min(26, n)):
-    print(" ", np.round(tr[i, :8]).astype(int).tolist())
+    print(" ", np.round(tr[i, :13]).astype(int).tolist())
+for t in (0, 1):
+    sl = slice(4, n - 4)
+    first, last, pvd, qk = tr[:, 4 + 2 * t], tr[:, 8 + 2 * t], tr[:, 9 + 2 * t], tr[:, 5 + 2 * t]
+    print(f" tile {t}: MMA first->last P chunk {np.nanmedian((last - first)[sl]):.0f}; last P -> PV issued "
+          f"{np.nanmedian((pvd - last)[sl]):.0f}; PV issued -> QK issued {np.nanmedian((qk - pvd)[sl]):.0f}")
