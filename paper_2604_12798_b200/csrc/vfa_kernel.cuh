@@ -162,8 +162,9 @@ struct Cfg {
   // Q resident in TMEM (D/2 columns per tile, bf16 pairs) where it fits, for BC = 64: QK^T then
   // runs A-from-TMEM, reading only K from shared memory. With both operands in shared memory an
   // N = 64 MMA is shared-memory bound (48 instead of 32 cycles, profiles/ubench_mma_rate_r01.txt);
-  // at N = 128 both modes run at the 64-cycle floor.
-  static constexpr bool kQT = PAIR == 1 && BC == 64 && VFA_Q_TMEM && kColsUsed0 + NQ * D / 2 <= 512;
+  // at N = 128 both modes run at the 64-cycle floor (VFA_Q_TMEM=2 also moves Q for Bc = 128:
+  // measured slower at d = 64, profiles/ab_r01_chain.txt).
+  static constexpr bool kQT = PAIR == 1 && (BC == 64 || VFA_Q_TMEM == 2) && VFA_Q_TMEM && kColsUsed0 + NQ * D / 2 <= 512;
   static constexpr int kQBase = kColsUsed0;
   static constexpr int kColsUsed = kColsUsed0 + (kQT ? NQ * D / 2 : 0);
   static constexpr uint32_t kTmemCols = kColsUsed <= 256 ? 256 : 512;
