@@ -14,7 +14,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from bench import CONFIGS, Runner, causal_flops, make_inputs, time_interleaved  # noqa: E402
+from bench import CONFIGS, ClockSampler, Runner, causal_flops, make_inputs, time_interleaved  # noqa: E402
 
 
 def planted_sink(q, k, boost, bc):
@@ -87,8 +87,10 @@ def run_c5():
                     r.krepr(sh)
                     r.attn(sh)
             torch.cuda.synchronize()
-            timed = time_interleaved(runners, 10, flush, lambda: None)
-            line = {"config": "C5", "head_dim": d, "k_block": bc, "n_local": nl}
+            clk = ClockSampler(0)
+            with clk:
+                timed = time_interleaved(runners, 10, flush, lambda: None)
+            line = {"config": "C5", "head_dim": d, "k_block": bc, "n_local": nl, "clocks": clk.summary()}
             for name in runners:
                 line[f"{name}_tflops"] = round(flops / timed[name][1] / 1e9, 1)
             line["vfa_speedup"] = round(timed["fa"][1] / timed["vfa"][1], 4)
