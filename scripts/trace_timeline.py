@@ -74,11 +74,14 @@ for t in (0, 1):
           f" MMA sees P after {np.nanmedian(seen[sl]):.0f}; S ready {np.nanmedian(qk_to_s[sl]):.0f} after QK issue;"
           f" period {np.nanmedian(np.diff(s_ready)[sl]):.0f}")
 print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK,"
-      " mma0 lastP, mma0 PVdone, mma1 lastP, mma1 PVdone, K acq]")
+      " mma0 lastP, mma0 PVdone, mma1 lastP, mma1 PVdone, K acq, sm0 enter, sm1 enter]")
 for i in range(20, min(26, n)):
-    print(" ", np.round(tr[i, :13]).astype(int).tolist())
+    print(" ", np.round(tr[i, :15]).astype(int).tolist())
 for t in (0, 1):
     sl = slice(4, n - 4)
     first, last, pvd, qk = tr[:, 4 + 2 * t], tr[:, 8 + 2 * t], tr[:, 9 + 2 * t], tr[:, 5 + 2 * t]
     print(f" tile {t}: MMA first->last P chunk {np.nanmedian((last - first)[sl]):.0f}; last P -> PV issued "
           f"{np.nanmedian((pvd - last)[sl]):.0f}; PV issued -> QK issued {np.nanmedian((qk - pvd)[sl]):.0f}")
+    enter, sready, pdone_prev = tr[:, 13 + t], tr[:, 2 * t], np.roll(tr[:, 2 * t + 1], 1)
+    print(f" tile {t}: softmax enters wait_s {np.nanmedian((enter - pdone_prev)[sl]):.0f} after its previous P; "
+          f"waits {np.nanmedian((sready - enter)[sl]):.0f} in wait_s")
