@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int t = tile0 + ti;
           const int g = nchunks + pos;
           const int b = g % SB;
+          if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 13 + t);
           wait_s(t, g);
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
           if (r == 0 && part == 0 && t == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
