@@ -2,6 +2,7 @@
 // representation kernel launch, per-variant dispatch of the attention kernel, and the
 // host-resident pipelined forward. Device code lives in vfa_kernel.cuh.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -441,6 +442,17 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
   uint8_t* kv_base = base;
   uint8_t* q_base = base + g.kv_slots * g.kv_slot_bytes;
 
+  // debug: VFA_HOST_TIMELINE=1 records timing events along the pipeline and prints them
+  // (ms from entry) to stderr, synchronizing at the end (scripts/host_timeline.py)
+  const bool timeline = std::getenv("VFA_HOST_TIMELINE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  auto mark = [&](const std::string& what, cudaStream_t s) {
+    if (!timeline) return;
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    marks.emplace_back(what, e);
+  };
   std::vector<cudaEvent_t> ev;
   auto new_event = [&]() -> cudaEvent_t {
     cudaEvent_t e = nullptr;
@@ -459,6 +471,7 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
   cudaStreamWaitEvent(hs->h2d, entry, 0);
   cudaStreamWaitEvent(hs->comp[0], entry, 0);
   cudaStreamWaitEvent(hs->comp[1], entry, 0);
+  mark("entry", hs->h2d);
 
   const int64_t D = p->head_dim, group = p->heads_q / p->heads_kv;
   const int64_t per_b = p->heads_kv / g.ck;
@@ -479,6 +492,7 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
     cudaEvent_t kv_in = new_event();
     if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
     cudaEventRecord(kv_in, hs->h2d);
+    mark("kv_in " + std::to_string(gi), hs->h2d);
     if (g.minit) {
       // representations once per group, on the compute stream of its first sub-chunk (a kernel
       // on the copy stream would stall the copies behind the running attention kernels)
@@ -503,17 +517,21 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       cudaEvent_t q_in = new_event(), done = new_event(), out = new_event();
       if (!q_in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
       cudaEventRecord(q_in, hs->h2d);
+      mark("q_in " + std::to_string(c), hs->h2d);
       cudaStream_t cs = hs->comp[c & 1];
       cudaStreamWaitEvent(cs, kv_in, 0);
       cudaStreamWaitEvent(cs, q_in, 0);
+      mark("k_start " + std::to_string(c), cs);
       rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, nullptr, cs,
                         false, static_cast<long long>(loff));
       if (rc) return cleanup(), rc;
       cudaEventRecord(done, cs);
+      mark("k_end " + std::to_string(c), cs);
       cudaStreamWaitEvent(hs->d2h, done, 0);
       cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
       if (lse_host) cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
       cudaEventRecord(out, hs->d2h);
+      mark("out " + std::to_string(c), hs->d2h);
       q_free[c % g.q_slots] = out;
       // the D2H stream has waited for every sub-chunk's kernel of this group by now
       if (si + 1 == g.subs) kv_free[gi % g.kv_slots] = out;
@@ -523,6 +541,16 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
   if (!exit_ev) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
   cudaEventRecord(exit_ev, hs->d2h);
   cudaStreamWaitEvent(caller, exit_ev, 0);
+  if (timeline && !marks.empty()) {
+    cudaError_t se = cudaEventSynchronize(exit_ev);
+    for (auto& m : marks) {
+      float ms = -1.f;
+      cudaError_t ee = cudaEventElapsedTime(&ms, marks.front().second, m.second);
+      std::fprintf(stderr, "vfa_host_timeline %s %.4f %s %s\n", m.first.c_str(), ms, cudaGetErrorName(se),
+                   cudaGetErrorName(ee));
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
   cleanup();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("vfa_fwd_host: ") + cudaGetErrorString(e));
