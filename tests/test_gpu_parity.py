@@ -728,3 +728,20 @@ def test_small_query_blocks_host_pipeline_and_trace():
     r = vo.forward_head(qf[0, 0], kf[0, 0], vf[0, 0], **kw)
     got = info["stab_block"][0, 0].cpu().numpy()
     assert (got != r.stab).mean() <= 0.01
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa"])
+@pytest.mark.parametrize("hq,hkv,b,qb,bc", [(3, 1, 2, 64, 128), (2, 2, 1, 32, 128), (4, 2, 1, 16, 64)])
+def test_small_query_blocks_geometries(variant, hq, hkv, b, qb, bc):
+    # small reference query blocks with d = 128, odd GQA groups (one tile per CTA), batch > 1
+    L, d = 384, 128
+    q, k, v = _rand((b, hq, L, d), 261), _rand((b, hkv, L, d), 262), _rand((b, hkv, L, d), 263)
+    kw = dict(variant=variant, causal=True, q_block=qb, k_block=bc)
+    if variant == "vsa":
+        kw["lam"] = 1e-2
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    assert st["visited"] == ref_st["visited"]
+    if variant != "vsa":
+        assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
