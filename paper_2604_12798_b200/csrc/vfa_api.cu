@@ -504,8 +504,22 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
       cudaEventRecord(kv_in, cs0);
     }
-    for (int64_t si = 0; si < g.subs; ++si, ++c) {
-      const int64_t h0 = kv0 * group + si * g.nqs;
+    // The first and last K/V groups run in half-size query sub-chunks: the pipeline's fill (the
+    // first copies before any kernel) and drain (the last kernel and its copy-back, after the
+    // last H2D) shrink. Only where the smaller sub-chunk
+    // computes bit-identically (an even head count, or VFA's 4-threads-per-row layout, which a
+    // single-tile CTA also uses).
+    const bool same_bits = (g.nqs / 2) % 2 == 0 ||
+                           (p->variant == VFA_VARIANT_VFA && (p->softmax_split == 0 || p->softmax_split == 4));
+    const bool tail = (gi == g.groups - 1 || gi == 0) && g.ck == 1 && g.nqs >= 2 && g.nqs % 2 == 0 && g.groups > 1 && same_bits;
+    const int64_t nq_g = tail ? g.nqs / 2 : g.nqs;
+    VfaParams cpg = g.cp;
+    cpg.heads_q = nq_g;
+    const size_t q_bytes_g = static_cast<size_t>(nq_g * p->seq_q * D * 2);
+    const size_t lse_bytes_g = static_cast<size_t>(nq_g * p->seq_q * 4);
+    const int64_t subs_g = g.subs * (g.nqs / nq_g);
+    for (int64_t si = 0; si < subs_g; ++si, ++c) {
+      const int64_t h0 = kv0 * group + si * nq_g;
       uint8_t* qsl = q_base + (c % g.q_slots) * g.q_slot_bytes;
       uint8_t* dq = qsl;
       uint8_t* dout = dq + align_up(g.q_bytes);
@@ -513,7 +527,7 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
       const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
       if (q_free[c % g.q_slots]) cudaStreamWaitEvent(hs->h2d, q_free[c % g.q_slots], 0);
-      cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, g.q_bytes, cudaMemcpyHostToDevice, hs->h2d);
+      cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, q_bytes_g, cudaMemcpyHostToDevice, hs->h2d);
       cudaEvent_t q_in = new_event(), done = new_event(), out = new_event();
       if (!q_in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
       cudaEventRecord(q_in, hs->h2d);
@@ -522,19 +536,19 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       cudaStreamWaitEvent(cs, kv_in, 0);
       cudaStreamWaitEvent(cs, q_in, 0);
       mark("k_start " + std::to_string(c), cs);
-      rc = forward_impl(&g.cp, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, nullptr, cs,
+      rc = forward_impl(&cpg, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, nullptr, cs,
                         false, static_cast<long long>(loff));
       if (rc) return cleanup(), rc;
       cudaEventRecord(done, cs);
       mark("k_end " + std::to_string(c), cs);
       cudaStreamWaitEvent(hs->d2h, done, 0);
-      cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, g.q_bytes, cudaMemcpyDeviceToHost, hs->d2h);
-      if (lse_host) cudaMemcpyAsync(lse_host + loff, dlse, g.lse_bytes, cudaMemcpyDeviceToHost, hs->d2h);
+      cudaMemcpyAsync(static_cast<uint8_t*>(o_host) + qoff, dout, q_bytes_g, cudaMemcpyDeviceToHost, hs->d2h);
+      if (lse_host) cudaMemcpyAsync(lse_host + loff, dlse, lse_bytes_g, cudaMemcpyDeviceToHost, hs->d2h);
       cudaEventRecord(out, hs->d2h);
       mark("out " + std::to_string(c), hs->d2h);
       q_free[c % g.q_slots] = out;
       // the D2H stream has waited for every sub-chunk's kernel of this group by now
-      if (si + 1 == g.subs) kv_free[gi % g.kv_slots] = out;
+      if (si + 1 == subs_g) kv_free[gi % g.kv_slots] = out;
     }
   }
   cudaEvent_t exit_ev = new_event();
