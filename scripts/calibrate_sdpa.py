@@ -37,6 +37,15 @@ for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLA
         print(f"sdpa[{name}] {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s", flush=True)
     except Exception as e:  # noqa: BLE001
         print(f"sdpa[{name}] unavailable: {str(e).splitlines()[0][:120]}", flush=True)
+# cuDNN without the GQA flag: K / V expanded to the query heads
+ke, ve = (x.repeat_interleave(Hq // Hkv, dim=1) for x in (k, v))
+for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION),):
+    try:
+        with sdpa_kernel(be):
+            ms = timeit(lambda: F.scaled_dot_product_attention(q, ke, ve, is_causal=True))
+        print(f"sdpa[{name}, K/V expanded] {ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s", flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(f"sdpa[{name}, K/V expanded] unavailable: {str(e).splitlines()[0][:120]}", flush=True)
 try:
     import flashinfer
     qf = q[0].transpose(0, 1).contiguous()  # [L, Hq, d]
