@@ -112,6 +112,9 @@ size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+#ifndef VFA_PAIR_NQ2
+#define VFA_PAIR_NQ2 1
+#endif
 // CTA pairs off by default: measured slower than one CTA per unit (profiles/ab_r01_pair.txt);
 // cta_pair = 2 selects them per call
 #ifndef VFA_PAIR_DEFAULT
@@ -234,6 +237,9 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   // tile through M = 256 MMAs; needs an even GQA group and d = 128
   const bool pair_ok = nq == 2 && D == 128 && p->q_block == 128;
   const int pair = (pair_ok && (p->cta_pair == 2 || (p->cta_pair == 0 && default_pair(p->variant)))) ? 2 : 1;
+  // a pair holds two query tiles per CTA (four heads per cluster, the tiles ping-pong on the
+  // tensor pipe as in the single-CTA kernel) when the GQA group allows, else one
+  const int pair_nq = (VFA_PAIR_NQ2 && group % 4 == 0) ? 2 : 1;
 
   CUtensorMap mq, mk, mv, mr;
   if (!make_map(&mq, q, p->batch, p->heads_q, p->seq_q, D, p->q_stride[0], p->q_stride[1], p->q_stride[2], 128) ||
@@ -291,9 +297,9 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.Tr = static_cast<int>(p->seq_q / p->q_block);
   a.qrows = p->q_block;
   a.Tc = static_cast<int>(n_key_blocks(p));
-  a.heads_per_unit = nq;
+  a.heads_per_unit = pair == 2 ? 2 * pair_nq : nq;
   a.pair = pair;
-  a.units_per_kvh = a.Tr * (group / nq);
+  a.units_per_kvh = a.Tr * (group / a.heads_per_unit);
   const double scale = p->scale > 0 ? p->scale : 1.0 / std::sqrt(static_cast<double>(D));
   a.c_scale = static_cast<float>(scale * 1.4426950408889634);
   a.log2_lambda = (p->variant >= VFA_VARIANT_VSA && p->lam > 0) ? static_cast<float>(std::log2(p->lam)) : -INFINITY;

@@ -176,7 +176,7 @@ struct Cfg {
 
 template <int NS, int NQ, int SB>
 struct __align__(16) Ctl {
-  uint32_t skip2[SB][2];       // CTA pair: each CTA's skip decision, gathered in the leader
+  uint32_t skip2[NQ][SB][2];   // CTA pair: each CTA's skip decision, gathered in the leader
   uint64_t q_full[NQ];
   uint64_t kv_full[NS];
   uint64_t kv_empty[NS];
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
   using C = Cfg<D, BC, NQ, SPLIT, MODE, PAIR>;
-  static_assert(PAIR == 1 || (NQ == 1 && SPLIT == 4 && D == 128), "CTA pairs: one local tile, d = 128");
+  static_assert(PAIR == 1 || (SPLIT == 4 && D == 128), "CTA pairs: d = 128, all softmax warps on every tile");
   constexpr int NS = C::kStages;
   constexpr int CP = C::kCP;
   constexpr int OP = C::kOP;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (PAIR == 2) cluster_sync_all();  // peer barriers initialised before any remote op
   tc_fence_after();
   // the query head of local tile t (a pair's CTAs each hold one of the unit's two heads)
-  auto head_of = [&](const Unit& u, int t) { return u.h0 + (PAIR == 2 ? static_cast<int>(crank) : t); };
+  auto head_of = [&](const Unit& u, int t) { return u.h0 + (PAIR == 2 ? static_cast<int>(crank) * NQ + t : t); };
   (void)head_of;
   // softmax -> MMA hand-offs arrive on the MMA-issuing CTA's barrier (the leader of a pair).
   // The TMEM data they publish is ordered by tcgen05.fence::* around the barrier, so the
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (c == 0) {
                 if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
                 if constexpr (PAIR == 2)  // the pair's PV is skipped only if both tiles skip
-                  skip = skips(MODE) && ctl->skip2[b][0] != 0 && ctl->skip2[b][1] != 0;
+                  skip = skips(MODE) && ctl->skip2[t][b][0] != 0 && ctl->skip2[t][b][1] != 0;
                 else
                   skip = skips(MODE) && (ctl->skip[t][b] != 0);
               }
@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (r == 0 && part == 0) {
             if (skips(MODE)) {
               if constexpr (PAIR == 2)  // the leader's MMA warp needs both CTAs' decisions
-                st_cluster_u32(mapa_shared(&ctl->skip2[b][crank], 0), skipped ? 1u : 0u);
+                st_cluster_u32(mapa_shared(&ctl->skip2[t][b][crank], 0), skipped ? 1u : 0u);
               else
                 ctl->skip[t][b] = skipped ? 1u : 0u;
             }

@@ -36,7 +36,8 @@ if a.sink:
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local,
            cta_pair=a.pair)
 T = cfg["L"] // a.k_block
-units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2) * (2 if a.pair == 2 else 1)
+# CTAs: one per unit (two heads); CTA pairs cover four heads per cluster when the group allows
+units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
 buf = torch.zeros(T * 16 + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)

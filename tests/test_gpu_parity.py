@@ -623,11 +623,12 @@ PAIR_VARIANTS = [("fa", {}), ("vfa", {}), ("vsa", dict(lam=1e-2)), ("blasst", di
 @pytest.mark.parametrize("variant,extra", PAIR_VARIANTS, ids=[v for v, _ in PAIR_VARIANTS])
 @pytest.mark.parametrize("bc", [64, 128])
 @pytest.mark.parametrize("causal", [True, False])
-def test_cta_pair_against_oracle(variant, extra, bc, causal):
-    # cta_group::2 path: the unit's two query heads on a CTA pair, K/V tiles split between the
-    # two SMs' shared memory and consumed by M = 256 MMAs issued by the leader CTA. Planted
-    # sink so that the skipping variants skip / elide / mask.
-    B, Hq, Hkv, L, d = 1, 4, 2, 640, 128
+@pytest.mark.parametrize("hq", [4, 8])
+def test_cta_pair_against_oracle(variant, extra, bc, causal, hq):
+    # cta_group::2 path: K/V tiles split between the two SMs' shared memory and consumed by
+    # M = 256 MMAs issued by the leader CTA; GQA group 2: one query tile per CTA, group 4: two
+    # per CTA (four heads per cluster). Planted sink so the skipping variants skip / elide / mask.
+    B, Hq, Hkv, L, d = 1, hq, 2, 640, 128
     q, k, v = _rand((B, Hq, L, d), 211), _rand((B, Hkv, L, d), 212), _rand((B, Hkv, L, d), 213)
     if variant not in ("fa", "vfa"):
         amp = float(np.sqrt(8.0 * np.sqrt(d)))
@@ -643,7 +644,7 @@ def test_cta_pair_against_oracle(variant, extra, bc, causal):
     o_ref, l_ref = np.empty(out.shape), np.empty(lse.shape)
     visited = 0
     for h in range(Hq):
-        r = vo.forward_head(qf[0, h], kf[0, h // 2], vf[0, h // 2], **okw)
+        r = vo.forward_head(qf[0, h], kf[0, h // (Hq // Hkv)], vf[0, h // (Hq // Hkv)], **okw)
         o_ref[0, h], l_ref[0, h] = r.out, r.lse
         visited += r.visited
     _compare(out, lse, o_ref, l_ref, f"{kw} pair")
