@@ -21,9 +21,9 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("cudaFuncGetAttributes: ") + cudaGetErrorString(e));
-    if (vfa::kRegBudget > fa.numRegs * vfa::kThreads)
-      return vfa_host::fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(vfa::kRegBudget) + " exceeds the launch allocation " +
-                                    std::to_string(fa.numRegs * vfa::kThreads) + " (would deadlock)");
+    if (C::kRegBudget > fa.numRegs * C::kThreads)
+      return vfa_host::fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(C::kRegBudget) + " exceeds the launch allocation " +
+                                    std::to_string(fa.numRegs * C::kThreads) + " (would deadlock)");
     attr_set = true;
   }
   const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
@@ -33,7 +33,7 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
     // one cluster of two CTAs per unit (the unit's two query heads, one per CTA)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
-    cfg.blockDim = dim3(vfa::kThreads);
+    cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -46,7 +46,7 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
     e = cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, mr, args);
     if (e == cudaSuccess) e = cudaGetLastError();
   } else {
-    kern<<<static_cast<unsigned>(units), vfa::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
+    kern<<<static_cast<unsigned>(units), C::kThreads, C::kSmem, stream>>>(mq, mk, mv, mr, args);
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -65,6 +65,7 @@ template <int D, int BC, int NQ, int MODE>
 int dispatch_split(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                    const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
   const int split = p->softmax_split ? p->softmax_split : default_split(MODE);
+  if (split == 1) return launch_fwd<D, BC, NQ, MODE, 1>(p, mq, mk, mv, mr, args, st);
   if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
   return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
 }

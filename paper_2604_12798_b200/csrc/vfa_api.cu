@@ -153,8 +153,8 @@ int vfa_check_params(const VfaParams* p) {
   if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
   if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
   if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
-  if (p->softmax_split != 0 && p->softmax_split != 2 && p->softmax_split != 4)
-    return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 2 or 4");
+  if (p->softmax_split != 0 && p->softmax_split != 1 && p->softmax_split != 2 && p->softmax_split != 4)
+    return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 1, 2 or 4");
   if (p->cta_pair < 0 || p->cta_pair > 2) return fail(VFA_ERR_CONFIG, "cta_pair must be 0 (auto), 1 (off) or 2 (on)");
   if (p->variant >= VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
   if (!(p->tau >= 0.0)) return fail(VFA_ERR_CONFIG, "tau must be >= 0");  // src/sparse.py:52-53 (NaN rejected)

@@ -48,20 +48,14 @@
 namespace vfa {
 
 constexpr int kBR = 128;          // query rows per tile (tcgen05 M)
-// warps 0-15: four softmax warpgroups (2 query tiles x 2 column halves); warp 16: MMA
-// issuer (both query tiles, strictly alternating) + TMEM allocator; warp 17: TMA producer;
-// warps 18-19 complete the last warpgroup. (One issuer per tile was measured slower: the
-// tiles drift into phase and contend for the softmax issue slots.)
-constexpr int kSoftmaxWarps = 16;
-constexpr int kMmaWarp = 16;
-constexpr int kLoadWarp = 17;
-constexpr int kThreads = 640;
-// setmaxnreg budgets. The CTA's register pool is what the launch allocated
-// (threads x compiled registers/thread, 640 x 96 = 61440); asking for more than the pool
-// blocks setmaxnreg.inc forever, so the host checks this budget before launching.
-constexpr int kRegsSoftmax = 104;
-constexpr int kRegsOther = 56;
-constexpr int kRegBudget = kSoftmaxWarps * 32 * kRegsSoftmax + (kThreads - kSoftmaxWarps * 32) * kRegsOther;
+// Warp layout (Cfg::kSoftmaxWarps ...): SPLIT 2 / 4: warps 0-15 are four softmax warpgroups
+// (2 or 4 threads per row); SPLIT 1: one softmax warpgroup per query tile (one thread per row).
+// Then the MMA issuer (all query tiles, strictly alternating) + TMEM allocator, the TMA
+// producer, and two warps completing the last warpgroup. (One issuer per tile was measured
+// slower: the tiles drift into phase and contend for the softmax issue slots.)
+#ifndef VFA_REGS_SPLIT1
+#define VFA_REGS_SPLIT1 216
+#endif
 constexpr int kMaxSmem = 227 * 1024;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -142,6 +136,16 @@ struct Cfg {
   static constexpr int kNCH = kCP >= 32 ? 2 : 1;     // P hand-off chunks per block
   static constexpr int kCW = kCP / kNCH;             // columns per P chunk (16 or 32)
   static constexpr int kWarpsPerTile = SPLIT * 4;    // softmax warps covering one tile
+  static constexpr int kSoftmaxWarps = SPLIT == 1 ? 4 * NQ : 16;
+  static constexpr int kMmaWarp = kSoftmaxWarps;
+  static constexpr int kLoadWarp = kSoftmaxWarps + 1;
+  static constexpr int kThreads = (kSoftmaxWarps + 4) * 32;
+  // setmaxnreg budgets. The CTA's register pool is what the launch allocated (threads x
+  // compiled registers/thread, e.g. 640 x 96 = 61440); asking for more than the pool blocks
+  // setmaxnreg.inc forever, so the host checks this budget before launching.
+  static constexpr int kRegsSoftmax = SPLIT == 1 ? VFA_REGS_SPLIT1 : 104;
+  static constexpr int kRegsOther = 56;
+  static constexpr int kRegBudget = kSoftmaxWarps * 32 * kRegsSoftmax + (kThreads - kSoftmaxWarps * 32) * kRegsOther;
   static constexpr int kCtlBytes = 16384;
   static constexpr int kAvail = kMaxSmem - 1024 - kCtlBytes - NQ * kQBytes;
   static constexpr int kStagesRaw = kAvail / kKVBytes;
@@ -171,7 +175,8 @@ struct Cfg {
   static_assert(kColsUsed <= 512, "TMEM over-subscribed");
   static_assert(kStages >= 3, "not enough shared memory for a K/V ring");
   static_assert(kCW % 16 == 0 && kOP % 16 == 0, "parts must be whole 16-column chunks");
-  static_assert(SPLIT == 2 || SPLIT == 4, "SPLIT is 2 (per-tile warp sets) or 4 (all warps, both tiles)");
+  static_assert(SPLIT == 1 || SPLIT == 2 || SPLIT == 4,
+                "SPLIT is 1 (a warpgroup per tile, a thread per row), 2 (per-tile warp sets) or 4 (all warps, both tiles)");
 };
 
 template <int NS, int NQ, int SB>
@@ -337,7 +342,7 @@ __device__ __forceinline__ void p_chunk(const float* v, float2 cs2, float2 nmu2,
 
 // ------------------------------------------------------------------------------------
 template <int D, int BC, int NQ, int MODE, int SPLIT, int PAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1)
     vfa_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
@@ -384,13 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == kLoadWarp && lane == 0) {
+  if (warp == C::kLoadWarp && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmR);
   }
-  if (warp == kMmaWarp) {
+  if (warp == C::kMmaWarp) {
     if constexpr (PAIR == 2)
       tmem_alloc_pair<C::kTmemCols>(&ctl->tmem_base);
     else
@@ -435,9 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G = nchunks + N;                                                   \
   (void)tbase; (void)nrep; (void)nchunks; (void)N; (void)G
 
-  if (warp >= kSoftmaxWarps) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
-    if (warp == kLoadWarp) {
+  if (warp >= C::kSoftmaxWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kRegsOther));
+    if (warp == C::kLoadWarp) {
       // ============================ TMA producer ============================
       if (lane == 0) {
         VFA_ROLE_SETUP();
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g + SB < G) load_s_operand(g + SB);
         }
       }
-    } else if (warp == kMmaWarp && (PAIR == 1 || crank == 0)) {
+    } else if (warp == C::kMmaWarp && (PAIR == 1 || crank == 0)) {
       // ============================ MMA issuer ============================
       // (a CTA pair's MMAs are all issued by the leader, M = 256 over both CTAs' tiles)
       // The whole warp runs the issue loop (warp-uniform state in uniform registers); one
@@ -670,10 +675,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     //               that run in anti-phase, each hiding under the other tile's MMA window);
     //   SPLIT == 4: all four warpgroups serve both tiles in turn (tile 0 then tile 1 of each
     //               key block): half the per-thread work per tile-block, one shared issue stream.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kRegsSoftmax));
     constexpr int NT = (SPLIT == 4) ? NQ : 1;  // query tiles this thread serves
-    const int part = (SPLIT == 4) ? (warp >> 2) : ((warp >> 2) & 1);
-    const int tile0 = (SPLIT == 4) ? 0 : (warp >> 3);
+    const int part = SPLIT == 4 ? (warp >> 2) : (SPLIT == 2 ? ((warp >> 2) & 1) : 0);
+    const int tile0 = SPLIT == 4 ? 0 : warp / (4 * SPLIT);
     if (tile0 < NQ) {
       const int r = tid & 127;
       VFA_ROLE_SETUP();
@@ -702,6 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto tO = [&](int t) { return tbase + C::kOBase + t * D + part * OP + lane_off; };
       // row-max exchange across the SPLIT parts of a row (named barrier 1 + t)
       auto exchange_max = [&](int ti, int t, float mine) -> float {
+        if constexpr (SPLIT == 1) return mine;  // one thread holds the whole row
         ctl->xmax[t][xpar[ti]][part][r] = mine;
         named_bar_sync(1 + t, SPLIT * kBR);
         const float* x = ctl->xmax[t][xpar[ti]][0];
@@ -893,7 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p_chunk<CW, true, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
               else
                 p_chunk<CW, false, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
-              if constexpr (CW == 32) tmem_st16(tS(t, b) + c * 16, u);
+              if constexpr (CW == 64) tmem_st32(tS(t, b) + c * 32, u);
+              else if constexpr (CW == 32) tmem_st16(tS(t, b) + c * 16, u);
               else tmem_st8(tS(t, b) + c * 8, u);
               if (!defer) {
                 tmem_wait_st();
@@ -943,10 +950,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ti = 0; ti < NT; ++ti) {
         const int t = tile0 + ti;
         const int h = head_of(unit, t);
-        ctl->xl[t][part][r] = l[ti];
-        named_bar_sync(1 + t, SPLIT * kBR);
-        float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
-        if constexpr (SPLIT == 4) lsum = __fadd_rn(lsum, __fadd_rn(ctl->xl[t][2][r], ctl->xl[t][3][r]));
+        float lsum = l[ti];
+        if constexpr (SPLIT > 1) {
+          ctl->xl[t][part][r] = l[ti];
+          named_bar_sync(1 + t, SPLIT * kBR);
+          lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
+          if constexpr (SPLIT == 4) lsum = __fadd_rn(lsum, __fadd_rn(ctl->xl[t][2][r], ctl->xl[t][3][r]));
+        }
         mbar_wait(&ctl->o_final[t], 0);
         tc_fence_after();
         const float inv = 1.0f / lsum;
@@ -988,10 +998,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           // a row is non-finite if any part is: combine through smem, count it once
-          ctl->xfin[t][part][r] = finite ? 1 : 0;
-          named_bar_sync(1 + t, SPLIT * kBR);
-          bool row_ok = ctl->xfin[t][0][r] && ctl->xfin[t][1][r];
-          if constexpr (SPLIT == 4) row_ok = row_ok && ctl->xfin[t][2][r] && ctl->xfin[t][3][r];
+          bool row_ok = finite;
+          if constexpr (SPLIT > 1) {
+            ctl->xfin[t][part][r] = finite ? 1 : 0;
+            named_bar_sync(1 + t, SPLIT * kBR);
+            row_ok = ctl->xfin[t][0][r] && ctl->xfin[t][1][r];
+            if constexpr (SPLIT == 4) row_ok = row_ok && ctl->xfin[t][2][r] && ctl->xfin[t][3][r];
+          }
           if (part == 0 && !row_ok) any_nonfinite = true, atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
         }
       }
@@ -1021,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if constexpr (PAIR == 2) cluster_sync_all();  // the peer may still be reading our smem / TMEM
   if (tid == 0) VFA_TRACE_UNIT(a, 3);
-  if (warp == kMmaWarp) {
+  if (warp == C::kMmaWarp) {
     tc_fence_after();
     if constexpr (PAIR == 2)
       tmem_dealloc_pair<C::kTmemCols>(ctl->tmem_base);
