@@ -397,9 +397,10 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     stab_trace: also return info["stab_block"], int32 [B, Hq, Lq]: per row the key block after
     whose visit the running max held its final value (the StateTrace stabilization position,
     src/analysis.py:39-78), see DeviceTrace / stabilization_positions.
-    cta_pair: 0 (default), 1 (one CTA per unit) or 2 (the unit's two query heads on a CTA pair
-    sharing each K/V tile through M = 256 tcgen05 MMAs; even GQA groups, d = 128).
-    softmax_split: 0 (per-variant default), 2 or 4 threads per row of a query tile (a layout
+    cta_pair: 0 (default: off), 1 (one CTA per unit) or 2 (CTA pairs sharing each K/V tile
+    through M = 256 tcgen05 MMAs: two query tiles per CTA for GQA groups divisible by 4, one for
+    other even groups; d = 128, q_block = 128; falls back to single CTAs elsewhere).
+    softmax_split: 0 (per-variant default), 1, 2 or 4 threads per row of a query tile (a layout
     choice: results are within tolerance of each other, bitwise-stable for a fixed split).
     """
     if variant not in _lib.VARIANTS:
