@@ -746,3 +746,23 @@ def test_small_query_blocks_geometries(variant, hq, hkv, b, qb, bc):
     assert st["visited"] == ref_st["visited"]
     if variant != "vsa":
         assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa", "blasst_rowskip"])
+@pytest.mark.parametrize("lq,lk,qb,bc,causal", [(192, 192, 64, 64, True), (320, 320, 32, 64, True),
+                                                (96, 256, 32, 128, False), (64, 64, 16, 64, True)])
+def test_small_query_blocks_ragged_lengths(variant, lq, lk, qb, bc, causal):
+    # lengths that are not multiples of the 128-row tile: the last tile's idle rows read past
+    # the sequence (TMA zero fill) and are never stored
+    d = 64
+    q, k, v = _rand((1, 2, lq, d), 271), _rand((1, 1, lk, d), 272), _rand((1, 1, lk, d), 273)
+    kw = dict(variant=variant, causal=causal, q_block=qb, k_block=bc)
+    if variant in ("vsa", "blasst_rowskip"):
+        kw["lam"] = 1e-2
+    if variant.startswith("blasst"):
+        kw["reorder"] = False
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    okw = {key: val for key, val in kw.items() if key != "reorder"}
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **okw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    assert st["visited"] == ref_st["visited"]
