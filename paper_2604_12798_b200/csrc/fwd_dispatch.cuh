@@ -75,6 +75,14 @@ int launch_mode(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtenso
                 const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
   const int D = static_cast<int>(p->head_dim), BC = p->k_block;
   if (a.pair == 2) {  // CTA pairs (d = 128): K/V shared by M = 256 MMAs; 2 or 1 query tiles per CTA
+    if (p->softmax_split == 1) {  // one thread per row
+      if (a.heads_per_unit == 4) {
+        if (BC == 128) return launch_fwd<128, 128, 2, MODE, 1, 2>(p, mq, mk, mv, mr, a, st);
+        return launch_fwd<128, 64, 2, MODE, 1, 2>(p, mq, mk, mv, mr, a, st);
+      }
+      if (BC == 128) return launch_fwd<128, 128, 1, MODE, 1, 2>(p, mq, mk, mv, mr, a, st);
+      return launch_fwd<128, 64, 1, MODE, 1, 2>(p, mq, mk, mv, mr, a, st);
+    }
     if (a.heads_per_unit == 4) {
       if (BC == 128) return launch_fwd<128, 128, 2, MODE, 4, 2>(p, mq, mk, mv, mr, a, st);
       return launch_fwd<128, 64, 2, MODE, 4, 2>(p, mq, mk, mv, mr, a, st);

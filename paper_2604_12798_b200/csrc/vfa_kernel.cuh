@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
                    const FwdArgs a) {
   using C = Cfg<D, BC, NQ, SPLIT, MODE, PAIR>;
-  static_assert(PAIR == 1 || (SPLIT == 4 && D == 128), "CTA pairs: d = 128, all softmax warps on every tile");
+  static_assert(PAIR == 1 || ((SPLIT == 4 || SPLIT == 1) && D == 128), "CTA pairs: d = 128, split 4 or 1");
   constexpr int NS = C::kStages;
   constexpr int CP = C::kCP;
   constexpr int OP = C::kOP;

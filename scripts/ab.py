@@ -23,6 +23,7 @@ ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--k-block", type=int, default=128)
 ap.add_argument("--head-dim", type=int, default=128)
 ap.add_argument("--pair", action="store_true", help="also time every build with cta_pair=2")
+ap.add_argument("--split", type=int, default=0, help="softmax_split for every runner (0: per-variant default)")
 a = ap.parse_args()
 cfg = dict(CONFIGS["c2"], d=a.head_dim)
 dev = torch.device("cuda", 0)
@@ -35,6 +36,7 @@ for spec in a.libs:
     for pair in ((1, 2) if a.pair else (0,)):
         runners[name + ("" if pair == 0 else f"/pair{pair}")] = Runner(
             q, k, v, a.variant, lam=1e-2 if a.variant == "vsa" else None, k_block=a.k_block, lib=lib, cta_pair=pair)
+        runners[name + ("" if pair == 0 else f"/pair{pair}")].p.softmax_split = a.split
 sh = torch.cuda.current_stream().cuda_stream
 for r in runners.values():
     for _ in range(3):

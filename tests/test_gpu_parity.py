@@ -766,3 +766,21 @@ def test_small_query_blocks_ragged_lengths(variant, lq, lk, qb, bc, causal):
     ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **okw)
     _compare(out, lse, ref_o, ref_lse, str(kw))
     assert st["visited"] == ref_st["visited"]
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa"])
+@pytest.mark.parametrize("hq", [4, 8])
+def test_cta_pair_one_thread_per_row(variant, hq):
+    # CTA pairs with the one-thread-per-row softmax layout (softmax_split = 1)
+    B, Hkv, L, d = 1, 2, 512, 128
+    q, k, v = _rand((B, hq, L, d), 281), _rand((B, Hkv, L, d), 282), _rand((B, Hkv, L, d), 283)
+    kw = dict(variant=variant, causal=True, q_block=128, k_block=128)
+    if variant == "vsa":
+        kw["lam"] = 1e-2
+    out, lse, _, st = _run_gpu(q, k, v, cta_pair=2, softmax_split=1, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, f"{kw} pair split 1")
+    assert st["visited"] == ref_st["visited"]
+    out1, _, _, _ = _run_gpu(q, k, v, cta_pair=1, softmax_split=1, **kw)
+    if variant == "vfa":
+        assert torch.equal(out, out1)
