@@ -83,7 +83,7 @@ struct FwdArgs {
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
   const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
-  int pair;            // host: 2 = launched as CTA pairs (one query tile per CTA), else 1
+  int pair;            // host: 2 = launched as CTA pairs (clusters of two CTAs), else 1
   long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
@@ -122,9 +122,9 @@ constexpr int kTraceSlots = 16;
 #endif
 
 // PAIR == 2: a CTA pair (cluster of 2) shares every K/V tile through M = 256 tcgen05 MMAs
-// (cta_group::2): each CTA holds ONE query tile (NQ == 1 locally), half of each K tile's rows
-// and half of each V tile's columns, so a K/V stage is half as large and S can be double
-// buffered in TMEM.
+// (cta_group::2) over the same local tile index of both CTAs: each CTA holds NQ query tiles
+// (its own heads), half of each K tile's rows and half of each V tile's columns, so a K/V stage
+// is half as large.
 template <int D, int BC, int NQ, int SPLIT, int MODE, int PAIR = 1>
 struct Cfg {
   static constexpr int kQBytes = kBR * D * 2;
@@ -674,7 +674,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
     //   SPLIT == 2: warpgroups 2t, 2t+1 serve query tile t only (two independent warp sets
     //               that run in anti-phase, each hiding under the other tile's MMA window);
     //   SPLIT == 4: all four warpgroups serve both tiles in turn (tile 0 then tile 1 of each
-    //               key block): half the per-thread work per tile-block, one shared issue stream.
+    //               key block): half the per-thread work per tile-block, one shared issue stream;
+    //   SPLIT == 1: one warpgroup per tile, one thread per row (no row-max exchange).
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kRegsSoftmax));
     constexpr int NT = (SPLIT == 4) ? NQ : 1;  // query tiles this thread serves
     const int part = SPLIT == 4 ? (warp >> 2) : (SPLIT == 2 ? ((warp >> 2) & 1) : 0);
