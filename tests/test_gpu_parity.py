@@ -784,3 +784,17 @@ def test_cta_pair_one_thread_per_row(variant, hq):
     out1, _, _, _ = _run_gpu(q, k, v, cta_pair=1, softmax_split=1, **kw)
     if variant == "vfa":
         assert torch.equal(out, out1)
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa"])
+def test_large_shape_against_torch_sdpa(variant):
+    # full-size GQA problem (L = 8192, 32 query / 8 KV heads, batch 2): the device output against
+    # torch's fused attention on the same bf16 inputs (an independent fp32-accumulating kernel)
+    import torch.nn.functional as F
+    B, Hq, Hkv, L, d = 2, 32, 8, 8192, 128
+    q, k, v = _rand((B, Hq, L, d), 291), _rand((B, Hkv, L, d), 292), _rand((B, Hkv, L, d), 293)
+    out, lse, _, st = _run_gpu(q, k, v, variant=variant, causal=True)
+    ref = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+    err = (out.float() - ref.float()).abs().max().item()
+    assert err <= O_ABS, err
+    assert st["visited"] == B * Hq * sum(range(1, L // 128 + 1))
