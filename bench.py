@@ -8,7 +8,13 @@ block, sabsmax key representations. A step is one full forward over that problem
 additionally flushed between timed steps (outside the timed intervals).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c4] [--sweep c3|c5]
+                  [--config c2|c4] [--no-sweeps] [--no-cpu] [--no-e2e]
+
+The line also carries (rank 0, N = 1): `parity` (the GPU's O / LSE on the CPU sample's query
+blocks against the float64 oracle; exit code 3 on a breach), `c3_vsa_lambda_sweep` (BASELINE
+configs[2]: planted-sink VSA at the C2 shape, skipped fraction and error vs the oracle / VFA),
+`c5_ablation` (configs[4]: VFA / FA at Bc x d in {64,128}^2) and `calibration` (cuDNN's and
+FlashAttention-4's plain online-softmax attention on the same problem, interleaved with VFA).
 
 Multi-GPU (torchrun, one process per GPU): the KV heads are split into N
 contiguous groups (with their GQA query heads); no collective runs in the timed
@@ -132,9 +138,11 @@ def _cpu_task(args):
     from oracle import vfa_oracle as vo
     q, k, v = _CPU["q"][h], _CPU["k"][h], _CPU["v"][h]
     t0 = time.perf_counter()
-    vo.forward_head(q, k, v, variant=variant, causal=True, q_block=qb, k_block=kb, q_blocks=[i],
-                    lam=1e-2 if variant == "vsa" else None)
-    return time.perf_counter() - t0
+    r = vo.forward_head(q, k, v, variant=variant, causal=True, q_block=qb, k_block=kb, q_blocks=[i],
+                        lam=1e-2 if variant == "vsa" else None, raise_errors=False)
+    dt = time.perf_counter() - t0
+    rows = slice((i - 1) * qb, i * qb)
+    return dt, h, i, r.out[rows].astype(np.float32), r.lse[rows]
 
 
 def cpu_sample_plan(L, heads, qb, budget_units):
@@ -158,8 +166,9 @@ def sample_flops(plan, qb, d):
     return 4.0 * d * tot
 
 
-def run_cpu_sample(q, k, v, plan, qb, kb, variant, cores):
-    """Time the oracle on `plan` with `cores` fork-workers (one BLAS thread each)."""
+def run_cpu_sample(q, k, v, plan, qb, kb, variant, cores, keep_outputs=False):
+    """Time the oracle on `plan` with `cores` fork-workers (one BLAS thread each); with
+    keep_outputs also return [(head, block, O rows, LSE rows)] for the parity check."""
     heads = sorted({h for h, _ in plan})
     _CPU["q"] = {h: q[h] for h in heads}
     _CPU["k"] = {h: k[h] for h in heads}
@@ -168,8 +177,11 @@ def run_cpu_sample(q, k, v, plan, qb, kb, variant, cores):
     tasks = [(h, i, qb, kb, variant) for h, i in sorted(plan, key=lambda x: -x[1])]
     with ctx.Pool(cores) as pool:
         t0 = time.perf_counter()
-        busy = sum(pool.map(_cpu_task, tasks, chunksize=1))
+        res = pool.map(_cpu_task, tasks, chunksize=1)
         wall = time.perf_counter() - t0
+    busy = sum(x[0] for x in res)
+    if keep_outputs:
+        return wall, busy, [x[1:] for x in res]
     return wall, busy
 
 
@@ -328,8 +340,10 @@ def main_ours(args):
 
     cfg = CONFIGS[args.config]
     B, Hq, Hkv, L, d = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["L"], cfg["d"]
-    from paper_2604_12798_b200.sharding import gather_heads, kv_head_shard, shard_inputs
-    shard = kv_head_shard(rank, world, Hq, Hkv)
+    from paper_2604_12798_b200.sharding import gather_units, shard_inputs, unit_major, unit_shard
+    # (batch, KV head) units, contiguous per rank; the C2 / C4 configs have B = 1, so a rank's
+    # range is one block of KV heads with their GQA query heads
+    shard = unit_shard(rank, world, B, Hq, Hkv)
     q_full, k_full, v_full = make_inputs(cfg, dev)
     q, k, v = shard_inputs(q_full, k_full, v_full, shard)
     if world > 1 and rank != 0:  # rank 0 keeps the full problem for the post-timing verification
@@ -368,13 +382,15 @@ def main_ours(args):
             res[name]["lam"] = args.lam
             res[name]["skipped_fraction"] = st["skipped"] / max(st["visited"], 1)
     status = runners["vfa"].status.cpu().numpy().view(np.uint32)
+    launches = args.steps * sum(r.launches_per_step for r in runners.values())
 
     # ---- verification (outside the timed region): gather O / LSE shards, compare to 1 GPU
     verified = None
     if world > 1:
         r = runners["vfa"]
-        o_all = gather_heads(r.o, world)  # NCCL all_gather over NVLink, verification only
-        l_all = gather_heads(r.lse, world)
+        # NCCL all_gather over NVLink, verification only
+        o_all = gather_units(unit_major(r.o, shard.units), shard, world).reshape(B, Hq, L, d)
+        l_all = gather_units(unit_major(r.lse, shard.units), shard, world).reshape(B, Hq, L)
         if rank == 0:
             full = Runner(q_full, k_full, v_full, "vfa", **tile)
             sh = torch.cuda.current_stream().cuda_stream
@@ -406,9 +422,19 @@ def main_ours(args):
         h2d, d2h = (int(x) for x in hb.tolist())
 
     # ---- CPU baseline (rank 0, N = 1 only)
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, args.cpu_core_seconds, "vfa")
+        cpu, parity = cpu_baseline(cfg, args.cpu_core_seconds, "vfa", runners["vfa"].o, runners["vfa"].lse)
+
+    # ---- C3 (VSA lambda sweep) and C5 (Bc x d ablation) at reduced step counts, and the
+    #      vendor calibration (rank 0, N = 1): extra keys, outside the headline timing
+    c3 = c5 = vendor = None
+    if rank == 0 and world == 1 and not args.no_sweeps:
+        del runners["fa"], runners["vsa"]
+        torch.cuda.empty_cache()
+        vendor = vendor_calibration(q, k, v, runners["vfa"], flush, flops_total, args.sweep_steps)
+        c3 = c3_sweep(cfg, dev, flush, args.sweep_steps)
+        c5 = c5_ablation(cfg, dev, flush, args.sweep_steps)
 
     if rank == 0:
         peak, peak_sus, peak_kind = load_peaks()
@@ -430,7 +456,7 @@ def main_ours(args):
             "config": {"workload": cfg["workload"], "batch": B, "heads_q": Hq, "heads_kv": Hkv,
                        "seq_len": L, "head_dim": d, "q_block": 128, "k_block": args.k_block, "causal": True,
                        "variant": "vfa", "key_repr": "sabsmax", "n_sink": args.n_sink, "n_local": args.n_local,
-                       "parallelism": f"kv-head sharding x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"(batch, kv-head) unit sharding x{world}" if world > 1 else "single GPU",
                        "flops_per_step": flops_total,
                        "l2": f"inputs {(B * Hq * L * d + 2 * B * Hkv * L * d) * 2 / 2**20:.0f} MiB, and L2 flushed "
                              "(256 MiB write) between timed steps",
@@ -444,7 +470,7 @@ def main_ours(args):
             "ablation": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
                          for k2, v2 in res.items()},
             "clocks": clocks.summary(),
-            "gpu_launches": args.steps * sum(r.launches_per_step for r in runners.values()),
+            "gpu_launches": launches,
             "status_flags": int(status[0]),
         }
         if "fa" in res:
@@ -459,26 +485,214 @@ def main_ours(args):
                            "chunk_kv_heads": args.e2e_chunk, "chunk_q_heads": args.e2e_qchunk}
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if parity is not None:
+            line["parity"] = parity
+        if vendor is not None:
+            line["calibration"] = vendor
+        if c3 is not None:
+            line["c3_vsa_lambda_sweep"] = c3
+        if c5 is not None:
+            line["c5_ablation"] = c5
         print(json.dumps(line), flush=True)
+        if parity is not None and not parity["ok"]:
+            print(f"PARITY BREACH against the oracle: {parity}", file=sys.stderr, flush=True)
+            sys.exit(3)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def cpu_baseline(cfg, core_seconds, variant):
+# ----------------------------------------------------------------------------- extra keys
+def planted_sink(q, k, boost, bc):
+    """C3 data: the coordinate-0 trick of src/tensor.py:153-175 applied to key
+    block 1, which scales to any L: q[:, 0] = amp, k[:, 0] = 0, k[:bc, 0] = amp."""
+    d = q.shape[-1]
+    amp = float(np.sqrt(boost * np.sqrt(d)))
+    q[..., 0] = amp
+    k[..., 0] = 0
+    k[:, :, :bc, 0] = amp
+
+
+def c3_sweep(cfg, dev, flush, steps, lams=(1e-4, 1e-3, 3e-3, 1e-2, 3e-2, 1e-1), blocks=(1, 128, 256)):
+    """BASELINE configs[2]: VSA on planted-sink data of the C2 shape over a lambda sweep,
+    interleaved with VFA on the same data: effective TFLOP/s (dense-equivalent FLOPs / kernel
+    time), skipped fraction on the GPU and, on sampled query blocks of head 0, in the float64
+    oracle, the error against the oracle and against VFA."""
+    import torch
+
+    from oracle import vfa_oracle as vo
+    q, k, v = make_inputs(cfg, dev, seed=4321)
+    planted_sink(q, k, 8.0, 128)
+    flops = causal_flops(cfg["B"], cfg["Hq"], cfg["L"], cfg["d"])
+    runners = {"vfa": Runner(q, k, v, "vfa")}
+    for lam in lams:
+        runners[f"vsa_{lam:g}"] = Runner(q, k, v, "vsa", lam=lam)
+    sh = torch.cuda.current_stream().cuda_stream
+    for r in runners.values():
+        for _ in range(2):
+            r.krepr(sh)
+            r.attn(sh)
+    torch.cuda.synchronize()
+    timed = time_interleaved(runners, steps, flush, lambda: None)
+    q0 = q[0, 0].double().cpu().numpy()
+    k0, v0 = k[0, 0].double().cpu().numpy(), v[0, 0].double().cpu().numpy()
+    rows = np.concatenate([np.arange((i - 1) * 128, i * 128) for i in blocks])
+    ref_vfa = runners["vfa"].o.float()
+    out = {"data": "planted sink (boost 8) on the C2 shape, seed 4321", "steps": steps,
+           "vfa_tflops": round(flops / timed["vfa"][1] / 1e9, 1), "oracle_blocks_head0": list(blocks), "lambdas": []}
+    for lam in lams:
+        r = runners[f"vsa_{lam:g}"]
+        st = r.stats_dict()
+        ref = vo.forward_head(q0, k0, v0, variant="vsa", causal=True, q_block=128, k_block=128, lam=lam,
+                              q_blocks=list(blocks), raise_errors=False)
+        got = r.o[0, 0].double().cpu().numpy()[rows]
+        # the GPU's skip decisions on the same sampled blocks (per-visit skip trace, one extra call)
+        from paper_2604_12798_b200 import attention_forward
+        _, _, info = attention_forward(q, k, v, variant="vsa", causal=True, lam=lam, check=False, skip_trace=True)
+        tr = info["skip_trace"][0, 0, [i - 1 for i in blocks]].cpu().numpy()
+        out["lambdas"].append({
+            "skipped_in_sample_gpu": int((tr == 2).sum()), "skipped_in_sample_oracle": int(ref.skipped),
+            "visited_in_sample": int(ref.visited),
+            "lam": lam, "effective_tflops": round(flops / timed[f"vsa_{lam:g}"][1] / 1e9, 1),
+            "attn_kernel_ms": round(timed[f"vsa_{lam:g}"][1], 4),
+            "skipped_fraction_gpu": round(st["skipped"] / max(st["visited"], 1), 4),
+            "skipped_fraction_oracle_sample": round(ref.skipped / max(ref.visited, 1), 4),
+            "o_max_abs_vs_oracle": float(np.abs(got - ref.out[rows]).max()),
+            "o_max_rel_err_vs_oracle": vo.max_rel_err(got, ref.out[rows]),
+            "o_max_abs_vs_vfa": float((r.o.float() - ref_vfa).abs().max())})
+    del runners, q, k, v
+    torch.cuda.empty_cache()
+    return out
+
+
+def c5_ablation(cfg, dev, flush, steps):
+    """BASELINE configs[4]: FA vs VFA at Bc in {64, 128} x d in {64, 128} on the C2 shape
+    (n_local = 2 at Bc = 64 so the local band covers the 128-row diagonal tile)."""
+    import torch
+    res = []
+    for d in (64, 128):
+        c = dict(cfg, d=d)
+        q, k, v = make_inputs(c, dev)
+        flops = causal_flops(c["B"], c["Hq"], c["L"], d)
+        for bc in (64, 128):
+            nl = 2 if bc == 64 else 1
+            runners = {"fa": Runner(q, k, v, "fa", k_block=bc, n_local=nl),
+                       "vfa": Runner(q, k, v, "vfa", k_block=bc, n_local=nl)}
+            sh = torch.cuda.current_stream().cuda_stream
+            for r in runners.values():
+                for _ in range(2):
+                    r.krepr(sh)
+                    r.attn(sh)
+            torch.cuda.synchronize()
+            timed = time_interleaved(runners, steps, flush, lambda: None)
+            res.append({"head_dim": d, "k_block": bc, "n_local": nl,
+                        "fa_tflops": round(flops / timed["fa"][1] / 1e9, 1),
+                        "vfa_tflops": round(flops / timed["vfa"][1] / 1e9, 1),
+                        "vfa_speedup_vs_fa": round(timed["fa"][1] / timed["vfa"][1], 4)})
+            del runners
+        del q, k, v
+        torch.cuda.empty_cache()
+    return res
+
+
+class _VendorRunner:
+    """A vendor attention kernel on the same problem (calibration only, never the product)."""
+
+    def __init__(self, kind, q, k, v):
+        import torch
+        self.kind = kind
+        rep = q.shape[1] // k.shape[1]
+        if kind == "cudnn":  # torch SDPA's cuDNN backend; K/V expanded to the query heads
+            self.q, self.k, self.v = q, k.repeat_interleave(rep, dim=1), v.repeat_interleave(rep, dim=1)
+        else:  # FlashAttention-4 (CuTe DSL, shipped in vllm): native GQA on [B, L, H, d]
+            from vllm.vllm_flash_attn.cute import flash_attn_func
+            self.f = flash_attn_func
+            self.q, self.k, self.v = (x.transpose(1, 2).contiguous() for x in (q, k, v))
+        self.torch = torch
+
+    def krepr(self, stream):
+        pass
+
+    def attn(self, stream):
+        if self.kind == "cudnn":
+            import torch.nn.functional as F
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                self.o = F.scaled_dot_product_attention(self.q, self.k, self.v, is_causal=True)
+        else:
+            out = self.f(self.q, self.k, self.v, causal=True)
+            self.o = (out[0] if isinstance(out, tuple) else out).transpose(1, 2)
+
+
+def vendor_calibration(q, k, v, vfa_runner, flush, flops, steps):
+    """cuDNN and FlashAttention-4 forward (plain online softmax) on the C2 problem, timed
+    interleaved with this repo's VFA kernel (same inputs, same L2 flush, same power state)."""
+    import torch
+    runners = {"vfa": vfa_runner}
+    out = {"note": "vendor kernels: calibration only (not the product, not in value / e2e)"}
+    for kind in ("cudnn", "fa4"):
+        try:
+            r = _VendorRunner(kind, q, k, v)
+            sh = torch.cuda.current_stream().cuda_stream
+            for _ in range(2):
+                r.attn(sh)
+            torch.cuda.synchronize()
+            runners[kind] = r
+        except Exception as e:  # noqa: BLE001 - calibration is best-effort
+            out[f"{kind}_error"] = f"{type(e).__name__}: {str(e)[:160]}"
+    timed = time_interleaved(runners, steps, flush, lambda: None)
+    for name in runners:
+        out[f"{name}_tflops"] = round(flops / timed[name][1] / 1e9, 1)
+    for kind in ("cudnn", "fa4"):
+        if kind in runners:
+            out[f"vfa_over_{kind}"] = round(timed[kind][1] / timed["vfa"][1], 4)
+            out[f"{kind}_max_abs_vs_vfa"] = float((runners[kind].o.float() - vfa_runner.o.float()).abs().max())
+    del runners
+    torch.cuda.empty_cache()
+    return out
+
+
+# parity tolerances against the float64 oracle (SURVEY.md §8c; the same as tests/test_gpu_parity.py)
+PARITY_TOL = {"o_max_abs": 2e-2, "o_max_rel_err": 1e-2, "lse_max_abs": 1e-4}
+
+
+def cpu_baseline(cfg, core_seconds, variant, gpu_o=None, gpu_lse=None):
+    """The oracle timed on a bounded sample of the workload on the host cores; with the GPU's
+    O / LSE of the same problem, also the parity of every sampled row against it."""
     cores = len(os.sched_getaffinity(0))
     L, d = cfg["L"], cfg["d"]
     # ~0.56 ms of one core per unit of i at d=128, Bc=128 (15.5 GF/s reference rate)
     heads = list(range(0, cfg["Hq"], max(cfg["Hq"] // 8, 1)))
     plan, _ = cpu_sample_plan(L, heads, 128, int(core_seconds / 0.6e-3))
     q, k, v = cpu_inputs(cfg, sorted({h for h, _ in plan}))
-    wall, busy = run_cpu_sample(q, k, v, plan, 128, 128, variant, cores)
+    wall, busy, outs = run_cpu_sample(q, k, v, plan, 128, 128, variant, cores, keep_outputs=True)
     fl = sample_flops(plan, 128, d)
-    return {"value": round(fl / wall / 1e12, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+    line = {"value": round(fl / wall / 1e12, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
             "sample": f"{len(plan)} query blocks (128 rows each) of {len(set(h for h, _ in plan))} heads of "
                       f"the same C2 problem, spread over causal depth; {fl:.3e} algorithmic FLOP; "
                       f"oracle/vfa_oracle.py float64 {variant}, {cores} fork workers x 1 BLAS thread",
             "wall_s": round(wall, 3), "core_s": round(busy, 3)}
+    parity = None
+    if gpu_o is not None:
+        o_err = rel = l_err = 0.0
+        nonfinite = rows = 0
+        for h, i, ref_o, ref_l in outs:
+            sl = slice((i - 1) * 128, i * 128)
+            g = gpu_o[0, h, sl].float().cpu().numpy().astype(np.float64)
+            gl = gpu_lse[0, h, sl].double().cpu().numpy()
+            nonfinite += int((~np.isfinite(g)).any(axis=1).sum() + (~np.isfinite(gl)).sum())
+            ref = ref_o.astype(np.float64)
+            o_err = max(o_err, float(np.abs(g - ref).max()))
+            den = np.maximum(np.abs(ref).max(axis=1), np.finfo(np.float64).tiny)
+            rel = max(rel, float((np.abs(g - ref).max(axis=1) / den).max()))
+            l_err = max(l_err, float(np.abs(gl - ref_l).max()))
+            rows += 128
+        parity = {"rows": rows, "blocks": len(outs), "o_max_abs": o_err, "o_max_rel_err": rel,
+                  "lse_max_abs": l_err, "nonfinite": nonfinite, "tol": PARITY_TOL,
+                  "reference": "oracle/vfa_oracle.py float64 (pinned bit-for-bit to vfa_lab), same bf16 inputs"}
+        parity["ok"] = bool(nonfinite == 0 and o_err <= PARITY_TOL["o_max_abs"]
+                            and rel <= PARITY_TOL["o_max_rel_err"] and l_err <= PARITY_TOL["lse_max_abs"])
+    return line, parity
 
 
 def main_reference(args):
@@ -542,6 +756,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="KV heads per pipelined host chunk")
     ap.add_argument("--e2e-qchunk", type=int, default=2, help="query heads per pipelined sub-chunk (0: all)")
+    ap.add_argument("--no-sweeps", action="store_true", help="skip the C3 / C5 / vendor extra keys")
+    ap.add_argument("--sweep-steps", type=int, default=5)
     ap.add_argument("--cpu-core-seconds", type=float, default=24.0)
     ap.add_argument("--cpu-core-seconds-ref", type=float, default=2.5,
                     help="per-step wall seconds of the reference arm (x cores)")

@@ -75,7 +75,16 @@ extern "C" {
 #define VFA_STAT_OVER_F16 5       /* monitor: exp args > ln(65504) */
 #define VFA_STAT_ELIDED 6         /* BLASST-FA4: SkipStats.rescales_elided */
 #define VFA_STAT_ROWS_MASKED 7    /* BLASST rowskip: SkipStats.rows_masked */
-#define VFA_STAT_COUNT 8
+/* monitor = 1 only (OverflowMonitor.exp_arg_max / calibration_gap, src/vfa.py:109-135). Float
+ * statistics in log2 units of the scaled scores (natural units = value * ln 2), stored as
+ * order-preserving keys: key = bits ^ (bits >> 31 ? 0xffffffff : 0x80000000), 0 = no value. */
+#define VFA_STAT_EXP_ARG_MAX 8    /* key of the largest finite exp argument (processed blocks) */
+#define VFA_STAT_GAP_NEG_MIN 9    /* key of -min over rows of (m seed - exact global row max) */
+#define VFA_STAT_GAP_MAX 10       /* key of max over rows of the same gap */
+#define VFA_STAT_GAP_SUM 11       /* double: sum of the gaps */
+#define VFA_STAT_GAP_BELOW 12     /* rows with gap < 0 (seed below the exact max) */
+#define VFA_STAT_GAP_ROWS 13      /* rows with a seed (m-init on); 0 = no gap recorded */
+#define VFA_STAT_COUNT 14
 
 /* status[] slots (uint32, device; initialised by vfa_fwd when non-NULL) */
 #define VFA_STATUS_FLAGS 0          /* bit0 fully-masked row, bit1 normalizer underflow, bit2 non-finite O */
@@ -90,9 +99,12 @@ typedef struct VfaParams {
   /* element strides for (batch, head, row); all must be multiples of 8 (16 bytes) */
   int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
   /* lse is a contiguous float32 [B, Hq, Lq] */
-  double scale;         /* softmax scale; <= 0 selects 1/sqrt(D) (src/reference.py:45-46) */
+  double scale;         /* softmax scale > 0; 0 selects 1/sqrt(D) (src/reference.py:45-46); negative,
+                           infinite or NaN is rejected (VFA_ERR_CONFIG): the kernels fold the scale in
+                           after the row max, which needs max(s) * scale == max(s * scale) */
   int32_t causal;       /* entrywise causal mask (requires Lq == Lk, src/reference.py:43-44) */
-  int32_t q_block;      /* BlockSpec.q_block: must be 128 (tcgen05 M) */
+  int32_t q_block;      /* BlockSpec.q_block: 16, 32, 64 or 128 (one reference query block per
+                           128-row tcgen05 tile; below 128 the remaining rows run idle) */
   int32_t k_block;      /* BlockSpec.k_block: 64 or 128 */
   int32_t variant;      /* VFA_VARIANT_* */
   int32_t kind;         /* VFA_KREPR_* */
@@ -106,6 +118,7 @@ typedef struct VfaParams {
   double lam;           /* VSA threshold lambda in (0, 1]; <= 0 disables skipping (SkipConfig.lam=None) */
   int32_t krepr_precomputed; /* 1: workspace already holds vfa_krepr() output for this K; skip recomputing */
   int32_t softmax_split; /* threads sharing one row of a query tile: 0 = per-variant default,
+                           1 = a softmax warpgroup per query tile (one thread per row),
                            2 = per-tile warp sets, 4 = all softmax warps serve both tiles */
   double tau;           /* BLASST-FA4 rescale elision: max increase <= tau * ln 2 (SkipConfig.tau) */
   int32_t cta_pair;     /* 0 = default, 1 = one CTA per unit, 2 = CTA pairs (even GQA group, d = 128):
@@ -130,6 +143,19 @@ VFA_API size_t vfa_workspace_bytes(const VfaParams* p);
 VFA_API int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                     void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                     unsigned char* skip_trace, int* stab_block, void* stream);
+
+/* vfa_fwd with a per-row exponent rebase: row_bias float32 [B, Hq, Lq] (device, log2 units of
+ * the scaled scores) multiplies the row's exponentials and normalizer by 2^bias, which leaves
+ * O = PV / l unchanged and is subtracted from the LSE. Recovery path for the fp32 normalizer
+ * underflow: a VFA row whose frozen max exceeds every score by more than fp32's exp range
+ * (~87 nats) gets l == 0 on the device (vfa_fwd flags it like NormalizerUnderflowError and
+ * writes the frozen max, natural units, into its LSE slot) although the float64 reference
+ * normalizes it (src/core.py:101-109) as long as the gap stays below ~745 nats; re-running with
+ * bias = (frozen max - exact row max) * log2(e) on those rows (0 elsewhere: bitwise vfa_fwd)
+ * computes them exactly. The Python layer does this automatically (api.attention_forward). */
+VFA_API int vfa_fwd_rebased(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                            void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                            const float* row_bias, void* stream);
 
 /* Bytes of device scratch vfa_fwd_host needs (up to four K/V group slots and eight query
  * sub-chunk slots), or 0 if the parameters or the chunking are invalid. */

@@ -200,13 +200,23 @@ def _skip_margin(m_tilde, m_merged, ln_lambda):
     return abs(float(g.max()) - ln_lambda)
 
 
+# arguments within this distance (natural units) of a monitor threshold are "near": an fp32
+# device computes the argument with error well below it, so its counts may differ from the
+# float64 ones by at most the near counts (test infrastructure, not in the reference)
+NEAR_MARGIN = 5e-3
+
+
 @dataclass
 class Monitor:
-    """src/vfa.py:109-128 (OverflowMonitor.record), without the calibration gap."""
+    """src/vfa.py:109-135 (OverflowMonitor.record / record_gap)."""
 
     exp_arg_max: float = NEG_INF
     count_over_f16: int = 0
     count_over_f32: int = 0
+    near_f16: int = 0
+    near_f32: int = 0
+    calibration_gap: dict | None = None
+    gap: np.ndarray | None = None  # per-row m seed - exact global row max (record_gap input)
 
     def record(self, args):
         finite = args[~np.isneginf(args)]
@@ -215,6 +225,37 @@ class Monitor:
         self.exp_arg_max = max(self.exp_arg_max, float(finite.max()))
         self.count_over_f16 += int((finite > F16_EXP_LIMIT).sum())
         self.count_over_f32 += int((finite > F32_EXP_LIMIT).sum())
+        self.near_f16 += int((np.abs(finite - F16_EXP_LIMIT) <= NEAR_MARGIN).sum())
+        self.near_f32 += int((np.abs(finite - F32_EXP_LIMIT) <= NEAR_MARGIN).sum())
+
+    def record_gap(self, m_seed, exact_m):
+        """src/vfa.py:129-135."""
+        gap = m_seed - exact_m
+        self.gap = gap
+        self.calibration_gap = gap_summary([gap])
+
+
+def gap_summary(gaps):
+    """The calibration_gap dict (src/vfa.py:131-135) over the concatenated per-row gaps."""
+    gap = np.concatenate([np.asarray(g, dtype=np.float64) for g in gaps])
+    return {"min": float(gap.min()), "max": float(gap.max()), "mean": float(gap.mean()),
+            "frac_below": float((gap < 0).mean())}
+
+
+def exact_rowmax_global(q, k, scale, causal, rows=None):
+    """src/reference.py:55-63, 105-111: per-row maximum over all unmasked scaled scores,
+    (q @ k.T) * scale with the entrywise causal mask. rows: optional index array of query rows
+    (the full-matrix product is then restricted to them; used for large problems)."""
+    qq = q if rows is None else q[rows]
+    s = (qq @ k.T) * scale
+    if causal:
+        r = np.arange(q.shape[0]) if rows is None else np.asarray(rows)
+        cols = np.arange(k.shape[0])
+        s[cols[None, :] > r[:, None]] = NEG_INF
+    m = s.max(axis=1)
+    if np.isneginf(m).any():
+        raise FullyMaskedRow(int(np.argmax(np.isneginf(m))))
+    return m
 
 
 @dataclass
@@ -245,7 +286,7 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
                  scale=None, kind="sabsmax", qkind="row_wise", reorder=True,
                  use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None, tau=0.0,
                  order="sequential", raise_errors=True, record_decisions=False,
-                 q_blocks=None) -> HeadResult:
+                 q_blocks=None, monitor=False) -> HeadResult:
     """One head of fa_forward (src/fa.py:28-61), vfa_forward (src/vfa.py:156-223),
     vsa_forward (src/sparse.py:256-329) or the BLASST family -- blasst_forward (order
     'sequential' | 'sink_local', src/sparse.py:112-152), blasst_fa4_forward (tau rescale
@@ -255,6 +296,9 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
     q_blocks: optional iterable of 1-based query blocks to compute (the others are left
     NaN); used to time bounded samples of large problems. Query blocks are independent
     (SPEC.md:212), so a sampled block is computed exactly as in the full pass.
+    monitor: also record the calibration gap (src/vfa.py:217-221, src/sparse.py:324-327) when
+    the m-init seeds are in use; the argument statistics are recorded on every call, like the
+    reference.
     """
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
@@ -292,8 +336,11 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
     lse = np.full(nq, np.nan)
     res = HeadResult(out=out, lse=lse, stab=np.zeros(nq, dtype=np.int64))
     kreprs = precompute_kreprs(k, kb, kind, tc1) if use_m_init else None
+    seeds = np.full(nq, np.nan) if (monitor and use_m_init) else None
+    blocks_done = []
 
     for i in (range(1, t_r + 1) if q_blocks is None else q_blocks):
+        blocks_done.append(i)
         vmax = visible_key_blocks(i, qb, kb, t_c, causal)
         local = local_key_block(i, qb, kb, t_c)
         if variant in ("fa", "blasst", "blasst_fa4", "blasst_rowskip"):
@@ -309,6 +356,8 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
             m = m_init(qi, kreprs[: min(vmax, len(kreprs))], scale, qkind)
         else:
             m = np.full(qb, NEG_INF)
+        if seeds is not None:
+            seeds[(i - 1) * qb: i * qb] = m
         l = np.zeros(qb)
         o = np.zeros((qb, d))
         dec = []
@@ -393,6 +442,11 @@ def forward_head(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=1
         with np.errstate(divide="ignore", invalid="ignore"):
             out[(i - 1) * qb: i * qb] = o / l[:, None]
             lse[(i - 1) * qb: i * qb] = m + np.log(l)
+    if seeds is not None:
+        rows = None if q_blocks is None else np.concatenate(
+            [np.arange((i - 1) * qb, i * qb) for i in blocks_done])
+        exact = exact_rowmax_global(q, k, scale, causal, rows)
+        res.monitor.record_gap(seeds if rows is None else seeds[rows], exact)
     return res
 
 
@@ -426,8 +480,14 @@ def forward(q, k, v, **kw):
 
 def _stats(results):
     st = {"visited": 0, "skipped": 0, "special": 0, "frozen": 0, "elided": 0, "rows_masked": 0,
-          "count_over_f16": 0, "count_over_f32": 0, "exp_arg_max": NEG_INF}
+          "count_over_f16": 0, "count_over_f32": 0, "near_f16": 0, "near_f32": 0,
+          "exp_arg_max": NEG_INF, "calibration_gap": None}
+    gaps = [r.monitor.gap for r in results if r.monitor.gap is not None]
+    if gaps:
+        st["calibration_gap"] = gap_summary(gaps)
     for r in results:
+        st["near_f16"] += r.monitor.near_f16
+        st["near_f32"] += r.monitor.near_f32
         st["elided"] += r.elided
         st["rows_masked"] += r.rows_masked
         st["visited"] += r.visited

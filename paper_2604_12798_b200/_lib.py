@@ -27,15 +27,16 @@ KEY_REPRS = ("sabsmax", "k_max", "k_mean", "k_absmax_unsigned")  # src/vfa.py:39
 QUERY_REPRS = ("row_wise", "q_absmax", "q_sabsmax", "q_mean")  # src/vfa.py:40
 
 (STAT_VISITED, STAT_SKIPPED, STAT_SPECIAL, STAT_FROZEN, STAT_OVER_F32, STAT_OVER_F16, STAT_ELIDED,
- STAT_ROWS_MASKED) = range(8)
-STAT_COUNT = 8
+ STAT_ROWS_MASKED, STAT_EXP_ARG_MAX, STAT_GAP_NEG_MIN, STAT_GAP_MAX, STAT_GAP_SUM, STAT_GAP_BELOW,
+ STAT_GAP_ROWS) = range(14)
+STAT_COUNT = 14
 STATUS_FLAGS, STATUS_UNDERFLOW_ROW, STATUS_MASKED_ROW, STATUS_NONFINITE_ROWS = range(4)
 STATUS_COUNT = 4
 
 # every symbol include/vfa_b200.h declares
 EXPORTS = ("vfa_check_params", "vfa_workspace_bytes", "vfa_fwd", "vfa_krepr", "vfa_schedule",
            "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace",
-           "vfa_host_scratch_bytes", "vfa_fwd_host", "vfa_krepr_range")
+           "vfa_host_scratch_bytes", "vfa_fwd_host", "vfa_krepr_range", "vfa_fwd_rebased")
 
 
 class VfaParams(ctypes.Structure):
@@ -77,6 +78,8 @@ def bind(path: str):
     lib.vfa_workspace_bytes.restype = ctypes.c_size_t
     lib.vfa_fwd.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp, vp]
     lib.vfa_fwd.restype = ctypes.c_int
+    lib.vfa_fwd_rebased.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
+    lib.vfa_fwd_rebased.restype = ctypes.c_int
     lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int, ctypes.c_int]
     lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
     lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, ctypes.c_int,
@@ -111,6 +114,16 @@ def load():
                 f"{LIB_PATH} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
         _lib = bind(LIB_PATH)
         return _lib
+
+
+def key_to_float(key: int) -> float:
+    """Decode an order-preserving float key of the stats word (include/vfa_b200.h); NaN if unset."""
+    import struct
+    key &= 0xFFFFFFFF
+    if key == 0:
+        return float("nan")
+    bits = key ^ 0x80000000 if key & 0x80000000 else (~key) & 0xFFFFFFFF
+    return struct.unpack("<f", struct.pack("<I", bits))[0]
 
 
 def last_error() -> str:

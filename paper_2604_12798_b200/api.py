@@ -17,8 +17,8 @@ tensors. Differences that follow from running on the GPU: O is returned as a bf1
 torch tensor on the device (shape of q), the LSE is returned as well (`.lse`),
 `trace` is a DeviceTrace (the per-row stabilization positions the reference's
 StateTrace feeds into stabilization_positions, recorded by the kernel instead of per-visit
-m snapshots), and the OverflowMonitor counts come from device counters when monitor=True
-(exp_arg_max is not tracked).
+m snapshots), and the OverflowMonitor statistics come from device counters when
+monitor=True.
 """
 
 from __future__ import annotations
@@ -33,6 +33,7 @@ import torch
 from . import _lib
 
 NEG_INF = float("-inf")
+LN2 = math.log(2.0)
 
 
 # ----------------------------------------------------------------------------- errors
@@ -310,9 +311,11 @@ class OpCounters:
 
 @dataclass
 class OverflowMonitor:
-    """src/vfa.py:109-135; GPU counts exp arguments > ln 65504 and > 88.7228."""
+    """src/vfa.py:109-135: exp arguments > ln 65504 and > 88.7228 counted on the device, the
+    largest argument, and the calibration gap (m seed - exact global row max: min / max / mean /
+    frac_below) from the device's seeds and exact row maxima (monitor=True)."""
 
-    exp_arg_max: float = float("nan")
+    exp_arg_max: float = NEG_INF
     count_over_f16: int = 0
     count_over_f32: int = 0
     calibration_gap: dict | None = None
@@ -352,6 +355,10 @@ def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind
     p.k_stride[:] = _strides(k)
     p.v_stride[:] = _strides(v)
     p.o_stride[:] = _strides(o)
+    if scale is not None and not (math.isfinite(scale) and scale > 0):
+        # the kernels fold the scale into exp2 after the row max: a positive finite scale keeps
+        # max(s) * scale == max(s * scale); None (0.0 across the C ABI) means 1/sqrt(d)
+        raise ValueError(f"scale must be a positive finite number, got {scale}")
     p.scale = float(scale) if scale is not None else 0.0
     p.causal = int(bool(causal))
     p.q_block, p.k_block = int(q_block), int(k_block)
@@ -368,6 +375,31 @@ def _params(q, k, v, o, *, variant, causal, q_block, k_block, scale, kind, qkind
     p.softmax_split = int(softmax_split)
     p.cta_pair = int(cta_pair)
     return p
+
+
+def _check_shapes(q, k, v):
+    """The AttentionProblem checks (src/reference.py:31-46) on [B, H, N, d] tensors: the C ABI
+    takes batch and head_dim from q and the key length from k, so a mismatch must be caught
+    here (it would otherwise index past the end of k / v)."""
+    if tuple(k.shape) != tuple(v.shape):
+        raise ValueError("K and V must have the same shape")
+    if k.shape[0] != q.shape[0]:
+        raise ValueError("Q and K/V batch sizes differ")
+    if k.shape[3] != q.shape[3]:
+        raise ValueError("Q, K, V must share the head dimension")
+    if q.shape[1] % k.shape[1]:
+        raise ValueError("query heads must be a multiple of key/value heads")
+
+
+def _check_outputs(q, out, lse, dev):
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.bfloat16 or out.device != dev:
+        raise ValueError("out must be a bf16 tensor on q's device")
+    if tuple(out.shape) != tuple(q.shape) or out.stride(-1) != 1:
+        raise ValueError(f"out must have q's shape {tuple(q.shape)} with a contiguous head dimension")
+    if not isinstance(lse, torch.Tensor) or lse.dtype != torch.float32 or lse.device != dev:
+        raise ValueError("lse must be a float32 tensor on q's device")
+    if tuple(lse.shape) != tuple(q.shape[:3]) or not lse.is_contiguous():
+        raise ValueError(f"lse must be a contiguous float32 tensor of shape {tuple(q.shape[:3])}")
 
 
 def _raise_for(rc):
@@ -424,11 +456,15 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
             raise TypeError(f"{name} must be a bf16 CUDA tensor")
         if x.dim() != 4:
             raise ValueError(f"{name} must be 4-D [B, H, N, d]")
+    _check_shapes(q, k, v)
     dev = q.device
+    if k.device != dev or v.device != dev:
+        raise ValueError("q, k and v must be on the same device")
     if out is None:
         out = torch.empty(q.shape, dtype=torch.bfloat16, device=dev)
     if lse is None:
         lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
+    _check_outputs(q, out, lse, dev)
     p = _params(q, k, v, out, variant=variant, causal=causal, q_block=q_block, k_block=k_block,
                 scale=scale, kind=kind, qkind=qkind, reorder=reorder, use_m_init=use_m_init,
                 tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, monitor=monitor,
@@ -463,8 +499,73 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
         _raise_for(rc)
     info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws, "stab_block": stab}
     if check:
+        flags = int(status[_lib.STATUS_FLAGS].item())
+        if flags & 2 and not flags & 1 and variant == "vfa" and use_m_init:
+            # fp32 normalizer underflow with a finite frozen max: recompute those rows exactly
+            # (or raise like the float64 reference when its own exp underflows too)
+            with torch.cuda.device(dev):
+                _rebase_underflow_rows(lib, p, q, k, v, out, lse, ws, ws_bytes, st, status)
+            info["rebased_rows"] = True
+            return out, lse, info
         check_status(status)
     return out, lse, info
+
+
+# np.exp(x) == 0 in float64 for x below this (src/core.py:101-109: the reference's l underflows)
+F64_EXP_UNDERFLOW = -745.1332191019412
+
+
+def _rebase_underflow_rows(lib, p, q, k, v, out, lse, ws, ws_bytes, st, first_status):
+    """Recovery of rows whose fp32 normalizer underflowed (include/vfa_b200.h, vfa_fwd_rebased).
+
+    VFA freezes the running max at its m-init seed; when the seed exceeds every score of a row by
+    more than fp32's exp range (~87 nats) each exponential flushes to zero on the device, while
+    the float64 reference (src/vfa.py:209-215, src/core.py:95-109) still normalizes the row. The
+    kernel flags such rows (O = NaN, the frozen max in the LSE slot); here their exact row max is
+    computed (q . k^T over the visible keys, fp32), and the forward re-runs with the per-row
+    exponent rebase 2^(frozen - exact). Rows whose gap exceeds float64's exp range raise
+    NormalizerUnderflowError like the reference."""
+    flagged = torch.isnan(out[..., 0]) & torch.isfinite(lse)
+    idx = flagged.nonzero()
+    if idx.numel() == 0:  # (the kernel flags every such row; keep the first pass's error)
+        check_status(first_status)
+    B, Hq, Lq, d = q.shape
+    group = Hq // k.shape[1]
+    scale = p.scale if p.scale > 0 else 1.0 / math.sqrt(d)
+    exact = torch.empty(idx.shape[0], dtype=torch.float32, device=q.device)
+    lin = (idx[:, 0] * Hq + idx[:, 1]) * Lq + idx[:, 2]
+    order = torch.argsort(lin)
+    idx, lin = idx[order], lin[order]
+    heads = torch.unique(idx[:, 0] * Hq + idx[:, 1]).tolist()
+    for bh in heads:
+        b, h = divmod(int(bh), Hq)
+        sel = ((idx[:, 0] == b) & (idx[:, 1] == h)).nonzero().flatten()
+        kk = k[b, h // group].float()
+        for c0 in range(0, sel.numel(), 2048):
+            rows_i = sel[c0:c0 + 2048]
+            rows = idx[rows_i, 2]
+            s = (q[b, h, rows].float() @ kk.T) * scale
+            if p.causal:
+                cols = torch.arange(kk.shape[0], device=q.device)
+                s = s.masked_fill(cols[None, :] > rows[:, None], float("-inf"))
+            exact[rows_i] = s.max(dim=1).values
+    frozen = lse[idx[:, 0], idx[:, 1], idx[:, 2]]
+    gap = frozen.double() - exact.double()
+    dead = (-gap < F64_EXP_UNDERFLOW).nonzero()
+    if dead.numel():
+        raise NormalizerUnderflowError(int(lin[dead[0, 0]].item()))
+    bias = torch.zeros(q.shape[:3], dtype=torch.float32, device=q.device)
+    bias[idx[:, 0], idx[:, 1], idx[:, 2]] = (gap / LN2).float()
+    stats = torch.empty(_lib.STAT_COUNT, dtype=torch.int64, device=q.device)
+    status = torch.empty(_lib.STATUS_COUNT, dtype=torch.int32, device=q.device)
+    p2 = _lib.VfaParams.from_buffer_copy(p)
+    p2.krepr_precomputed = 1  # the representations of the first pass are still in `ws`
+    rc = lib.vfa_fwd_rebased(ctypes.byref(p2), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                             lse.data_ptr(), ws.data_ptr(), ws_bytes, stats.data_ptr(), status.data_ptr(),
+                             bias.data_ptr(), ctypes.c_void_p(st))
+    if rc:
+        _raise_for(rc)
+    check_status(status)
 
 
 def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128, k_block=128,
@@ -489,6 +590,7 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
             raise ValueError(f"{name} must be 4-D [B, H, N, d]")
         if not x.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
+    _check_shapes(q, k, v)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     pin = q.is_pinned()
     if out is None:
@@ -524,7 +626,18 @@ def attention_forward_host(q, k, v, *, variant="vfa", causal=False, q_block=128,
         _raise_for(rc)
     info = {"stats": stats, "status": status, "skip_trace": None, "workspace": None}
     if check:
-        check_status(status)  # reads the status word: synchronizes with the stream
+        flags = int(status[_lib.STATUS_FLAGS].item())  # synchronizes with the stream
+        if flags & 2 and not flags & 1 and variant == "vfa" and use_m_init:
+            # fp32 normalizer underflow: the (rare) recovery runs on device-resident copies
+            o_d, l_d, info = attention_forward(
+                q.to(dev), k.to(dev), v.to(dev), variant=variant, causal=causal, q_block=q_block,
+                k_block=k_block, scale=scale, kind=kind, qkind=qkind, reorder=reorder,
+                use_m_init=use_m_init, tc1=tc1, n_sink=n_sink, n_local=n_local, lam=lam, tau=tau,
+                monitor=monitor, check=True, softmax_split=softmax_split, cta_pair=cta_pair)
+            out.copy_(o_d.cpu())
+            lse.copy_(l_d.cpu())
+            return out, lse, info
+        check_status(status)
         torch.cuda.synchronize(dev)
     return out, lse, info
 
@@ -542,11 +655,24 @@ def check_status(status: torch.Tensor):
 
 def stats_dict(info) -> dict:
     s = info["stats"].cpu().tolist()
-    return {"visited": s[_lib.STAT_VISITED], "skipped": s[_lib.STAT_SKIPPED],
-            "special": s[_lib.STAT_SPECIAL], "frozen": s[_lib.STAT_FROZEN],
-            "elided": s[_lib.STAT_ELIDED], "rows_masked": s[_lib.STAT_ROWS_MASKED],
-            "count_over_f32": s[_lib.STAT_OVER_F32], "count_over_f16": s[_lib.STAT_OVER_F16],
-            "nonfinite_rows": int(info["status"].cpu()[_lib.STATUS_NONFINITE_ROWS])}
+    d = {"visited": s[_lib.STAT_VISITED], "skipped": s[_lib.STAT_SKIPPED],
+         "special": s[_lib.STAT_SPECIAL], "frozen": s[_lib.STAT_FROZEN],
+         "elided": s[_lib.STAT_ELIDED], "rows_masked": s[_lib.STAT_ROWS_MASKED],
+         "count_over_f32": s[_lib.STAT_OVER_F32], "count_over_f16": s[_lib.STAT_OVER_F16],
+         "nonfinite_rows": int(info["status"].cpu()[_lib.STATUS_NONFINITE_ROWS])}
+    # monitor statistics (log2 units on the device -> natural units, src/vfa.py:109-135)
+    amax = _lib.key_to_float(s[_lib.STAT_EXP_ARG_MAX])
+    d["exp_arg_max"] = NEG_INF if math.isnan(amax) else amax * LN2
+    rows = s[_lib.STAT_GAP_ROWS]
+    if rows:
+        gsum = np.array([s[_lib.STAT_GAP_SUM]], dtype=np.int64).view(np.float64)[0]
+        d["calibration_gap"] = {"min": -_lib.key_to_float(s[_lib.STAT_GAP_NEG_MIN]) * LN2,
+                                "max": _lib.key_to_float(s[_lib.STAT_GAP_MAX]) * LN2,
+                                "mean": float(gsum) / rows * LN2,
+                                "frac_below": s[_lib.STAT_GAP_BELOW] / rows}
+    else:
+        d["calibration_gap"] = None
+    return d
 
 
 # ----------------------------------------------------------------------------- reference-shaped entry points
@@ -621,10 +747,16 @@ def _counters(st, p: AttentionProblem, variant: str) -> OpCounters:
 
 
 def _monitor(st, monitor: bool) -> OverflowMonitor:
+    """OverflowMonitor from the device counters (src/vfa.py:109-135). The reference records
+    the argument statistics on every call and the calibration gap only with monitor=True;
+    the device records all of them only with monitor=True (the counting costs kernel time),
+    so without it exp_arg_max is -inf and the counts are 0."""
     m = OverflowMonitor()
     if monitor:
         m.count_over_f16 = st["count_over_f16"]
         m.count_over_f32 = st["count_over_f32"]
+        m.exp_arg_max = st["exp_arg_max"]
+        m.calibration_gap = st["calibration_gap"]
     return m
 
 

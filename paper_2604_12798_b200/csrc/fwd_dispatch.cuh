@@ -2,6 +2,7 @@
 // (fwd_<variant>.cu). Each TU instantiates one MODE for every head dim / key block /
 // query-tiles-per-CTA / softmax split.
 #pragma once
+#include <atomic>
 #include <string>
 
 #include "vfa_internal.h"
@@ -14,8 +15,14 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
                const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t stream) {
   using C = vfa::Cfg<D, BC, NQ, SPLIT, MODE, PAIR>;
   auto kern = vfa::vfa_fwd_kernel<D, BC, NQ, MODE, SPLIT, PAIR>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // cudaFuncSetAttribute applies to the current device only: one flag bit per device, set
+  // after the attribute is in place (a racing second setter is harmless)
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+    return vfa_host::fail(VFA_ERR_CUDA, "cudaGetDevice failed");
+  const unsigned long long bit = 1ull << dev;
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return vfa_host::fail(VFA_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     cudaFuncAttributes fa;
@@ -24,7 +31,7 @@ int launch_fwd(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk,
     if (C::kRegBudget > fa.numRegs * C::kThreads)
       return vfa_host::fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(C::kRegBudget) + " exceeds the launch allocation " +
                                     std::to_string(fa.numRegs * C::kThreads) + " (would deadlock)");
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   const long long units = static_cast<long long>(args.B) * args.Hkv * args.units_per_kvh;
   if (units <= 0) return VFA_OK;

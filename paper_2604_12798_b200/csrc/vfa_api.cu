@@ -133,7 +133,7 @@ void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                  unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
-                 long long row_base);
+                 long long row_base, void* seed_ws = nullptr, const float* row_bias = nullptr);
 
 }  // namespace
 
@@ -158,6 +158,9 @@ int vfa_check_params(const VfaParams* p) {
   if (p->cta_pair < 0 || p->cta_pair > 2) return fail(VFA_ERR_CONFIG, "cta_pair must be 0 (auto), 1 (off) or 2 (on)");
   if (p->variant >= VFA_VARIANT_VSA && p->lam > 1.0) return fail(VFA_ERR_CONFIG, "lambda must be in (0, 1]");
   if (!(p->tau >= 0.0)) return fail(VFA_ERR_CONFIG, "tau must be >= 0");  // src/sparse.py:52-53 (NaN rejected)
+  // 0 selects 1/sqrt(d); the kernels fold the scale in after the row max, which needs scale > 0
+  if (!(p->scale >= 0.0) || std::isinf(p->scale))
+    return fail(VFA_ERR_CONFIG, "scale must be a positive finite number (0 = 1/sqrt(head_dim))");
   if (p->batch < 1 || p->heads_q < 1 || p->heads_kv < 1 || p->seq_q < 1 || p->seq_k < 1)
     return fail(VFA_ERR_DATA, "all dimensions must be >= 1");
   if (p->heads_q % p->heads_kv) return fail(VFA_ERR_DATA, "heads_q must be a multiple of heads_kv");
@@ -213,6 +216,18 @@ int vfa_fwd(const VfaParams* p, const void* q, const void* k, const void* v, voi
                       static_cast<cudaStream_t>(stream), true, 0);
 }
 
+int vfa_fwd_rebased(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                    void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                    const float* row_bias, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !row_bias) return fail(VFA_ERR_DATA, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
+  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, nullptr, nullptr,
+                      static_cast<cudaStream_t>(stream), true, 0, nullptr, row_bias);
+}
+
 }  // extern "C"
 
 namespace {
@@ -221,7 +236,7 @@ namespace {
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                  unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
-                 long long row_base) {
+                 long long row_base, void* seed_ws, const float* row_bias) {
   int rc = VFA_OK;
   // m-initialisation belongs to the frozen-max variants; FA and the BLASST family start at -inf
   const bool minit = (p->variant == VFA_VARIANT_VFA || p->variant == VFA_VARIANT_VSA) && p->use_m_init;
@@ -260,7 +275,9 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   const float* m0_tile = nullptr;
   if (minit && p->qkind != 0) {
     // block-wise query representation: per query tile, seed = max_j qrepr . krepr_j
-    uint8_t* qrep = static_cast<uint8_t*>(workspace) + ws_krepr_bytes(p);
+    // (seed_ws: a per-call seed area, so launches sharing one K/V workspace on different
+    // streams do not overwrite each other's query representations and seeds)
+    uint8_t* qrep = seed_ws ? static_cast<uint8_t*>(seed_ws) : static_cast<uint8_t*>(workspace) + ws_krepr_bytes(p);
     float* m0 = reinterpret_cast<float*>(qrep + ws_qrepr_bytes(p));
     const int tr = static_cast<int>(p->seq_q / p->q_block);
     rc = launch_block_repr(q, p->batch, p->heads_q, p->q_stride, D, p->q_block, tr, qkind_as_block_kind(p->qkind), qrep, 0,
@@ -322,6 +339,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.skip_trace = skip_trace;
   a.stab = stab_block;
   a.m0_tile = m0_tile;
+  a.row_bias = row_bias;
   a.row_base = row_base;
   a.trace = g_debug_trace;
 
@@ -347,6 +365,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct HostPlan {
   int64_t ck = 0, nqs = 0, subs = 0, groups = 0, chunks = 0, kv_slots = 0, q_slots = 0;
   size_t q_bytes = 0, kv_bytes = 0, lse_bytes = 0, ws_bytes = 0, kv_slot_bytes = 0, q_slot_bytes = 0;
+  size_t seed_bytes = 0;  // block-wise qkind: query representations + per-tile seeds, per Q slot
   bool minit = false;
   VfaParams cp{};  // the per-sub-chunk problem (dense device layout)
 };
@@ -389,7 +408,8 @@ bool host_plan(const VfaParams* p, int chunk_kv_heads, int chunk_q_heads, HostPl
   g.lse_bytes = static_cast<size_t>(g.nqs * p->seq_q * 4);
   g.ws_bytes = vfa_workspace_bytes(&g.cp);
   g.kv_slot_bytes = 2 * align_up(g.kv_bytes) + align_up(g.ws_bytes);
-  g.q_slot_bytes = 2 * align_up(g.q_bytes) + align_up(g.lse_bytes);
+  if (g.minit && p->qkind != 0) g.seed_bytes = align_up(ws_qrepr_bytes(&g.cp) + ws_m0_bytes(&g.cp));
+  g.q_slot_bytes = 2 * align_up(g.q_bytes) + align_up(g.lse_bytes) + g.seed_bytes;
   *out = g;
   return true;
 }
@@ -469,6 +489,14 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
   auto cleanup = [&]() {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);  // released once their work completes
   };
+  // error after work was enqueued: wait for every in-flight copy / kernel of the pipeline before
+  // returning, since they reference caller-owned host buffers and scratch the caller may reuse
+  auto abort_pipeline = [&](int code) {
+    cudaStream_t all[4] = {hs->h2d, hs->d2h, hs->comp[0], hs->comp[1]};
+    for (cudaStream_t x : all) cudaStreamSynchronize(x);
+    cleanup();
+    return code;
+  };
   // counters accumulate over chunks; scratch reuse is ordered after the caller's prior work
   reset_counters(stats, status, caller);
   cudaEvent_t entry = new_event();
@@ -496,7 +524,7 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
     cudaMemcpyAsync(dk, static_cast<const uint8_t*>(k_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
     cudaMemcpyAsync(dv, static_cast<const uint8_t*>(v_host) + koff, g.kv_bytes, cudaMemcpyHostToDevice, hs->h2d);
     cudaEvent_t kv_in = new_event();
-    if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+    if (!kv_in) return abort_pipeline(fail(VFA_ERR_CUDA, "cudaEventCreate failed"));
     cudaEventRecord(kv_in, hs->h2d);
     mark("kv_in " + std::to_string(gi), hs->h2d);
     if (g.minit) {
@@ -505,9 +533,9 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       cudaStream_t cs0 = hs->comp[c & 1];
       cudaStreamWaitEvent(cs0, kv_in, 0);
       rc = launch_krepr(&g.cp, dk, dws, cs0);
-      if (rc) return cleanup(), rc;
+      if (rc) return abort_pipeline(rc);
       kv_in = new_event();
-      if (!kv_in) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+      if (!kv_in) return abort_pipeline(fail(VFA_ERR_CUDA, "cudaEventCreate failed"));
       cudaEventRecord(kv_in, cs0);
     }
     // The first and last K/V groups run in half-size query sub-chunks: the pipeline's fill (the
@@ -530,12 +558,13 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       uint8_t* dq = qsl;
       uint8_t* dout = dq + align_up(g.q_bytes);
       float* dlse = reinterpret_cast<float*>(dout + align_up(g.q_bytes));
+      void* dseed = g.seed_bytes ? reinterpret_cast<uint8_t*>(dlse) + align_up(g.lse_bytes) : nullptr;
       const size_t qoff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q * D) * 2;
       const size_t loff = static_cast<size_t>((b * p->heads_q + h0) * p->seq_q);
       if (q_free[c % g.q_slots]) cudaStreamWaitEvent(hs->h2d, q_free[c % g.q_slots], 0);
       cudaMemcpyAsync(dq, static_cast<const uint8_t*>(q_host) + qoff, q_bytes_g, cudaMemcpyHostToDevice, hs->h2d);
       cudaEvent_t q_in = new_event(), done = new_event(), out = new_event();
-      if (!q_in || !done || !out) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+      if (!q_in || !done || !out) return abort_pipeline(fail(VFA_ERR_CUDA, "cudaEventCreate failed"));
       cudaEventRecord(q_in, hs->h2d);
       mark("q_in " + std::to_string(c), hs->h2d);
       cudaStream_t cs = hs->comp[c & 1];
@@ -543,8 +572,8 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
       cudaStreamWaitEvent(cs, q_in, 0);
       mark("k_start " + std::to_string(c), cs);
       rc = forward_impl(&cpg, dq, dk, dv, dout, dlse, dws, g.ws_bytes, stats, status, nullptr, nullptr, cs,
-                        false, static_cast<long long>(loff));
-      if (rc) return cleanup(), rc;
+                        false, static_cast<long long>(loff), dseed);
+      if (rc) return abort_pipeline(rc);
       cudaEventRecord(done, cs);
       mark("k_end " + std::to_string(c), cs);
       cudaStreamWaitEvent(hs->d2h, done, 0);
@@ -558,7 +587,7 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
     }
   }
   cudaEvent_t exit_ev = new_event();
-  if (!exit_ev) return cleanup(), fail(VFA_ERR_CUDA, "cudaEventCreate failed");
+  if (!exit_ev) return abort_pipeline(fail(VFA_ERR_CUDA, "cudaEventCreate failed"));
   cudaEventRecord(exit_ev, hs->d2h);
   cudaStreamWaitEvent(caller, exit_ev, 0);
   if (timeline && !marks.empty()) {

@@ -83,11 +83,20 @@ struct FwdArgs {
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
   const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
+  const float* row_bias;  // per-row exponent rebase (log2 units, [B, Hq, Lq]) or null: P and l of the
+                          // row are scaled by 2^bias (O = PV / l unchanged), LSE corrected; used to
+                          // recover rows whose fp32 normalizer underflowed (vfa_fwd_rebased)
   int pair;            // host: 2 = launched as CTA pairs (clusters of two CTAs), else 1
   long long row_base;  // linear-row offset of this launch's (b=0, h=0, r=0) in the status word
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
 
+#ifndef VFA_S1_SPLIT34
+#define VFA_S1_SPLIT34 1
+#endif
+#ifndef VFA_POLY_S1
+#define VFA_POLY_S1 0  // one thread per row: exp2 pairs (of 8) on the FMA pipe in columns 32-95
+#endif
 #ifndef VFA_SB_MAX
 #define VFA_SB_MAX 2  // S buffers per tile (tuning experiments: 1 disables double buffering)
 #endif
@@ -100,7 +109,7 @@ struct FwdArgs {
 
 // debug timeline slots per visited block (CTA 0 only, builds with -DVFA_TRACE): softmax t:
 // S ready, P done; MMA t: P observed, next QK issued
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 20;
 #ifdef VFA_TRACE
 #define VFA_TRACE_EVENT(args, pos, slot)                                                     \
   do {                                                                                       \
@@ -135,6 +144,11 @@ struct Cfg {
   static constexpr int kOP = D / SPLIT;              // O columns rescaled / stored per part
   static constexpr int kNCH = kCP >= 32 ? 2 : 1;     // P hand-off chunks per block
   static constexpr int kCW = kCP / kNCH;             // columns per P chunk (16 or 32)
+  // PV K-steps (16 P columns each) released by the first P hand-off. One thread per row with
+  // 128-column rows (VFA_S1_SPLIT34): the first hand-off comes after 3/4 of the row, so only
+  // 2 K-steps of PV remain after the softmax finishes (a shorter P -> PV -> QK -> S chain).
+  static constexpr bool kS1Split = SPLIT == 1 && PAIR == 1 && kCP == 128 && VFA_S1_SPLIT34;
+  static constexpr int kKS0 = kS1Split ? 6 : kCW / 16;
   static constexpr int kWarpsPerTile = SPLIT * 4;    // softmax warps covering one tile
   static constexpr int kSoftmaxWarps = SPLIT == 1 ? 4 * NQ : 16;
   static constexpr int kMmaWarp = kSoftmaxWarps;
@@ -260,8 +274,14 @@ constexpr int kPolyOverride = -1;
 // P (hence O) does not depend on the split or the variant.
 // At head dim 64 (half the MMA work per exponential; the GPU is not power-capped) one pair
 // in eight on the FMA pipe is measured +4 % at Bc 128 (profiles/ab_r01_poly.txt).
-__host__ __device__ constexpr int poly_pairs(int d, int bc) {
+__host__ __device__ constexpr int poly_pairs(int d, int bc, int split) {
   return kPolyOverride >= 0 ? kPolyOverride : (d == 64 && bc == 128 ? 1 : 0);
+}
+#ifndef VFA_LATE_ROWSUM
+#define VFA_LATE_ROWSUM 0  // 1: row sums after the P hand-off for every split, 2: split 1 only
+#endif
+__host__ __device__ constexpr bool late_rowsum_on(int split) {
+  return VFA_LATE_ROWSUM == 1 || (VFA_LATE_ROWSUM == 2 && split == 1);
 }
 // softmax column split per mode (see the softmax role): measured best per variant
 #ifndef VFA_SPLIT_FA
@@ -295,12 +315,60 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   return y;
 }
 
+// Degree-3 FMA-pipe exp2 with a floor split (x = j + f, f in [0, 1)): 2^f by a polynomial
+// fitted here for minimax relative error (8.6e-5, far inside the bf16 rounding of P),
+// 2^j by an exponent add. 12 instructions per element pair (2 FMNMX clamps per element, one
+// FADD2 with round-down to extract floor(x), 2 FADD2, 3 FFMA2, 2 shift-adds) against 2 MUFU.EX2
+// (16 XU cycles). Clamped to [-127, 128] like MUFU.EX2.FTZ: x <= -127 and -inf give +0, x >= 128
+// gives +inf; x in (-127, -126) gives a denormal, which the flush-to-zero row sum drops.
+__device__ __forceinline__ float2 add_rm2(float2 a, float2 b) {
+  uint64_t r;
+  asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "add.rm.ftz.f32x2 %0, ra, rb;\n\t}"
+      : "=l"(r) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return make_float2(__uint_as_float(static_cast<uint32_t>(r)), __uint_as_float(static_cast<uint32_t>(r >> 32)));
+}
+__device__ __forceinline__ float2 add_ftz2(float2 a, float2 b) {
+  uint64_t r;
+  asm("{\n\t.reg .b64 ra, rb;\n\tmov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+      "add.rn.ftz.f32x2 %0, ra, rb;\n\t}"
+      : "=l"(r) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return make_float2(__uint_as_float(static_cast<uint32_t>(r)), __uint_as_float(static_cast<uint32_t>(r >> 32)));
+}
+__device__ __forceinline__ float2 ex2_poly3(float2 x) {
+  x.x = fminf(fmaxf(x.x, -127.f), 128.f);
+  x.y = fminf(fmaxf(x.y, -127.f), 128.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 r = add_rm2(x, magic);                          // floor(x) in the low mantissa bits
+  const float2 j = __fadd2_rn(r, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));    // exact, in [0, 1)
+  float2 p = __ffma2_rn(make_float2(0.07706704f, 0.07706704f), f, make_float2(0.22764499f, 0.22764499f));
+  p = __ffma2_rn(p, f, make_float2(0.69511676f, 0.69511676f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  float2 y;
+  y.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(r.x) << 23));
+  y.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(r.y) << 23));
+  return y;
+}
+#ifndef VFA_POLY3
+#define VFA_POLY3 1  // the FMA-pipe exp2 is the degree-3 floor form (0: degree-4, round to nearest)
+#endif
+
+// order-preserving key of a float (include/vfa_b200.h, VFA_STAT_EXP_ARG_MAX): larger float,
+// larger unsigned key
+__device__ __forceinline__ unsigned float_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 template <bool MON>
-__device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o16) {
+__device__ __forceinline__ void count_over(float2 x, uint32_t& o32, uint32_t& o16, float& xmax) {
   if (MON) {
-    // OverflowMonitor (src/vfa.py:122-128) thresholds, in log2 units
+    // OverflowMonitor (src/vfa.py:122-128) thresholds, in log2 units; exp_arg_max over the
+    // finite arguments (masked entries are -inf and never raise the max)
     o32 += (x.x > 128.0f) + (x.y > 128.0f);
     o16 += (x.x > 15.999295f) + (x.y > 15.999295f);
+    xmax = fmax3(xmax, x.x, x.y);
   }
 }
 
@@ -320,24 +388,37 @@ __device__ __forceinline__ float part_max(const float* v) {
 }
 
 // W consecutive columns (masked entries already -inf): P = exp2(s*cs - m2) -> W/2 packed
-// bf16x2 words; row sums into two independent packed accumulators (halves the FADD2 chain).
-template <int W, bool MON, int kPoly>
-__device__ __forceinline__ void p_chunk(const float* v, float2 cs2, float2 nmu2, uint32_t* u, float2 (&acc)[2],
-                                        uint32_t& o32, uint32_t& o16) {
+// bf16x2 words. LATE: P stays in v (fp32) for a row sum after the hand-off (off the
+// S -> P -> PV chain); otherwise row sums go into two independent packed accumulators.
+template <int W, bool MON, int kPoly, bool LATE>
+__device__ __forceinline__ void p_chunk(float* v, float2 cs2, float2 nmu2, uint32_t* u, float2 (&acc)[2],
+                                        uint32_t& o32, uint32_t& o16, float& xmax) {
 #pragma unroll
   for (int e = 0; e < W; e += 2) {
     const float2 x = __ffma2_rn(make_float2(v[e], v[e + 1]), cs2, nmu2);
-    count_over<MON>(x, o32, o16);
+    count_over<MON>(x, o32, o16, xmax);
     float2 p;
     if (((e >> 1) & 7) < kPoly) {
-      p = ex2_poly2(x);
+      p = VFA_POLY3 ? ex2_poly3(x) : ex2_poly2(x);
     } else {
       p.x = ex2_approx(x.x);
       p.y = ex2_approx(x.y);
     }
-    acc[(e >> 1) & 1] = __fadd2_rn(acc[(e >> 1) & 1], p);
+    if constexpr (LATE) {
+      v[e] = p.x;
+      v[e + 1] = p.y;
+    } else {
+      acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], p);
+    }
     u[e >> 1] = pack_bf16x2(p.x, p.y);
   }
+}
+
+// row sum of W exponentials left in v by a LATE p_chunk
+template <int W>
+__device__ __forceinline__ void late_rowsum(const float* v, float2 (&acc)[2]) {
+#pragma unroll
+  for (int e = 0; e < W; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
 }
 
 // ------------------------------------------------------------------------------------
@@ -353,7 +434,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
   constexpr int OP = C::kOP;
   constexpr int NCH = C::kNCH;
   constexpr int CW = C::kCW;
-  constexpr int kPoly = poly_pairs(D, BC);
+  constexpr int kPoly = poly_pairs(D, BC, SPLIT);
+  constexpr bool kLate = late_rowsum_on(SPLIT);
   constexpr int SB = C::kSB;
   using CtlT = Ctl<NS, NQ, SB>;
   static_assert(sizeof(CtlT) <= C::kCtlBytes, "control block too large");
@@ -503,8 +585,14 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         };
         for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
         for (int g = 0; g < G; ++g) {
-          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC, true);
-          if (g + SB < G) load_s_operand(g + SB);
+          if (g >= nchunks) {
+            load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC, true);
+            VFA_TRACE_EVENT(a, g - nchunks, 15);
+          }
+          if (g + SB < G) {
+            load_s_operand(g + SB);
+            if (g >= nchunks) VFA_TRACE_EVENT(a, g - nchunks, 16);
+          }
         }
       }
     } else if (warp == C::kMmaWarp && (PAIR == 1 || crank == 0)) {
@@ -538,15 +626,17 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
       if constexpr (C::kQT) {
         // Q_t -> TMEM (lane = row, 8 columns per 16-element K-step); executes ahead of the MMAs
         // issued after it by this thread (in-order tcgen05 pipe)
+        if (elect_one()) {
 #pragma unroll
-        for (int t = 0; t < NQ; ++t)
+          for (int t = 0; t < NQ; ++t)
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
-            const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + t * (C::kQBytes >> 4) + kLboK + oq);
-            if (elect_one()) tmem_cp_128x256b(tbase + C::kQBase + t * (D / 2) + kk * 8, da);
-            __syncwarp();
-          }
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+              const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + t * (C::kQBytes >> 4) + kLboK + oq);
+              tmem_cp_128x256b(tbase + C::kQBase + t * (D / 2) + kk * 8, da);
+            }
+        }
+        __syncwarp();
       }
       int stage = 0;
       uint32_t phase = 0;
@@ -560,16 +650,19 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         }
         return st;
       };
+      // One elected lane issues a whole batch of MMAs straight-line (electing per instruction
+      // costs an ELECT, uniform-register broadcasts and a reconvergence per MMA: the issue of
+      // a QK^T then took longer than its 512-cycle execution, profiles/trace_r02b.txt).
       auto issue_qk = [&](int t, int b, int st) {
         const uint32_t a_lo = q_lo + t * (C::kQBytes >> 4) + kLboK;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
-          const uint32_t ok = ((kk >> 2) * ((BC / PAIR) * 128) + (kk & 3) * 32) >> 4;
-          const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq);
-          const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok);
-          if (elect_one()) {
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oq = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t ok = ((kk >> 2) * ((BC / PAIR) * 128) + (kk & 3) * 32) >> 4;
+            const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (a_lo + oq);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + ok);
             if constexpr (PAIR == 2)
               mma_ss_pair(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
             else if constexpr (C::kQT)
@@ -577,30 +670,33 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
             else
               mma_ss(tbase + C::s_off(t, b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
           }
-          __syncwarp();
         }
+        __syncwarp();
       };
       // P of part pp occupies TMEM columns [pp*CP, pp*CP + CP/2) of S_t (packed bf16 pairs).
       // PV chunk c: the K-steps over P columns [c*CW, c*CW + CW) of every part.
       auto issue_pv_chunk = [&](int t, int b, int st, int c, bool& first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
+        const int k_lo = c == 0 ? 0 : C::kKS0, k_hi = c == 0 ? C::kKS0 : CP / 16;  // this chunk's K-steps
+        if (elect_one()) {
+          bool acc = !first;
 #pragma unroll
-        for (int pp = 0; pp < SPLIT; ++pp) {
+          for (int pp = 0; pp < SPLIT; ++pp) {
 #pragma unroll
-          for (int k2 = 0; k2 < CW / 16; ++k2) {
-            const int kk = pp * (CP / 16) + c * (CW / 16) + k2;  // K-step (16 key rows of V)
-            const uint32_t pcol = pp * CP + c * (CW / 2) + k2 * 8;
-            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
-            if (elect_one()) {
+            for (int k2 = k_lo; k2 < k_hi; ++k2) {
+              const int kk = pp * (CP / 16) + k2;  // K-step (16 key rows of V)
+              const uint32_t pcol = pp * CP + k2 * 8;
+              const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
               if constexpr (PAIR == 2)
-                mma_ts_pair(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, first ? 0u : 1u);
+                mma_ts_pair(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, acc ? 1u : 0u);
               else
-                mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, first ? 0u : 1u);
+                mma_ts(tbase + C::kOBase + t * D, tbase + C::s_off(t, b) + pcol, db, kIdescPV, acc ? 1u : 0u);
+              acc = true;
             }
-            __syncwarp();
-            first = false;
           }
         }
+        __syncwarp();
+        first = false;
       };
       uint32_t o_init = 0, p_ph = 0;  // p_ph bit t*SB+b: p_full[t][b] phase (visited blocks only)
       auto issue_s_tile = [&](int g, int t, int st) {
@@ -628,6 +724,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         const bool signal_pv = SB == 2 && main_blk && pos + 1 < N &&
                                (all_exact(MODE) || sched_is_special(sched, sched_block(sched, pos + 1)));
         const int vs = main_blk ? acquire() : -1;
+        if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 17);
         int ks = -1;
         for (int t = 0; t < NQ; ++t) {
           if (main_blk) {
@@ -703,6 +800,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         stab[ti] = sched_block(sched, 0);
       }
       uint32_t over32 = 0, over16 = 0;
+      float argmax = -INFINITY;  // monitor: largest exp argument (log2 units)
       uint32_t pv_ph = 0;  // bit ti: pv_done phase (SB 2)
       auto tS = [&](int t, int b) { return tbase + C::s_off(t, b) + part * CP + lane_off; };
       auto tO = [&](int t) { return tbase + C::kOBase + t * D + part * OP + lane_off; };
@@ -769,6 +867,20 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
           m2[ti] = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + head_of(unit, tile0 + ti)) * a.Tr + unit.qt] * cs;
       }
 
+      // monitor: the m-init seed and the exact row max over every visited block (calibration
+      // gap, src/vfa.py:129-135); this thread's part of the row until the epilogue combines it
+      float seed2[NT], emax[NT];
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti) {
+        seed2[ti] = m2[ti];
+        emax[ti] = -INFINITY;
+      }
+      float rbias[NT];
+#pragma unroll
+      for (int ti = 0; ti < NT; ++ti)
+        rbias[ti] = (a.row_bias != nullptr && live)
+                        ? a.row_bias[(static_cast<size_t>(unit.b) * a.Hq + head_of(unit, tile0 + ti)) * a.Lq + R]
+                        : 0.f;
       const float2 cs2 = make_float2(cs, cs);
       // block-class counts beyond the closed form (skip / elision / row-mask variants only)
       int n_skipped = 0, n_skipped_special = 0, n_elided = 0, n_rows_masked = 0;
@@ -792,6 +904,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
 #pragma unroll
             for (int e = 0; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
           }
+          // monitor only: the frozen block's part max for the exact global row max
+          if (MODE == kVFA && !special && a.monitor) emax[ti] = fmaxf(emax[ti], part_max<CP>(v) * cs);
           bool skipped = false;
           bool rescale = false;  // this block rescales O by f (exact update, not skipped / elided)
           float f = 1.0f;
@@ -802,6 +916,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
             //      decides without exchanging row maxima; the frozen max is not updated.
             const float pm = part_max<CP>(v);
             const float pm2 = pm * cs;
+            if (a.monitor) emax[ti] = fmaxf(emax[ti], pm2);
             const bool below = (pm2 - fmaxf(m2[ti], pm2) < a.log2_lambda) ||
                                (pm2 == -INFINITY && m2[ti] == -INFINITY && a.log2_lambda != -INFINITY) || !live;
             skipped = named_bar_and(1 + t, SPLIT * kBR, below);
@@ -811,6 +926,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
             //      src/vfa.py:202-208, src/sparse.py:296-300), then rescale
             const float mt = exchange_max(ti, t, part_max<CP>(v));
             const float mt2 = mt * cs;
+            if (a.monitor) emax[ti] = fmaxf(emax[ti], mt2);
             const float m2n = fmaxf(m2[ti], mt2);
             bool keep = true;  // rowskip: this row takes part in the update
             if (MODE == kBLR) {
@@ -890,16 +1006,38 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
           if (!skipped) {
             // P = exp2(S*c - m2) in CW-column chunks; each chunk is handed to the MMA warp as
             // soon as it is in TMEM (PV of chunk 0 overlaps the softmax of chunk 1)
-            const float nm = m2[ti] == -INFINITY ? 0.f : -m2[ti];
+            const float nm = (m2[ti] == -INFINITY ? 0.f : -m2[ti]) + rbias[ti];
             const float2 nmu2 = make_float2(nm, nm);
             float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            if constexpr (C::kS1Split) {
+              // 32-column sub-chunks; hand-off after 96 columns (PV K-steps 0-5) and after 128
+#pragma unroll
+              for (int sc = 0; sc < 4; ++sc) {
+                uint32_t u[16];
+                constexpr int kP1 = VFA_POLY_S1;
+                if (a.monitor)
+                  p_chunk<32, true, 0, kLate>(v + sc * 32, cs2, nmu2, u, acc, over32, over16, argmax);
+                else if (sc == 1 || sc == 2)
+                  p_chunk<32, false, kP1, kLate>(v + sc * 32, cs2, nmu2, u, acc, over32, over16, argmax);
+                else
+                  p_chunk<32, false, 0, kLate>(v + sc * 32, cs2, nmu2, u, acc, over32, over16, argmax);
+                tmem_st16(tS(t, b) + sc * 16, u);
+                if (!defer && (sc == 2 || sc == 3)) {
+                  tmem_wait_st();
+                  tc_fence_before();
+                  __syncwarp();
+                  const int c = sc == 2 ? 0 : 1;
+                  if (lane == 0) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && (warp & 3) == 0 && part == 0 && c == 0);
+                }
+              }
+            } else {
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
               uint32_t u[CW / 2];
               if (a.monitor)
-                p_chunk<CW, true, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
+                p_chunk<CW, true, kPoly, kLate>(v + c * CW, cs2, nmu2, u, acc, over32, over16, argmax);
               else
-                p_chunk<CW, false, kPoly>(v + c * CW, cs2, nmu2, u, acc, over32, over16);
+                p_chunk<CW, false, kPoly, kLate>(v + c * CW, cs2, nmu2, u, acc, over32, over16, argmax);
               if constexpr (CW == 64) tmem_st32(tS(t, b) + c * 32, u);
               else if constexpr (CW == 32) tmem_st16(tS(t, b) + c * 16, u);
               else tmem_st8(tS(t, b) + c * 8, u);
@@ -907,9 +1045,11 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && warp == 0 && c == 0);
+                if (lane == 0) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && (warp & 3) == 0 && part == 0 && c == 0);
               }
             }
+            }
+            if constexpr (kLate) late_rowsum<NCH * CW>(v, acc);
             l[ti] = __fadd_rn(l[ti], __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
           }
           if (defer) {
@@ -935,7 +1075,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
             tc_fence_before();
             __syncwarp();
             if (lane == 0)
-              for (int c = 0; c < NCH; ++c) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && warp == 0 && c == 0);
+              for (int c = 0; c < NCH; ++c) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && (warp & 3) == 0 && part == 0 && c == 0);
           }
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
           if (r == 0 && part == 0 && pos == N - 1 && t == NQ - 1) VFA_TRACE_UNIT(a, 2);
@@ -951,6 +1091,27 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
       for (int ti = 0; ti < NT; ++ti) {
         const int t = tile0 + ti;
         const int h = head_of(unit, t);
+        if (a.monitor && a.stats && (MODE == kVFA || MODE == kVSA) && a.use_m_init) {
+          // OverflowMonitor.record_gap (src/vfa.py:129-135): m seed - exact global row max
+          const float ex = exchange_max(ti, t, emax[ti]);
+          if (part == 0) {
+            const float gap = seed2[ti] - ex;
+            const unsigned gmax = __reduce_max_sync(0xffffffffu, live ? float_key(gap) : 0u);
+            const unsigned gneg = __reduce_max_sync(0xffffffffu, live ? float_key(-gap) : 0u);
+            const unsigned below = __popc(__ballot_sync(0xffffffffu, live && gap < 0.f));
+            const unsigned rows = __popc(__ballot_sync(0xffffffffu, live));
+            float gsum = live ? gap : 0.f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+            if (lane == 0 && rows) {
+              atomicMax(&a.stats[VFA_STAT_GAP_MAX], static_cast<unsigned long long>(gmax));
+              atomicMax(&a.stats[VFA_STAT_GAP_NEG_MIN], static_cast<unsigned long long>(gneg));
+              atomicAdd(reinterpret_cast<double*>(&a.stats[VFA_STAT_GAP_SUM]), static_cast<double>(gsum));
+              atomicAdd(&a.stats[VFA_STAT_GAP_BELOW], static_cast<unsigned long long>(below));
+              atomicAdd(&a.stats[VFA_STAT_GAP_ROWS], static_cast<unsigned long long>(rows));
+            }
+          }
+        }
         float lsum = l[ti];
         if constexpr (SPLIT > 1) {
           ctl->xl[t][part][r] = l[ti];
@@ -986,7 +1147,10 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
         const unsigned srow = static_cast<unsigned>(lrow + a.row_base);  // whole-problem row for the status
         finite = finite || !live;
-        if (part == 0 && live && a.lse) a.lse[lrow] = (m2[ti] + __log2f(lsum)) * kLn2;
+        // (a row whose fp32 normalizer underflowed, l == 0 with a finite max, reports that max
+        // instead, for the host's rebase, src/core.py:101-109 / vfa_fwd_rebased)
+        if (part == 0 && live && a.lse)
+          a.lse[lrow] = (lsum == 0.f && m2[ti] != -INFINITY) ? m2[ti] * kLn2 : (m2[ti] - rbias[ti] + __log2f(lsum)) * kLn2;
         if (part == 0 && live && a.stab) a.stab[lrow] = stab[ti];
         if (a.status) {
           if (part == 0 && live && lsum == 0.f) {
@@ -1011,9 +1175,13 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
       }
       if (any_nonfinite) atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
       if (a.stats) {
-        if (a.monitor && live) {
-          atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
-          atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
+        if (a.monitor) {
+          if (live) {
+            atomicAdd(&a.stats[VFA_STAT_OVER_F32], static_cast<unsigned long long>(over32));
+            atomicAdd(&a.stats[VFA_STAT_OVER_F16], static_cast<unsigned long long>(over16));
+          }
+          const unsigned km = __reduce_max_sync(0xffffffffu, (live && argmax > -INFINITY) ? float_key(argmax) : 0u);
+          if (lane == 0 && km) atomicMax(&a.stats[VFA_STAT_EXP_ARG_MAX], static_cast<unsigned long long>(km));
         }
         if (MODE == kBLR && part == 0) {
           const unsigned masked = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_rows_masked));

@@ -1,6 +1,6 @@
 """A/B timing of library builds (tuning experiments; not bench values).
 
-    python scripts/ab.py [--variant vfa] [--steps 20] NAME=path/to/lib.so [NAME=...]
+    python scripts/ab.py [--variant vfa] [--steps 20] NAME=path/to/lib.so[@SPLIT] [NAME=...]
 Loads every build into one process and times them interleaved step by step on the C2 problem
 (same inputs, same clock / power state), so small differences are attributable to the code.
 Also checks every build's output is bitwise identical to the first one's where expected.
@@ -32,11 +32,15 @@ flops = causal_flops(cfg["B"], cfg["Hq"], cfg["L"], cfg["d"])
 runners = {}
 for spec in a.libs:
     name, path = spec.split("=", 1)
+    split = a.split
+    if "@" in path:
+        path, split = path.split("@")
+        split = int(split)
     lib = _lib.bind(os.path.abspath(path))
     for pair in ((1, 2) if a.pair else (0,)):
         runners[name + ("" if pair == 0 else f"/pair{pair}")] = Runner(
             q, k, v, a.variant, lam=1e-2 if a.variant == "vsa" else None, k_block=a.k_block, lib=lib, cta_pair=pair)
-        runners[name + ("" if pair == 0 else f"/pair{pair}")].p.softmax_split = a.split
+        runners[name + ("" if pair == 0 else f"/pair{pair}")].p.softmax_split = split
 sh = torch.cuda.current_stream().cuda_stream
 for r in runners.values():
     for _ in range(3):

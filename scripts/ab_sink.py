@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from bench import CONFIGS, Runner, causal_flops, make_inputs, time_interleaved  # noqa: E402
 from paper_2604_12798_b200 import _lib  # noqa: E402
-from scripts.sweeps import planted_sink  # noqa: E402
+from bench import planted_sink  # noqa: E402
 
 cfg = dict(CONFIGS["c2"])
 dev = torch.device("cuda", 0)

@@ -20,6 +20,7 @@ ap.add_argument("--head-dim", type=int, default=128)
 ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--n-local", type=int, default=1)
 ap.add_argument("--pair", type=int, default=0)
+ap.add_argument("--split", type=int, default=0, help="softmax_split (0: per-variant default)")
 ap.add_argument("--lib", default=None, help="experiment build (libvfa_b200_<name>.so) instead of the product library")
 ap.add_argument("--stats-out", default=None, help="write the pass's block-class counts here (JSON)")
 a = ap.parse_args()
@@ -33,6 +34,7 @@ if a.lib:
     lib = _lib.bind(os.path.abspath(a.lib))
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block,
            n_local=a.n_local, cta_pair=a.pair, lib=lib)
+r.p.softmax_split = a.split
 sh = torch.cuda.current_stream().cuda_stream
 for _ in range(a.iters):
     r.krepr(sh)

@@ -26,19 +26,21 @@ ap.add_argument("--n-local", type=int, default=1)
 ap.add_argument("--sink", type=float, default=0.0, help="planted-sink boost (C3 data); 0 = Gaussian")
 ap.add_argument("--lam", type=float, default=1e-2)
 ap.add_argument("--pair", type=int, default=0, help="cta_pair (2 = CTA pairs)")
+ap.add_argument("--split", type=int, default=0, help="softmax_split (0: per-variant default)")
 a = ap.parse_args()
 cfg = CONFIGS["c2"]
 dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
 if a.sink:
-    from scripts.sweeps import planted_sink
+    from bench import planted_sink
     planted_sink(q, k, a.sink, a.k_block)
 r = Runner(q, k, v, a.variant, lam=a.lam if a.variant == "vsa" else None, k_block=a.k_block, n_local=a.n_local,
            cta_pair=a.pair)
+r.p.softmax_split = a.split
 T = cfg["L"] // a.k_block
 # CTAs: one per unit (two heads); CTA pairs cover four heads per cluster when the group allows
 units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
-buf = torch.zeros(T * 16 + units * 4, dtype=torch.int64, device=dev)
+buf = torch.zeros(T * 20 + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)
 r.attn(sh)  # warm-up
@@ -48,7 +50,7 @@ r.attn(sh)
 torch.cuda.synchronize()
 r.lib.vfa_debug_trace(None)
 allbuf = buf.cpu().numpy()
-ut = allbuf[T * 16:].reshape(units, 4).astype(np.float64)
+ut = allbuf[T * 20:].reshape(units, 4).astype(np.float64)
 ok = (ut > 0).all(axis=1)
 ut = ut[ok]
 dur = ut[:, 3] - ut[:, 0]
@@ -56,7 +58,7 @@ pro = ut[:, 1] - ut[:, 0]
 epi = ut[:, 3] - ut[:, 2]
 print(f"units {ok.sum()}: mean cycles {dur.mean():.0f}; prologue (entry -> first S) {pro.mean():.0f} "
       f"({pro.sum() / dur.sum():.1%}), epilogue (last P -> exit) {epi.mean():.0f} ({epi.sum() / dur.sum():.1%})")
-tr = allbuf[: T * 16].reshape(T, 16).astype(np.float64)
+tr = allbuf[: T * 20].reshape(T, 20).astype(np.float64)
 n = int((tr[:, 1] > 0).sum())
 tr = tr[:n]
 t0 = tr[tr > 0].min()
@@ -78,6 +80,12 @@ print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mm
       " mma0 lastP, mma0 PVdone, mma1 lastP, mma1 PVdone, K acq, sm0 enter, sm1 enter]")
 for i in range(20, min(26, n)):
     print(" ", np.round(tr[i, :15]).astype(int).tolist())
+print("producer / V: [V(g) TMA issued, K(g+1) TMA issued, MMA acquired V(g)]")
+for i in range(20, min(26, n)):
+    print(" ", np.round(tr[i, 15:18]).astype(int).tolist())
+sl = slice(4, n - 4)
+print(f" V TMA issue -> MMA acquires V: median {np.nanmedian((tr[:, 17] - tr[:, 15])[sl]):.0f}; "
+      f"K(g+1) TMA issue -> K acquired (next block's slot 12): {np.nanmedian((tr[1:, 12] - tr[:-1, 16])[sl]):.0f}")
 for t in (0, 1):
     sl = slice(4, n - 4)
     first, last, pvd, qk = tr[:, 4 + 2 * t], tr[:, 8 + 2 * t], tr[:, 9 + 2 * t], tr[:, 5 + 2 * t]

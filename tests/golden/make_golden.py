@@ -93,23 +93,24 @@ def run_case(name, spec, data, causal, variant, **kw):
         if variant == "fa":
             out, counters, trace = vfa_lab.fa_forward(p)
         elif variant == "vfa":
-            out, counters, trace, mon = vfa_lab.vfa_forward(p, **kw)
+            # monitor=True: the calibration gap is recorded too (src/vfa.py:217-221)
+            out, counters, trace, mon = vfa_lab.vfa_forward(p, monitor=True, **kw)
         elif variant == "vsa":
             lam = kw.pop("lam")
-            out, counters, stats, mon = vfa_lab.vsa_forward(p, SkipConfig(lam=lam), **kw)
-            rec["lam"] = lam
+            rec["lam"] = lam  # (recorded before the call: an error case keeps its parameters)
+            out, counters, stats, mon = vfa_lab.vsa_forward(p, SkipConfig(lam=lam), monitor=True, **kw)
         elif variant == "blasst":
             lam, order = kw.pop("lam"), kw.pop("order", "sequential")
-            out, counters, stats = vfa_lab.blasst_forward(p, SkipConfig(lam=lam), order=order)
             rec["lam"], rec["order"] = lam, order
+            out, counters, stats = vfa_lab.blasst_forward(p, SkipConfig(lam=lam), order=order)
         elif variant == "blasst_fa4":
             lam, tau = kw.pop("lam"), kw.pop("tau")
-            out, counters, stats = vfa_lab.blasst_fa4_forward(p, SkipConfig(lam=lam, tau=tau))
             rec["lam"], rec["tau"] = lam, tau
+            out, counters, stats = vfa_lab.blasst_fa4_forward(p, SkipConfig(lam=lam, tau=tau))
         elif variant == "blasst_rowskip":
             lam = kw.pop("lam")
-            out, counters, stats = vfa_lab.blasst_rowskip_forward(p, SkipConfig(lam=lam, granularity="row"))
             rec["lam"] = lam
+            out, counters, stats = vfa_lab.blasst_rowskip_forward(p, SkipConfig(lam=lam, granularity="row"))
         else:
             raise ValueError(variant)
     except (vfa_lab.FullyMaskedRowError, vfa_lab.NormalizerUnderflowError) as e:
@@ -147,6 +148,9 @@ def run_case(name, spec, data, causal, variant, **kw):
         rec["mon.count_over_f16"] = mon.count_over_f16
         rec["mon.count_over_f32"] = mon.count_over_f32
         rec["mon.exp_arg_max"] = mon.exp_arg_max
+        if mon.calibration_gap is not None:
+            for key, val in mon.calibration_gap.items():
+                rec[f"mon.gap.{key}"] = val
     rec["error"] = err
     return arrays, rec
 
@@ -199,6 +203,20 @@ def main():
     v = np.ones((128, 64))
     s = BlockSpec(128, 128, 64, 128, 128)
     cases.append(("vfa_underflow_kmax", s, (q, k, v), False, "vfa", dict(kind="k_max")))
+
+    # fp32 underflow window: k_absmax_unsigned seeds 100 nats above every score (q . k = 0 on
+    # sign-balanced keys, q . |k| = 64 * 12.5 at scale 1/8). float64 normalizes (e^-100 is
+    # representable); fp32 exp2 flushes to zero below e^-87.3, so the kernel must rebase
+    q = np.ones((256, 64))
+    k = np.full((256, 64), 12.5); k[:, 32:] = -12.5
+    k[1::2] *= -1.0
+    v = gen_gaussian(BlockSpec(256, 256, 64, 128, 128), 20)[2]
+    s = BlockSpec(256, 256, 64, 128, 128)
+    cases.append(("vfa_fp32_underflow_window", s, (q, k, v), True, "vfa", dict(kind="k_absmax_unsigned")))
+    cases.append(("vsa_fp32_underflow_window", s, (q, k, v), True, "vsa", dict(kind="k_absmax_unsigned", lam=1e-3)))
+    # beyond float64's range (seed 800 nats above every score): the reference raises too
+    k2 = k * 8.0
+    cases.append(("vfa_f64_underflow", s, (q, k2, v), True, "vfa", dict(kind="k_absmax_unsigned")))
 
     # BLASST family (src/sparse.py:112-253), SURVEY.md §8f row 1
     s = BlockSpec(1024, 1024, 64, 128, 128)

@@ -62,6 +62,7 @@ def _params(**kw):
     ("variant", 7, 2), ("kind", 9, 2), ("qkind", 4, 2), ("q_block", 48, 2), ("k_block", 96, 2),
     ("head_dim", 96, 2), ("seq_q", 1000, 3), ("seq_k", 1000, 3), ("heads_q", 3, 3), ("tc1", 99, 2),
     ("n_sink", -1, 2), ("tau", -1.0, 2), ("softmax_split", 3, 2), ("variant", 6, 2),
+    ("scale", -0.125, 2), ("scale", float("nan"), 2), ("scale", float("inf"), 2),
 ])
 def test_check_params_codes(lib, field, value, code):
     assert lib.vfa_check_params(ctypes.byref(_params())) == 0
@@ -157,6 +158,51 @@ def test_api_validation_without_gpu():
         AttentionProblem(z, np.zeros((256, 32)), np.zeros((256, 32)))
     with pytest.raises(ValueError):
         AttentionProblem(z, z, z, blocks=BlockSpec(512, 512, 64, 128, 128))
+
+
+def test_tensor_validation_without_gpu():
+    # shape mismatches must raise ValueError before any pointer crosses the C ABI (the C side
+    # takes batch / head_dim from q and the key length from k)
+    import torch
+    from paper_2604_12798_b200 import attention_forward_host
+    from paper_2604_12798_b200.api import _check_outputs, _params
+    bf = torch.bfloat16
+    q = torch.zeros(1, 4, 256, 64, dtype=bf)
+    k = torch.zeros(1, 2, 256, 64, dtype=bf)
+    for kk, vv, msg in ((k, torch.zeros(1, 2, 128, 64, dtype=bf), "same shape"),
+                        (torch.zeros(2, 2, 256, 64, dtype=bf),) * 2 + ("batch",),
+                        (torch.zeros(1, 2, 256, 32, dtype=bf),) * 2 + ("head dimension",),
+                        (torch.zeros(1, 3, 256, 64, dtype=bf),) * 2 + ("multiple",)):
+        with pytest.raises(ValueError, match=msg):
+            attention_forward_host(q, kk, vv, variant="vfa", causal=True)
+    with pytest.raises(ValueError, match="out must have"):
+        _check_outputs(q, torch.zeros(1, 4, 128, 64, dtype=bf), torch.zeros(1, 4, 256), q.device)
+    with pytest.raises(ValueError, match="lse"):
+        _check_outputs(q, torch.zeros_like(q), torch.zeros(1, 4, 256, dtype=torch.float64), q.device)
+    _check_outputs(q, torch.zeros_like(q), torch.zeros(1, 4, 256), q.device)
+    kw = dict(variant="vfa", causal=True, q_block=128, k_block=128, kind="sabsmax", qkind="row_wise",
+              reorder=True, use_m_init=True, tc1=None, n_sink=1, n_local=1, lam=None, monitor=False)
+    for bad in (0.0, -0.5, float("nan")):  # an explicit scale is never silently replaced
+        with pytest.raises(ValueError, match="scale"):
+            _params(q, k, k, q, scale=bad, **kw)
+    assert _params(q, k, k, q, scale=None, **kw).scale == 0.0
+    assert _params(q, k, k, q, scale=0.3, **kw).scale == 0.3
+
+
+def test_stat_float_keys_roundtrip():
+    import struct
+    from paper_2604_12798_b200 import _lib
+
+    def key(f):  # the kernel's float_key
+        u = struct.unpack("<I", struct.pack("<f", f))[0]
+        return (~u & 0xFFFFFFFF) if u & 0x80000000 else (u | 0x80000000)
+
+    vals = [-1e30, -100.0, -1.5, -0.0, 0.0, 1e-30, 2.5, 127.9, 3e38]
+    keys = [key(v) for v in vals]
+    assert keys == sorted(keys)  # order preserving
+    for v in vals:
+        assert _lib.key_to_float(key(v)) == np.float32(v)
+    assert np.isnan(_lib.key_to_float(0))
 
 
 def test_entry_points_fail_loudly_without_library(monkeypatch, tmp_path):

@@ -28,7 +28,7 @@ def _kw(m):
 @pytest.mark.parametrize("name", case_names())
 def test_oracle_bitwise_equals_reference(name):
     m, q, k, v, out32, lse = case(name)
-    r = vo.forward_head(q, k, v, **_kw(m))
+    r = vo.forward_head(q, k, v, monitor=True, **_kw(m))
     if m["error"]:
         kind, row = m["error"].split(":")
         assert r.error is not None
@@ -55,6 +55,12 @@ def test_oracle_bitwise_equals_reference(name):
     if "mon.count_over_f32" in m:
         assert r.monitor.count_over_f32 == m["mon.count_over_f32"]
         assert r.monitor.count_over_f16 == m["mon.count_over_f16"]
+        assert r.monitor.exp_arg_max == m["mon.exp_arg_max"]
+    if "mon.gap.min" in m:  # OverflowMonitor.record_gap (src/vfa.py:129-135), bit-for-bit
+        for key in ("min", "max", "mean", "frac_below"):
+            assert r.monitor.calibration_gap[key] == m[f"mon.gap.{key}"], key
+    else:
+        assert r.monitor.calibration_gap is None or m["variant"] not in ("vfa", "vsa")
     stab = case_stab(name)
     if stab is not None:  # StateTrace -> stabilization_positions (src/analysis.py:39-78)
         assert np.array_equal(r.stab, stab)
