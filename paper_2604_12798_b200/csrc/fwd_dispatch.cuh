@@ -72,15 +72,24 @@ template <int D, int BC, int NQ, int MODE>
 int dispatch_split(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                    const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st) {
   const int split = p->softmax_split ? p->softmax_split : default_split(MODE);
-  if (split == 1) return launch_fwd<D, BC, NQ, MODE, 1>(p, mq, mk, mv, mr, args, st);
-  if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
-  return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
+  if constexpr (BC == 32) {
+    // 32-column S tiles: a part needs >= 16 columns, so 2 threads per row (two query tiles) or
+    // one thread per row; a requested split of 4 runs as 2
+    if (NQ == 2 && split != 1) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
+    return launch_fwd<D, BC, NQ, MODE, 1>(p, mq, mk, mv, mr, args, st);
+  } else {
+    if (split == 1) return launch_fwd<D, BC, NQ, MODE, 1>(p, mq, mk, mv, mr, args, st);
+    if (NQ == 2 && split == 2) return launch_fwd<D, BC, NQ, MODE, 2>(p, mq, mk, mv, mr, args, st);
+    return launch_fwd<D, BC, NQ, MODE, 4>(p, mq, mk, mv, mr, args, st);
+  }
 }
 
 template <int MODE>
 int launch_mode(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                 const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
-  const int D = static_cast<int>(p->head_dim), BC = p->k_block;
+  // head_dim 32 runs on the D = 64 kernels: TMA zero-fills columns 32..63 of every Q / K / V
+  // tile (exact: zero columns add nothing to QK^T, and PV's extra O columns are not stored)
+  const int D = p->head_dim <= 64 ? 64 : 128, BC = p->k_block;
   if (a.pair == 2) {  // CTA pairs (d = 128): K/V shared by M = 256 MMAs; 2 or 1 query tiles per CTA
     if (p->softmax_split == 1) {  // one thread per row
       if (a.heads_per_unit == 4) {
@@ -102,7 +111,9 @@ int launch_mode(const VfaParams* p, int nq, const CUtensorMap& mq, const CUtenso
                  : dispatch_split<DD, BB, 1, MODE>(p, mq, mk, mv, mr, a, st)
   if (D == 128 && BC == 128) VFA_NQ(128, 128);
   if (D == 128 && BC == 64) VFA_NQ(128, 64);
+  if (D == 128 && BC == 32) VFA_NQ(128, 32);
   if (D == 64 && BC == 128) VFA_NQ(64, 128);
+  if (D == 64 && BC == 32) VFA_NQ(64, 32);
   VFA_NQ(64, 64);
 #undef VFA_NQ
 }

@@ -82,8 +82,11 @@ int launch_block_repr(const void* x, int64_t B, int64_t H, const int64_t* stride
   if (D == 128)
     vfa::krepr_kernel<128><<<grid, 128, 0, st>>>(xp, strides[0], strides[1], strides[2], static_cast<int>(H), rows,
                                                 nblk, kind, op, jb0);
-  else
+  else if (D == 64)
     vfa::krepr_kernel<64><<<grid, 128, 0, st>>>(xp, strides[0], strides[1], strides[2], static_cast<int>(H), rows,
+                                               nblk, kind, op, jb0);
+  else
+    vfa::krepr_kernel<32><<<grid, 128, 0, st>>>(xp, strides[0], strides[1], strides[2], static_cast<int>(H), rows,
                                                nblk, kind, op, jb0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("krepr launch: ") + cudaGetErrorString(e));
@@ -150,8 +153,10 @@ int vfa_check_params(const VfaParams* p) {
   // (same schedule / statistics as the reference at that block size, 128 / q_block x the work)
   if (p->q_block != 128 && p->q_block != 64 && p->q_block != 32 && p->q_block != 16)
     return fail(VFA_ERR_CONFIG, "q_block must be 16, 32, 64 or 128 (tcgen05 M = 128 tiles)");
-  if (p->k_block != 64 && p->k_block != 128) return fail(VFA_ERR_CONFIG, "k_block must be 64 or 128");
-  if (p->head_dim != 64 && p->head_dim != 128) return fail(VFA_ERR_CONFIG, "head_dim must be 64 or 128");
+  if (p->k_block != 32 && p->k_block != 64 && p->k_block != 128)
+    return fail(VFA_ERR_CONFIG, "k_block must be 32, 64 or 128");
+  if (p->head_dim != 32 && p->head_dim != 64 && p->head_dim != 128)
+    return fail(VFA_ERR_CONFIG, "head_dim must be 32, 64 or 128");
   if (p->n_sink < 0 || p->n_local < 0) return fail(VFA_ERR_CONFIG, "n_sink and n_local must be >= 0");
   if (p->softmax_split != 0 && p->softmax_split != 1 && p->softmax_split != 2 && p->softmax_split != 4)
     return fail(VFA_ERR_CONFIG, "softmax_split must be 0 (auto), 1, 2 or 4");
@@ -250,7 +255,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   const int nq = (group % 2 == 0) ? 2 : 1;
   // CTA pairs (cta_pair = 2, or auto): the unit's two query heads on two SMs sharing each K/V
   // tile through M = 256 MMAs; needs an even GQA group and d = 128
-  const bool pair_ok = nq == 2 && D == 128 && p->q_block == 128;
+  const bool pair_ok = nq == 2 && D == 128 && p->q_block == 128 && BC >= 64;
   const int pair = (pair_ok && (p->cta_pair == 2 || (p->cta_pair == 0 && default_pair(p->variant)))) ? 2 : 1;
   // a pair holds two query tiles per CTA (four heads per cluster, the tiles ping-pong on the
   // tensor pipe as in the single-CTA kernel) when the GQA group allows, else one
@@ -291,8 +296,12 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
       vfa::minit_block_kernel<128><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
                                                          static_cast<int>(p->heads_kv), tr, p->q_block,
                                                          static_cast<int>(nrep), BC, tc, p->causal ? 1 : 0, m0);
-    else
+    else if (D == 64)
       vfa::minit_block_kernel<64><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
+                                                        static_cast<int>(p->heads_kv), tr, p->q_block,
+                                                        static_cast<int>(nrep), BC, tc, p->causal ? 1 : 0, m0);
+    else
+      vfa::minit_block_kernel<32><<<grid, 128, 0, st>>>(qr, kr, static_cast<int>(p->heads_q),
                                                         static_cast<int>(p->heads_kv), tr, p->q_block,
                                                         static_cast<int>(nrep), BC, tc, p->causal ? 1 : 0, m0);
     cudaError_t e = cudaGetLastError();
@@ -340,6 +349,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.stab = stab_block;
   a.m0_tile = m0_tile;
   a.row_bias = row_bias;
+  a.dv = D;  // head_dim 32 runs on a D = 64 kernel: only the first 32 O columns are stored
   a.row_base = row_base;
   a.trace = g_debug_trace;
 

@@ -83,6 +83,7 @@ struct FwdArgs {
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
   const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
+  int dv;                 // head_dim (<= the kernel's D; 32 on a D = 64 kernel, zero-padded tiles)
   const float* row_bias;  // per-row exponent rebase (log2 units, [B, Hq, Lq]) or null: P and l of the
                           // row are scaled by 2^bias (O = PV / l unchanged), LSE corrected; used to
                           // recover rows whose fp32 normalizer underflowed (vfa_fwd_rebased)
@@ -1133,12 +1134,14 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
           reg_fence16(v);
           uint32_t u[8];
 #pragma unroll
+          const bool col_ok = part * OP + c * 16 < a.dv;  // (head_dim 32: padded columns are not O)
+#pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
-            finite = finite && isfinite(o0) && isfinite(o1);
+            finite = finite && (!col_ok || (isfinite(o0) && isfinite(o1)));
             u[e >> 1] = pack_bf16x2(o0, o1);
           }
-          if (live) {  // (the TMEM load above is warp-collective: idle lanes take part)
+          if (live && col_ok) {  // (the TMEM load above is warp-collective: idle lanes take part)
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
             dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
             dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
@@ -1222,7 +1225,7 @@ template <int D>
 __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restrict__ k, long long sb, long long sh,
                                                     long long sr, int Hkv, int BC, int nblk, int kind,
                                                     __nv_bfloat16* __restrict__ out, int jb0 = 0) {
-  constexpr int CPL = D / 32;  // columns per lane (2 or 4)
+  constexpr int CPL = D / 32;  // columns per lane (1, 2 or 4)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int jb = jb0 + blockIdx.x * 4 + warp;
   const int kvh = blockIdx.y, b = blockIdx.z;
@@ -1245,10 +1248,12 @@ __global__ void __launch_bounds__(128) krepr_kernel(const __nv_bfloat16* __restr
       x[1] = __high2float(p0);
       x[2] = __low2float(p1);
       x[3] = __high2float(p1);
-    } else {
+    } else if constexpr (CPL == 2) {
       const __nv_bfloat162 p0 = *reinterpret_cast<const __nv_bfloat162*>(base + row * sr);
       x[0] = __low2float(p0);
       x[1] = __high2float(p0);
+    } else {
+      x[0] = __bfloat162float(base[row * sr]);
     }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {

@@ -250,6 +250,22 @@ def main():
     s = BlockSpec(1024, 1024, 64, 32, 64)
     cases.append(("blasst_fa4_sink_q32_lam1e-3_tau8", s, sink, True, "blasst_fa4", dict(lam=1e-3, tau=8.0)))
 
+    # head_dim 32 (the reference acceptance matrix runs d in {32, 64, 128}, tests/test_acceptance.py:37-61)
+    # and 32-row key blocks
+    s = BlockSpec(256, 256, 32, 64, 64)
+    cases.append(("vfa_d32_q64k64_causal", s, gen_gaussian(s, 21), True, "vfa", {}))
+    cases.append(("fa_d32_q64k64_noncausal", s, gen_gaussian(s, 22), False, "fa", {}))
+    s = BlockSpec(512, 512, 32, 128, 128)
+    cases.append(("vsa_d32_midpeak_lam1e-2", s, (lambda g: (g.q, g.k, g.v))(gen_structured(s, 23, "middle_peak", 8.0)),
+                  True, "vsa", dict(lam=1e-2)))
+    s = BlockSpec(512, 512, 128, 128, 32)
+    cases.append(("vfa_k32_d128_causal", s, gen_gaussian(s, 24), True, "vfa", {}))
+    cases.append(("fa_k32_d128_causal", s, gen_gaussian(s, 24), True, "fa", {}))
+    s = BlockSpec(512, 512, 64, 64, 32)
+    cases.append(("vfa_k32_d64_q64_noncausal_kmax", s, gen_gaussian(s, 25), False, "vfa", dict(kind="k_max")))
+    s = BlockSpec(1024, 1024, 64, 128, 32)
+    cases.append(("blasst_fa4_k32_sink_lam1e-3_tau2", s, sink, True, "blasst_fa4", dict(lam=1e-3, tau=2.0)))
+
     arrays, meta = {}, []
     for name, spec, data, causal, variant, kw in cases:
         a, rec = run_case(name, spec, data, causal, variant, **dict(kw))

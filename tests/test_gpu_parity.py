@@ -927,3 +927,60 @@ def test_c2_planted_sink_vsa_skip_counts():
     assert flips <= 2
     skipped = (trace == 2).sum() / max((trace > 0).sum(), 1)
     assert skipped > 0.9  # the planted sink makes almost every block skippable at lambda 1e-2
+
+
+# ----------------------------------------------------------------------------- head_dim 32 / k_block 32
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa", "blasst", "blasst_fa4", "blasst_rowskip"])
+@pytest.mark.parametrize("qb,kb", [(64, 64), (128, 128), (128, 32), (32, 32)])
+@pytest.mark.parametrize("causal", [True, False])
+def test_head_dim_32(variant, qb, kb, causal):
+    # d = 32 runs on the D = 64 kernels with TMA zero-filled columns (exact); the reference's
+    # acceptance matrix covers d in {32, 64, 128} (tests/test_acceptance.py:37-61)
+    B, Hq, Hkv, L, d = 1, 4, 2, 512, 32
+    q, k, v = _rand((B, Hq, L, d), 501), _rand((B, Hkv, L, d), 502), _rand((B, Hkv, L, d), 503)
+    kw = dict(variant=variant, causal=causal, q_block=qb, k_block=kb)
+    if variant not in ("fa", "vfa"):
+        kw["lam"] = 1e-3
+    if variant == "blasst_fa4":
+        kw["tau"] = 2.0
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    assert st["visited"] == ref_st["visited"]
+    if variant in ("fa", "vfa"):
+        assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
+
+
+@pytest.mark.parametrize("variant", ["fa", "vfa", "vsa", "blasst_rowskip"])
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("split", [0, 1, 2, 4])
+@pytest.mark.parametrize("hq", [2, 3])
+def test_k_block_32(variant, d, split, hq):
+    # 32-row key blocks: 2 threads per row (two query tiles) or one thread per row
+    L = 640
+    q, k, v = _rand((1, hq, L, d), 511), _rand((1, 1, L, d), 512), _rand((1, 1, L, d), 513)
+    kw = dict(variant=variant, causal=True, q_block=128, k_block=32, softmax_split=split)
+    if variant in ("vsa", "blasst_rowskip"):
+        kw["lam"] = 1e-3
+    out, lse, _, st = _run_gpu(q, k, v, **kw)
+    kw.pop("softmax_split")
+    ref_o, ref_lse, ref_st = vo.forward(_f64(q), _f64(k), _f64(v), **kw)
+    _compare(out, lse, ref_o, ref_lse, str(kw))
+    if variant in ("fa", "vfa"):
+        assert (st["special"], st["frozen"]) == (ref_st["special"], ref_st["frozen"])
+
+
+@pytest.mark.parametrize("n", [64, 256, 1024])
+@pytest.mark.parametrize("d", [32, 64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_reference_acceptance_matrix(n, d, causal):
+    # the reference's acceptance gate #1 problem matrix (tests/test_acceptance.py:37-61: blocks of
+    # 64, n in {64, 256, 1024}, d in {32, 64, 128}) through the drop-in entry points, against the
+    # exact oracle (float64 naive attention there; bf16 tolerance here)
+    from paper_2604_12798_b200 import AttentionProblem, BlockSpec, fa_forward, vfa_forward
+    q, k, v = _rand((n, d), 601 + n + d), _rand((n, d), 602 + n + d), _rand((n, d), 603 + n + d)
+    p = AttentionProblem(q, k, v, blocks=BlockSpec(n, n, d, 64, 64), causal=causal)
+    ref = vo.forward_head(_f64(q), _f64(k), _f64(v), variant="fa", causal=causal, q_block=64, k_block=64)
+    for fwd in (fa_forward, vfa_forward):
+        res = fwd(p)
+        _compare(res[0], res.lse, ref.out, ref.lse, f"{fwd.__name__} n={n} d={d} causal={causal}")
