@@ -157,6 +157,15 @@ VFA_API int vfa_fwd_rebased(const VfaParams* p, const void* q, const void* k, co
                             void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                             const float* row_bias, void* stream);
 
+/* vfa_fwd recording the reference's StateTrace (src/core.py:35-54, src/vfa.py:197,216): m_trace
+ * float32 [B, Hq, Lq, Lk/k_block] (device) receives, per query row and visit position (the
+ * schedule's order, vfa_schedule), the running max after that visit in natural units (entries
+ * past the row's visible blocks are left untouched); stab_block as in vfa_fwd (nullable).
+ * A debug output: one extra store per row and visit. */
+VFA_API int vfa_fwd_state_trace(const VfaParams* p, const void* q, const void* k, const void* v, void* o,
+                                float* lse, void* workspace, size_t workspace_bytes, long long* stats,
+                                unsigned int* status, int* stab_block, float* m_trace, void* stream);
+
 /* Bytes of device scratch vfa_fwd_host needs (up to four K/V group slots and eight query
  * sub-chunk slots), or 0 if the parameters or the chunking are invalid. */
 VFA_API size_t vfa_host_scratch_bytes(const VfaParams* p, int chunk_kv_heads, int chunk_q_heads);

@@ -36,7 +36,8 @@ STATUS_COUNT = 4
 # every symbol include/vfa_b200.h declares
 EXPORTS = ("vfa_check_params", "vfa_workspace_bytes", "vfa_fwd", "vfa_krepr", "vfa_schedule",
            "vfa_status_code", "vfa_last_error", "vfa_version", "vfa_debug_trace",
-           "vfa_host_scratch_bytes", "vfa_fwd_host", "vfa_krepr_range", "vfa_fwd_rebased")
+           "vfa_host_scratch_bytes", "vfa_fwd_host", "vfa_krepr_range", "vfa_fwd_rebased",
+           "vfa_fwd_state_trace")
 
 
 class VfaParams(ctypes.Structure):
@@ -80,6 +81,8 @@ def bind(path: str):
     lib.vfa_fwd.restype = ctypes.c_int
     lib.vfa_fwd_rebased.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp]
     lib.vfa_fwd_rebased.restype = ctypes.c_int
+    lib.vfa_fwd_state_trace.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, vp, vp, vp]
+    lib.vfa_fwd_state_trace.restype = ctypes.c_int
     lib.vfa_host_scratch_bytes.argtypes = [P, ctypes.c_int, ctypes.c_int]
     lib.vfa_host_scratch_bytes.restype = ctypes.c_size_t
     lib.vfa_fwd_host.argtypes = [P, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_int, ctypes.c_int,

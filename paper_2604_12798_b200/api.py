@@ -413,7 +413,8 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                       kind="sabsmax", qkind="row_wise", reorder=True, use_m_init=True, tc1=None,
                       n_sink=1, n_local=1, lam=None, tau=0.0, monitor=False, out=None, lse=None,
                       check=True, skip_trace=False, stream=None, workspace=None,
-                      krepr_precomputed=False, softmax_split=0, stab_trace=False, cta_pair=0):
+                      krepr_precomputed=False, softmax_split=0, stab_trace=False, cta_pair=0,
+                      state_trace=False):
     """Launch the B200 forward on bf16 CUDA tensors [B, Hq, Lq, d] / [B, Hkv, Lk, d].
 
     Returns (out, lse, info) with info = {"stats": int64 device tensor | dict,
@@ -429,6 +430,9 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     stab_trace: also return info["stab_block"], int32 [B, Hq, Lq]: per row the key block after
     whose visit the running max held its final value (the StateTrace stabilization position,
     src/analysis.py:39-78), see DeviceTrace / stabilization_positions.
+    state_trace: also return info["m_trace"], float32 [B, Hq, Lq, T_c]: the reference's StateTrace
+    snapshots (src/core.py:35-54) -- per row and visit position (schedule order) the running max
+    after the visit, natural units; NaN past the row's visible blocks (a debug output).
     cta_pair: 0 (default: off), 1 (one CTA per unit) or 2 (CTA pairs sharing each K/V tile
     through M = 256 tcgen05 MMAs: two query tiles per CTA for GQA groups divisible by 4, one for
     other even groups; d = 128, q_block = 128; falls back to single CTAs elsewhere).
@@ -442,8 +446,9 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
     if not tau >= 0:
         raise ValueError(f"tau must be >= 0, got {tau}")
     if all(isinstance(x, torch.Tensor) and x.device.type == "cpu" for x in (q, k, v)):
-        if skip_trace or stab_trace or krepr_precomputed or workspace is not None:
-            raise ValueError("skip_trace / stab_trace / krepr_precomputed / workspace need device-resident inputs")
+        if skip_trace or stab_trace or state_trace or krepr_precomputed or workspace is not None:
+            raise ValueError("skip_trace / stab_trace / state_trace / krepr_precomputed / workspace need "
+                             "device-resident inputs")
         return attention_forward_host(q, k, v, variant=variant, causal=causal, q_block=q_block,
                                       k_block=k_block, scale=scale, kind=kind, qkind=qkind,
                                       reorder=reorder, use_m_init=use_m_init, tc1=tc1, n_sink=n_sink,
@@ -490,14 +495,27 @@ def attention_forward(q, k, v, *, variant="vfa", causal=False, q_block=128, k_bl
                             dtype=torch.uint8, device=dev)
     stab = torch.empty(q.shape[:3], dtype=torch.int32, device=dev) if stab_trace else None
     st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    m_trace = None
     with torch.cuda.device(dev):
-        rc = lib.vfa_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                         lse.data_ptr(), ws.data_ptr(), ws_bytes, stats.data_ptr(), status.data_ptr(),
-                         trace.data_ptr() if trace is not None else None,
-                         stab.data_ptr() if stab is not None else None, ctypes.c_void_p(st))
+        if state_trace:
+            if skip_trace:
+                raise ValueError("state_trace and skip_trace are separate debug runs")
+            m_trace = torch.full((*q.shape[:3], k.shape[2] // k_block), float("nan"), dtype=torch.float32,
+                                 device=dev)
+            rc = lib.vfa_fwd_state_trace(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         out.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws_bytes,
+                                         stats.data_ptr(), status.data_ptr(),
+                                         stab.data_ptr() if stab is not None else None, m_trace.data_ptr(),
+                                         ctypes.c_void_p(st))
+        else:
+            rc = lib.vfa_fwd(ctypes.byref(p), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                             lse.data_ptr(), ws.data_ptr(), ws_bytes, stats.data_ptr(), status.data_ptr(),
+                             trace.data_ptr() if trace is not None else None,
+                             stab.data_ptr() if stab is not None else None, ctypes.c_void_p(st))
     if rc:
         _raise_for(rc)
-    info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws, "stab_block": stab}
+    info = {"stats": stats, "status": status, "skip_trace": trace, "workspace": ws, "stab_block": stab,
+            "m_trace": m_trace}
     if check:
         flags = int(status[_lib.STATUS_FLAGS].item())
         if flags & 2 and not flags & 1 and variant == "vfa" and use_m_init:
@@ -687,6 +705,9 @@ def _run(p: AttentionProblem, variant, **kw):
     st = stats_dict(info)
     if info.get("stab_block") is not None:
         st["stab_block"] = info["stab_block"].view(*p.q.shape[:-1]) if two_d else info["stab_block"]
+    if info.get("m_trace") is not None:
+        mt = info["m_trace"]
+        st["m_trace"] = mt.view(*p.q.shape[:-1], mt.shape[-1]) if two_d else mt
     if two_d:
         out, lse = out.view(*p.q.shape), lse.view(p.q.shape[0])
     return out, lse, st
@@ -706,12 +727,36 @@ class DeviceTrace:
     q_block: int
     positions: torch.Tensor
     local_blocks: list
+    # the reference's per-visit records when the run kept them (state_trace): snapshots
+    # [..., Nq, T_c] (running max after each visit position, NaN past the visible blocks) and the
+    # visit order of every query block (1-based key blocks, the device scheduler's order)
+    snapshots: torch.Tensor | None = None
+    orders: list | None = None
 
     @classmethod
-    def from_run(cls, p: "AttentionProblem", stab) -> "DeviceTrace":
+    def from_run(cls, p: "AttentionProblem", stab, snapshots=None, variant="vfa", reorder=True,
+                 n_sink=1, n_local=1) -> "DeviceTrace":
         b = p.blocks
         local = [min((i * b.q_block - 1) // b.k_block + 1, b.t_c) for i in range(1, b.t_r + 1)]
-        return cls(q_block=b.q_block, positions=stab, local_blocks=local)
+        orders = None
+        if snapshots is not None:
+            orders = [tile_schedule(i, b.q_block, b.k_block, b.t_c, p.causal, n_sink, n_local, reorder,
+                                    variant)[0] for i in range(1, b.t_r + 1)]
+        return cls(q_block=b.q_block, positions=stab, local_blocks=local, snapshots=snapshots, orders=orders)
+
+    @property
+    def records(self) -> list:
+        """Per query block, [(pos, block, m after the visit)] like the reference's
+        StateTrace.records (src/core.py:35-54); needs the snapshots."""
+        if self.snapshots is None:
+            raise ValueError("this trace has no per-visit snapshots (run with state_trace=True)")
+        snap = self.snapshots.reshape(-1, self.snapshots.shape[-2], self.snapshots.shape[-1])
+        snap = snap.double().cpu().numpy()
+        out = []
+        for bi, order in enumerate(self.orders):
+            rows = snap[:, bi * self.q_block:(bi + 1) * self.q_block]
+            out.append([(pos, j, rows[..., pos].reshape(-1)) for pos, j in enumerate(order)])
+        return out
 
 
 @dataclass
@@ -727,12 +772,35 @@ class StabilizationReport:
         return self.frac_sink + self.frac_local
 
 
-def stabilization_positions(trace: DeviceTrace) -> StabilizationReport:
+def stabilization_positions(trace: DeviceTrace, final_m=None) -> StabilizationReport:
     """Fractions of rows whose running max stabilised in the sink block, the local block or
-    elsewhere (src/analysis.py:39-78), from a DeviceTrace of one or more heads."""
-    pos = trace.positions.to(torch.int64).cpu().numpy()
-    nq = pos.shape[-1]
+    elsewhere (src/analysis.py:39-78), from a DeviceTrace of one or more heads.
+
+    final_m: as in the reference, check the trace against maxima obtained elsewhere: the
+    position of a row is the block of its first visit whose running-max snapshot equals
+    final_m exactly (ValueError if none does); needs a trace with snapshots. Without final_m
+    the kernel's own positions are used (= the snapshots against their last value)."""
     qb = trace.q_block
+    if final_m is None:
+        pos = trace.positions.to(torch.int64).cpu().numpy()
+    else:
+        if trace.snapshots is None:
+            raise ValueError("final_m needs a trace with per-visit snapshots (state_trace=True)")
+        snap = trace.snapshots.double().cpu().numpy()
+        fm = np.asarray(final_m.cpu() if isinstance(final_m, torch.Tensor) else final_m, dtype=np.float64)
+        fm = np.broadcast_to(fm.reshape(*fm.shape), snap.shape[:-1])
+        pos = np.zeros(snap.shape[:-1], dtype=np.int64)
+        settled = np.zeros(snap.shape[:-1], dtype=bool)
+        for bi, order in enumerate(trace.orders):
+            rs = slice(bi * qb, (bi + 1) * qb)
+            pos[..., rs] = order[-1]
+            for p_i, j in enumerate(order):
+                hit = ~settled[..., rs] & (snap[..., rs, p_i] == fm[..., rs])
+                pos[..., rs][hit] = j
+                settled[..., rs] |= hit
+        if not settled.all():
+            raise ValueError("running max never reached its final value")
+    nq = pos.shape[-1]
     local = np.repeat(np.asarray(trace.local_blocks, dtype=np.int64), qb)[:nq]
     sink = pos == 1
     loc = (pos == local) & (local != 1)
@@ -740,6 +808,17 @@ def stabilization_positions(trace: DeviceTrace) -> StabilizationReport:
     return StabilizationReport(positions=pos, frac_sink=float(sink.sum()) / n,
                                frac_local=float(loc.sum()) / n,
                                frac_other=float((~sink & (pos != local)).sum()) / n)
+
+
+# the reference-shaped fa_forward / vfa_forward keep the per-visit StateTrace snapshots (one
+# float per row and key block) up to this many entries, i.e. for the reference's desk-scale
+# problems; larger problems return the per-row stabilization positions only
+SNAPSHOT_LIMIT = 1 << 24
+
+
+def _keep_snapshots(p: AttentionProblem) -> bool:
+    heads = 1 if p.q.dim() == 2 else p.q.shape[0] * p.q.shape[1]
+    return heads * p.blocks.seq_len_q * p.blocks.t_c <= SNAPSHOT_LIMIT
 
 
 def _counters(st, p: AttentionProblem, variant: str) -> OpCounters:
@@ -768,8 +847,9 @@ def fa_forward(p: AttentionProblem, order_hook=None):
     """
     if order_hook is not None:
         raise ValueError("order_hook is not supported by the GPU fa_forward")
-    out, lse, st = _run(p, "fa", stab_trace=True)
-    return ForwardResult((out, _counters(st, p, "fa"), DeviceTrace.from_run(p, st["stab_block"])), lse, st)
+    out, lse, st = _run(p, "fa", stab_trace=True, state_trace=_keep_snapshots(p))
+    trace = DeviceTrace.from_run(p, st["stab_block"], st.get("m_trace"), "fa", False)
+    return ForwardResult((out, _counters(st, p, "fa"), trace), lse, st)
 
 
 def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True,
@@ -785,9 +865,11 @@ def vfa_forward(p: AttentionProblem, kind: str = "sabsmax", reorder: bool = True
         raise ValueError(f"unknown query representation {qkind!r}")
     if tc1 is not None and not (1 <= tc1 <= p.t_c):
         raise ValueError(f"tc1 must be in 1..{p.t_c}, got {tc1}")
+    snaps = _keep_snapshots(p)
     out, lse, st = _run(p, "vfa", kind=kind, reorder=reorder, use_m_init=use_m_init, qkind=qkind,
-                        tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor, stab_trace=True)
-    trace = DeviceTrace.from_run(p, st["stab_block"])
+                        tc1=tc1, n_sink=n_sink, n_local=n_local, monitor=monitor, stab_trace=True,
+                        state_trace=snaps)
+    trace = DeviceTrace.from_run(p, st["stab_block"], st.get("m_trace"), "vfa", reorder, n_sink, n_local)
     return ForwardResult((out, _counters(st, p, "vfa"), trace, _monitor(st, monitor)), lse, st)
 
 

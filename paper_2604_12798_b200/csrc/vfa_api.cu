@@ -136,7 +136,8 @@ void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                  unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
-                 long long row_base, void* seed_ws = nullptr, const float* row_bias = nullptr);
+                 long long row_base, void* seed_ws = nullptr, const float* row_bias = nullptr,
+                 float* m_trace = nullptr);
 
 }  // namespace
 
@@ -233,6 +234,18 @@ int vfa_fwd_rebased(const VfaParams* p, const void* q, const void* k, const void
                       static_cast<cudaStream_t>(stream), true, 0, nullptr, row_bias);
 }
 
+int vfa_fwd_state_trace(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
+                        void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
+                        int* stab_block, float* m_trace, void* stream) {
+  int rc = vfa_check_params(p);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !m_trace) return fail(VFA_ERR_DATA, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+    return fail(VFA_ERR_DATA, "tensors must be 16-byte aligned");
+  return forward_impl(p, q, k, v, o, lse, workspace, workspace_bytes, stats, status, nullptr, stab_block,
+                      static_cast<cudaStream_t>(stream), true, 0, nullptr, nullptr, m_trace);
+}
+
 }  // extern "C"
 
 namespace {
@@ -241,7 +254,7 @@ namespace {
 int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, long long* stats, unsigned int* status,
                  unsigned char* skip_trace, int* stab_block, cudaStream_t st, bool zero_counters,
-                 long long row_base, void* seed_ws, const float* row_bias) {
+                 long long row_base, void* seed_ws, const float* row_bias, float* m_trace) {
   int rc = VFA_OK;
   // m-initialisation belongs to the frozen-max variants; FA and the BLASST family start at -inf
   const bool minit = (p->variant == VFA_VARIANT_VFA || p->variant == VFA_VARIANT_VSA) && p->use_m_init;
@@ -252,7 +265,10 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   }
   const int D = static_cast<int>(p->head_dim), BC = p->k_block;
   const int group = static_cast<int>(p->heads_q / p->heads_kv);
-  const int nq = (group % 2 == 0) ? 2 : 1;
+#ifndef VFA_FORCE_NQ1
+#define VFA_FORCE_NQ1 0  // experiments: one query tile per CTA even for even GQA groups
+#endif
+  const int nq = (group % 2 == 0 && !VFA_FORCE_NQ1) ? 2 : 1;
   // CTA pairs (cta_pair = 2, or auto): the unit's two query heads on two SMs sharing each K/V
   // tile through M = 256 MMAs; needs an even GQA group and d = 128
   const bool pair_ok = nq == 2 && D == 128 && p->q_block == 128 && BC >= 64;
@@ -347,6 +363,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.status = status;
   a.skip_trace = skip_trace;
   a.stab = stab_block;
+  a.m_trace = m_trace;
   a.m0_tile = m0_tile;
   a.row_bias = row_bias;
   a.dv = D;  // head_dim 32 runs on a D = 64 kernel: only the first 32 O columns are stored

@@ -82,6 +82,8 @@ struct FwdArgs {
   unsigned int* status;
   unsigned char* skip_trace;
   int* stab;  // per row: key block (1-based) of the visit where the running max last rose
+  float* m_trace;  // StateTrace snapshots (src/core.py:35-54): per row and visit position, the running
+                   // max after the visit (natural units), [B, Hq, Lq, Tc]; or null
   const float* m0_tile;  // block-wise qkind m-init: raw max_j qrepr_i . krepr_j per query tile, or null
   int dv;                 // head_dim (<= the kernel's D; 32 on a D = 64 kernel, zero-padded tiles)
   const float* row_bias;  // per-row exponent rebase (log2 units, [B, Hq, Lq]) or null: P and l of the
@@ -92,6 +94,9 @@ struct FwdArgs {
   long long* trace;  // debug: per-visit clock64 events of CTA 0 (vfa_debug_trace), or null
 };
 
+#ifndef VFA_S2_ALL
+#define VFA_S2_ALL 0
+#endif
 #ifndef VFA_S1_SPLIT34
 #define VFA_S1_SPLIT34 1
 #endif
@@ -151,14 +156,17 @@ struct Cfg {
   static constexpr bool kS1Split = SPLIT == 1 && PAIR == 1 && kCP == 128 && VFA_S1_SPLIT34;
   static constexpr int kKS0 = kS1Split ? 6 : kCW / 16;
   static constexpr int kWarpsPerTile = SPLIT * 4;    // softmax warps covering one tile
-  static constexpr int kSoftmaxWarps = SPLIT == 1 ? 4 * NQ : 16;
+  // SPLIT 2 with VFA_S2_ALL (and two query tiles): 8 softmax warps, 2 threads per row, all of them
+  // serving both tiles in turn like SPLIT 4 (half the softmax warps per sub-partition)
+  static constexpr bool kAllTiles = SPLIT == 4 || (SPLIT == 2 && VFA_S2_ALL && NQ == 2);
+  static constexpr int kSoftmaxWarps = SPLIT == 1 ? 4 * NQ : (SPLIT == 2 && kAllTiles ? 8 : 16);
   static constexpr int kMmaWarp = kSoftmaxWarps;
   static constexpr int kLoadWarp = kSoftmaxWarps + 1;
   static constexpr int kThreads = (kSoftmaxWarps + 4) * 32;
   // setmaxnreg budgets. The CTA's register pool is what the launch allocated (threads x
   // compiled registers/thread, e.g. 640 x 96 = 61440); asking for more than the pool blocks
   // setmaxnreg.inc forever, so the host checks this budget before launching.
-  static constexpr int kRegsSoftmax = SPLIT == 1 ? VFA_REGS_SPLIT1 : 104;
+  static constexpr int kRegsSoftmax = (SPLIT == 1 || kSoftmaxWarps == 8) ? VFA_REGS_SPLIT1 : 104;
   static constexpr int kRegsOther = 56;
   static constexpr int kRegBudget = kSoftmaxWarps * 32 * kRegsSoftmax + (kThreads - kSoftmaxWarps * 32) * kRegsOther;
   static constexpr int kCtlBytes = 16384;
@@ -171,12 +179,17 @@ struct Cfg {
   // QK of block n+2 is then issued before the softmax of block n+1 starts, so the softmax
   // never waits on the PV -> QK latency of the previous block. Used for the all-exact modes
   // only: measured faster for FA at BC = 64, slower for VFA / VSA (profiles/ab_r01_sb.txt).
+  // One query tile per CTA (VFA_SB_NQ1 >= 3): as many S buffers as TMEM holds next to O, up to
+  // VFA_SB_NQ1 (3 at d = Bc = 128): QK^T then runs up to two blocks ahead of the softmax.
+  static constexpr int kSBNQ1 = (512 - D) / BC < VFA_SB_NQ1 ? (512 - D) / BC : VFA_SB_NQ1;
   static constexpr int kSB =
-      (NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && (all_exact(MODE) || (NQ == 1 && VFA_SB_NQ1))) ? 2 : 1;
+      (NQ == 1 && VFA_SB_NQ1 >= 3 && VFA_SB_MAX >= 2 && PAIR == 1)
+          ? kSBNQ1
+          : ((NQ * 2 * BC + NQ * D <= 512 && VFA_SB_MAX >= 2 && (all_exact(MODE) || (NQ == 1 && VFA_SB_NQ1))) ? 2 : 1);
   static __host__ __device__ constexpr uint32_t s_off(int t, int b) {
-    return static_cast<uint32_t>(kSB == 2 ? (t * 2 + b) * BC : t * BC);
+    return static_cast<uint32_t>((t * kSB + b) * BC);
   }
-  static constexpr int kOBase = kSB == 2 ? NQ * 2 * BC : NQ * BC;
+  static constexpr int kOBase = NQ * kSB * BC;
   static constexpr int kColsUsed0 = kOBase + NQ * D;
   // Q resident in TMEM (D/2 columns per tile, bf16 pairs) where it fits, for BC = 64: QK^T then
   // runs A-from-TMEM, reading only K from shared memory. With both operands in shared memory an
@@ -251,6 +264,23 @@ __device__ __forceinline__ int minit_chunks(const FwdArgs& a, const TileSchedule
   return (n + BC - 1) / BC;
 }
 
+
+#ifndef VFA_MMA_SPIN
+#define VFA_MMA_SPIN 0  // 1: the MMA issuer spins on test_wait instead of (suspending) try_wait
+#endif
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t parity) {
+  if constexpr (VFA_MMA_SPIN) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
+#ifndef VFA_POLY_SMSP0
+// exp2 pairs (of 8) on the FMA pipe for the softmax warps of sub-partition 0 only, which also hosts
+// the MMA issuer: fewer MUFU there leaves room in that sub-partition's MIO queue for the issuer's
+// tcgen05.mma / mbarrier instructions
+#define VFA_POLY_SMSP0 0
+#endif
+#ifndef VFA_SM_SPIN
+#define VFA_SM_SPIN 0  // 1: the softmax warps spin on test_wait for S
+#endif
 
 // tcgen05.commit from one elected lane of the (converged) MMA warp.
 __device__ __forceinline__ void commit_elect(uint64_t* bar) {
@@ -642,7 +672,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
       int stage = 0;
       uint32_t phase = 0;
       auto acquire = [&]() -> int {
-        mbar_wait(&ctl->kv_full[stage], phase);
+        mma_wait(&ctl->kv_full[stage], phase);
         tc_fence_after();
         int st = stage;
         if (++stage == NS) {
@@ -722,7 +752,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
         const int b = g % SB;
         const bool next_s = g + SB < G;
         // SB 2: the softmax of the next exact-update block rescales O, so it waits for this PV
-        const bool signal_pv = SB == 2 && main_blk && pos + 1 < N &&
+        const bool signal_pv = SB >= 2 && main_blk && pos + 1 < N &&
                                (all_exact(MODE) || sched_is_special(sched, sched_block(sched, pos + 1)));
         const int vs = main_blk ? acquire() : -1;
         if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 17);
@@ -736,7 +766,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
               if constexpr (PAIR == 2 && skips(MODE))  // pairs with the follower's release
                 mbar_wait_cluster(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
               else
-                mbar_wait(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
+                mma_wait(&ctl->p_full[t][b][c], (p_ph >> (t * SB + b)) & 1u);
               tc_fence_after();
               if (c == 0) {
                 if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
@@ -775,9 +805,9 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
     //               key block): half the per-thread work per tile-block, one shared issue stream;
     //   SPLIT == 1: one warpgroup per tile, one thread per row (no row-max exchange).
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kRegsSoftmax));
-    constexpr int NT = (SPLIT == 4) ? NQ : 1;  // query tiles this thread serves
-    const int part = SPLIT == 4 ? (warp >> 2) : (SPLIT == 2 ? ((warp >> 2) & 1) : 0);
-    const int tile0 = SPLIT == 4 ? 0 : warp / (4 * SPLIT);
+    constexpr int NT = C::kAllTiles ? NQ : 1;  // query tiles this thread serves
+    const int part = C::kAllTiles ? (warp >> 2) : (SPLIT == 2 ? ((warp >> 2) & 1) : 0);
+    const int tile0 = C::kAllTiles ? 0 : warp / (4 * SPLIT);
     if (tile0 < NQ) {
       const int r = tid & 127;
       VFA_ROLE_SETUP();
@@ -818,7 +848,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
       };
       // sequence element g (m-init chunks, then visited blocks) lives in S buffer g % SB
       auto wait_s = [&](int t, int g) {
-        mbar_wait(&ctl->s_full[t][g % SB], (g / SB) & 1);
+        if constexpr (VFA_SM_SPIN) mbar_wait_spin(&ctl->s_full[t][g % SB], (g / SB) & 1);
+        else mbar_wait(&ctl->s_full[t][g % SB], (g / SB) & 1);
         tc_fence_after();
       };
       auto load_part = [&](int t, int b, float* v) {
@@ -988,7 +1019,7 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
           // SB 2: S(pos) was computed before PV(pos-1) was issued, so an exact block waits for
           // PV(pos-1) (pv_done, committed by the MMA warp ahead of every exact block) and hands
           // its P over only after the rescale.
-          const bool defer = SB == 2 && special && pos > 0;
+          const bool defer = SB >= 2 && special && pos > 0;
           if (SB == 1 && rescale) rescale_o();
           // ---- frozen blocks (src/vfa.py:209-215) skip all of the above: no rowmax, no rescale
           if (r == 0 && part == 0) {
@@ -1037,6 +1068,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
               uint32_t u[CW / 2];
               if (a.monitor)
                 p_chunk<CW, true, kPoly, kLate>(v + c * CW, cs2, nmu2, u, acc, over32, over16, argmax);
+              else if (VFA_POLY_SMSP0 > 0 && (warp & 3) == 0)  // the MMA issuer's sub-partition
+                p_chunk<CW, false, VFA_POLY_SMSP0, kLate>(v + c * CW, cs2, nmu2, u, acc, over32, over16, argmax);
               else
                 p_chunk<CW, false, kPoly, kLate>(v + c * CW, cs2, nmu2, u, acc, over32, over16, argmax);
               if constexpr (CW == 64) tmem_st32(tS(t, b) + c * 32, u);
@@ -1078,6 +1111,8 @@ __global__ void __launch_bounds__(Cfg<D, BC, NQ, SPLIT, MODE, PAIR>::kThreads, 1
             if (lane == 0)
               for (int c = 0; c < NCH; ++c) arrive_mma(&ctl->p_full[t][b][c], skips(MODE) && (warp & 3) == 0 && part == 0 && c == 0);
           }
+          if (a.m_trace != nullptr && part == 0 && live)  // (debug output: one store per row and visit)
+            a.m_trace[((static_cast<size_t>(unit.b) * a.Hq + head_of(unit, t)) * a.Lq + R) * a.Tc + pos] = m2[ti] * kLn2;
           if (r == 0 && part == 0) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
           if (r == 0 && part == 0 && pos == N - 1 && t == NQ - 1) VFA_TRACE_UNIT(a, 2);
         }

@@ -984,3 +984,36 @@ def test_reference_acceptance_matrix(n, d, causal):
     for fwd in (fa_forward, vfa_forward):
         res = fwd(p)
         _compare(res[0], res.lse, ref.out, ref.lse, f"{fwd.__name__} n={n} d={d} causal={causal}")
+
+
+@pytest.mark.parametrize("variant", ["vfa", "fa"])
+def test_state_trace_snapshots_and_final_m(variant):
+    # the reference's StateTrace records (src/core.py:35-54) from the device: per visit the running
+    # max after the visit; stabilization_positions(trace, final_m) (src/analysis.py:39-78) on them
+    from paper_2604_12798_b200 import AttentionProblem, BlockSpec, fa_forward, stabilization_positions, vfa_forward
+    L, d = 1024, 64
+    q, k, v = _rand((L, d), 701), _rand((L, d), 702), _rand((L, d), 703)
+    p = AttentionProblem(q, k, v, blocks=BlockSpec(L, L, d, 128, 64), causal=True)
+    res = (vfa_forward(p, n_local=2) if variant == "vfa" else fa_forward(p))
+    trace = res[2]
+    assert trace.snapshots is not None and trace.snapshots.shape == (L, L // 64)
+    snap = trace.snapshots.double().cpu().numpy()
+    ref = vo.forward_head(_f64(q), _f64(k), _f64(v), variant=variant, causal=True, q_block=128, k_block=64,
+                          n_local=2 if variant == "vfa" else 1)
+    # records: block order = the reference schedule; the last snapshot is the final running max
+    tc = L // 64
+    for bi, recs in enumerate(trace.records):
+        i = bi + 1
+        vmax, local = vo.visible_key_blocks(i, 128, 64, tc, True), vo.local_key_block(i, 128, 64, tc)
+        order = vo.build_schedule(i, vmax, local, True, 1, 2)[0] if variant == "vfa" else tuple(range(1, vmax + 1))
+        assert tuple(j for _, j, _ in recs) == tuple(order)
+    final = np.array([snap[r, np.where(np.isfinite(snap[r]))[0][-1]] for r in range(L)])
+    if variant == "fa":  # the running max ends at the exact row max (src/reference.py:105-111)
+        exact = vo.exact_rowmax_global(_f64(q), _f64(k), 1.0 / np.sqrt(d), True)
+        assert np.abs(final - exact).max() <= 1e-3
+    rep0 = stabilization_positions(trace)
+    rep1 = stabilization_positions(trace, final_m=final)
+    assert np.array_equal(rep0.positions, rep1.positions)
+    assert (rep0.positions != ref.stab).mean() <= 0.01
+    with pytest.raises(ValueError):
+        stabilization_positions(trace, final_m=final + 1.0)
