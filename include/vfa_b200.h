@@ -207,9 +207,11 @@ VFA_API int vfa_status_code(const unsigned int* status_host);
 /* Message for the last non-zero return on this thread. */
 VFA_API const char* vfa_last_error(void);
 
-/* Debug only: when non-NULL, subsequent vfa_fwd calls record clock64() timestamps of the
- * first CTA into device_buffer (long long[Lk/k_block * 8]: per visited block, softmax tile
- * 0/1 "S ready"/"P done", MMA tile 0/1 "P observed"/"next QK issued"). NULL disables. */
+/* Debug only (trace builds, -DVFA_TRACE): when non-NULL, subsequent vfa_fwd calls record
+ * clock64() timestamps into device_buffer (long long[Tc * 32 + units * 4]: per visited block
+ * of the first CTA 32 event slots -- softmax tile 0/1 "S ready"/"P done", MMA tile 0/1
+ * "P observed"/"next QK issued", ... (scripts/trace_timeline.py) -- then per CTA its entry /
+ * first S / last P / exit). NULL disables. */
 VFA_API int vfa_debug_trace(long long* device_buffer);
 
 /* Library version string. */

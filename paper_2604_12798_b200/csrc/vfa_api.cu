@@ -115,6 +115,9 @@ size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+#ifndef VFA_WS_ENABLE
+#define VFA_WS_ENABLE 0  // 1: the warp-specialised kernel serves its shapes (in development)
+#endif
 #ifndef VFA_PAIR_NQ2
 #define VFA_PAIR_NQ2 1
 #endif
@@ -123,6 +126,14 @@ bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15)
 #ifndef VFA_PAIR_DEFAULT
 #define VFA_PAIR_DEFAULT 0
 #endif
+// Shapes the warp-specialised kernel (ws_kernel.cuh) serves when a CTA holds two query tiles:
+// d = 128, 128-row query / key blocks, default softmax layout, FA / VFA / VSA without the
+// monitor. (Debug outputs -- state trace, row rebase, timeline -- also route to vfa_fwd_kernel.)
+bool ws_eligible(const VfaParams* p) {
+  return VFA_WS_ENABLE && p->head_dim == 128 && p->k_block == 128 && p->q_block == 128 && p->softmax_split == 0 &&
+         !p->monitor && p->cta_pair != 2 && p->variant <= VFA_VARIANT_VSA;
+}
+
 bool default_pair(int variant) { return VFA_PAIR_DEFAULT != 0 && variant >= 0; }
 
 void reset_counters(long long* stats, unsigned int* status, cudaStream_t st) {
@@ -370,7 +381,9 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.row_base = row_base;
   a.trace = g_debug_trace;
 
-  (void)BC;
+  // the warp-specialised kernel serves the headline shape (default layout, no debug outputs)
+  if (ws_eligible(p) && nq == 2 && pair == 1 && !m_trace && !row_bias)
+    return vfa_host::launch_ws(p, mq, mk, mv, mr, a, st);
   static const vfa_host::LaunchFn kLaunch[] = {vfa_host::launch_fa,     vfa_host::launch_vfa,
                                                vfa_host::launch_vsa,    vfa_host::launch_blasst,
                                                vfa_host::launch_blasst_fa4, vfa_host::launch_blasst_rowskip};
@@ -571,7 +584,8 @@ int vfa_fwd_host(const VfaParams* p, const void* q_host, const void* k_host, con
     // computes bit-identically (an even head count, or VFA's 4-threads-per-row layout, which a
     // single-tile CTA also uses).
     const bool same_bits = (g.nqs / 2) % 2 == 0 ||
-                           (p->variant == VFA_VARIANT_VFA && (p->softmax_split == 0 || p->softmax_split == 4));
+                           (p->variant == VFA_VARIANT_VFA && (p->softmax_split == 4 ||
+                                                              (p->softmax_split == 0 && !ws_eligible(p))));
     const bool tail = (gi == g.groups - 1 || gi == 0) && g.ck == 1 && g.nqs >= 2 && g.nqs % 2 == 0 && g.groups > 1 && same_bits;
     const int64_t nq_g = tail ? g.nqs / 2 : g.nqs;
     VfaParams cpg = g.cp;

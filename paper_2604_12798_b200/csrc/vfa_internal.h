@@ -34,5 +34,9 @@ int launch_blasst_fa4(const VfaParams*, int, const CUtensorMap&, const CUtensorM
                       const CUtensorMap&, const vfa::FwdArgs&, cudaStream_t);
 int launch_blasst_rowskip(const VfaParams*, int, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                           const CUtensorMap&, const vfa::FwdArgs&, cudaStream_t);
+// Warp-specialised kernel (ws_kernel.cuh) for d = 128, k_block = q_block = 128, two query tiles
+// per CTA; variants FA / VFA / VSA. Defined in fwd_ws.cu.
+int launch_ws(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+              const CUtensorMap& mr, const vfa::FwdArgs& args, cudaStream_t st);
 
 }  // namespace vfa_host

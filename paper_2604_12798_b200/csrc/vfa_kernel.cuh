@@ -115,7 +115,7 @@ struct FwdArgs {
 
 // debug timeline slots per visited block (CTA 0 only, builds with -DVFA_TRACE): softmax t:
 // S ready, P done; MMA t: P observed, next QK issued
-constexpr int kTraceSlots = 20;
+constexpr int kTraceSlots = 32;
 #ifdef VFA_TRACE
 #define VFA_TRACE_EVENT(args, pos, slot)                                                     \
   do {                                                                                       \

@@ -1,0 +1,612 @@
+// B200 (sm_100a) warp-specialised attention forward for the headline shape: head_dim 128,
+// 128-key blocks, 128-row query blocks, two query heads of one GQA group per CTA.
+//
+// Same work unit, schedule, m-init prologue and per-block math as vfa_fwd_kernel
+// (vfa_kernel.cuh; reference map there), with the roles split so that no role sits on
+// another's critical path:
+//   warps 0-3   softmax of query tile 0, one thread per row (TMEM lane = row)
+//   warps 4-7   softmax of query tile 1
+//   warps 8-11  correction: rescales O in TMEM on exact-update blocks (src/core.py:91) while
+//               the softmax already computes the block's exponentials, and the epilogue
+//               (O / l, src/core.py:101-109) while the softmax publishes LSE / status
+//   warps 12-13 MMA issuers, one per query tile (converged warps, elect.sync); 12 allocates TMEM
+//   warp 14     TMA producer
+//   warp 15     idle (completes the last warpgroup)
+// TMEM (512 columns): S_t at t*128 (P_t as packed bf16 over its first 64 columns), O_t at
+// 256 + t*128. Per key block and tile the tensor pipe runs PV_t, QK_t(next); the two tiles'
+// chains interleave on the pipe, each tile's softmax runs under the other tile's MMAs.
+// Exponentials: exp2 on MUFU.EX2 for most element pairs and a degree-3 polynomial on the FMA
+// pipe for kWsEmu of every 8 pairs in the middle two 32-column chunks, so the XU (16 exp2 per
+// SM-cycle = exactly the tensor pipe's rate at d = 128) is not the bound. Row sums are taken
+// after the P hand-off (off the S -> P -> PV chain).
+#pragma once
+#include "vfa_kernel.cuh"
+
+namespace vfa {
+
+#ifndef VFA_WS_EMU
+#define VFA_WS_EMU 2  // element pairs (of 8) on the FMA-pipe exp2 in chunks 1 and 2
+#endif
+#ifndef VFA_WS_EMU_CHUNKS
+#define VFA_WS_EMU_CHUNKS 0x6  // bit c: chunk c (32 columns) uses the FMA-pipe exp2 for VFA_WS_EMU pairs
+#endif
+#ifndef VFA_WS_HANDOFF
+#define VFA_WS_HANDOFF 3  // 32-column chunks before the first P hand-off (PV K-steps 0 .. 2*HANDOFF-1)
+#endif
+#ifndef VFA_WS_ACQ_FENCE
+#define VFA_WS_ACQ_FENCE 1  // tcgen05 fence after the K/V full wait (experiments: 0)
+#endif
+#ifndef VFA_WS_TOKEN
+#define VFA_WS_TOKEN 1  // MMA issuers take turns (0: free-running, the tiles drift into phase)
+#endif
+#ifndef VFA_WS_REGS_SOFTMAX
+#define VFA_WS_REGS_SOFTMAX 184
+#endif
+#ifndef VFA_WS_REGS_CORR
+#define VFA_WS_REGS_CORR 80
+#endif
+#ifndef VFA_WS_REGS_OTHER
+#define VFA_WS_REGS_OTHER 64
+#endif
+
+struct WsCfg {
+  static constexpr int D = 128, BC = 128, NQ = 2;
+  static constexpr int kThreads = 512;
+  static constexpr int kCorrWarp0 = 8;
+  static constexpr int kMmaWarp = 12;   // and 13: one MMA issuer per query tile
+  static constexpr int kLoadWarp = 14;
+  static constexpr int kQBytes = kBR * D * 2;    // 32 KB
+  static constexpr int kKVBytes = BC * D * 2;    // 32 KB
+#ifndef VFA_WS_STAGES
+#define VFA_WS_STAGES 5
+#endif
+  // K/V ring: the MMA holds V(g) and K(g+1); the other stages are loads in flight, which must
+  // cover the L2 -> smem latency of a 32 KB tile under full load (~2 us measured, more than a
+  // block's period: 4 stages left the MMA waiting on V)
+  static constexpr int kStages = VFA_WS_STAGES;
+  static constexpr int kCtlBytes = 3072;  // control block first, tiles from the next 1 KB boundary
+  static constexpr int kSmem = kCtlBytes + NQ * kQBytes + kStages * kKVBytes;
+  static __device__ __forceinline__ uint32_t s_off(int t) { return static_cast<uint32_t>(t * 128); }
+  static __device__ __forceinline__ uint32_t o_off(int t) { return static_cast<uint32_t>(256 + t * 128); }
+  static_assert(kSmem <= kMaxSmem, "shared memory");
+  static_assert((2 * VFA_WS_REGS_SOFTMAX + VFA_WS_REGS_CORR + VFA_WS_REGS_OTHER) * 128 <= 65536, "register budget");
+};
+
+struct __align__(16) WsCtl {
+  uint64_t q_full[2];
+  uint64_t kv_full[WsCfg::kStages];
+  uint64_t kv_empty[WsCfg::kStages];
+  uint64_t s_full[2];     // MMA -> softmax t: S_t of sequence element g ready (parity g & 1)
+  uint64_t s_free[2];     // softmax t -> MMA: m-init chunk read, S_t may be overwritten
+  uint64_t p_full[2][2];  // softmax t -> MMA: P chunk c in TMEM (or the block skipped)
+  uint64_t o_ready[2];    // correction -> MMA: O_t rescaled for the current exact block
+  uint64_t o_final[2];    // MMA -> correction: last PV_t complete
+  uint64_t tok[2];        // MMA issuer 1-t -> issuer t: your turn to enqueue (keeps the tiles in anti-phase)
+  uint32_t tmem_base;
+  uint32_t skip[2];
+  float scale[2][kBR];    // softmax t -> correction: rescale factor of the current exact block
+  float fin_l[2][kBR];    // softmax t -> correction: final row sums
+};
+static_assert(sizeof(WsCtl) <= WsCfg::kCtlBytes, "control block");
+
+// named barriers (0 = __syncthreads): 1+t rescale hand-off, 3+t final sums (256 threads:
+// softmax t + correction), 5+t softmax t's CTA-wide votes (128 threads)
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(WsCfg::kThreads, 1)
+    vfa_ws_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
+                  const FwdArgs a) {
+  using C = WsCfg;
+  constexpr int D = C::D, BC = C::BC, NS = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // the dynamic shared window starts 1 KB aligned (no static shared memory): control block,
+  // then the SWIZZLE_128B tiles at a 1 KB boundary
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+  WsCtl* ctl = reinterpret_cast<WsCtl*>(smem_raw);
+  uint8_t* sQ = smem_raw + C::kCtlBytes;
+  uint8_t* sKV = sQ + 2 * C::kQBytes;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (tid == 0) {
+    VFA_TRACE_UNIT(a, 0);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&ctl->q_full[t], 1);
+      mbar_init(&ctl->s_full[t], 1);
+      mbar_init(&ctl->s_free[t], 4);
+      mbar_init(&ctl->p_full[t][0], 4);
+      mbar_init(&ctl->p_full[t][1], 4);
+      mbar_init(&ctl->o_ready[t], 4);
+      mbar_init(&ctl->o_final[t], 1);
+      mbar_init(&ctl->tok[t], 1);
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&ctl->kv_full[s], 1);
+      mbar_init(&ctl->kv_empty[s], 2);  // released by both MMA issuers
+    }
+    fence_barrier_init();
+  }
+  if (warp == C::kLoadWarp && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmR);
+  }
+  if (warp == C::kMmaWarp) tmem_alloc<512>(&ctl->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+#define VFA_WS_SETUP()                                                   \
+  const uint32_t tbase = ctl->tmem_base;                                 \
+  const Unit unit = decode_unit(a, blockIdx.x);                          \
+  const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);        \
+  const int N = sched.vmax;                                              \
+  int nrep = 0;                                                          \
+  const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);           \
+  const int G = nchunks + N;                                             \
+  (void)tbase; (void)nrep; (void)G
+  // exact (rowmax + rescale) update at visit position pos
+  auto exact_at = [&](const TileSchedule& s, int pos) {
+    return all_exact(MODE) || sched_is_special(s, sched_block(s, pos));
+  };
+
+  if (warp >= C::kMmaWarp) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VFA_WS_REGS_OTHER));
+    if (warp == C::kLoadWarp) {
+      // ============================ TMA producer ============================
+      if (lane == 0) {
+        VFA_WS_SETUP();
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        for (int t = 0; t < 2; ++t) {
+          mbar_arrive_expect_tx(&ctl->q_full[t], C::kQBytes);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            tma_load_4d(sQ + t * C::kQBytes + c * kBR * 128, &tmQ, &ctl->q_full[t], c * 64, unit.qt * kBR,
+                        unit.h0 + t, unit.b, pol_q);
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+#ifndef VFA_WS_DBG_SKIP
+#define VFA_WS_DBG_SKIP 0  // timing experiments only (wrong results): 1 = no V transfers, 2 = no K transfers
+#endif
+        int nload = 0;
+        auto load_tile = [&](const CUtensorMap* map, int row) {
+          mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+          uint8_t* dst = sKV + stage * C::kKVBytes;
+          if (VFA_WS_DBG_SKIP && nload++ >= 8 &&
+              ((VFA_WS_DBG_SKIP == 1 && map == &tmV) || (VFA_WS_DBG_SKIP == 2 && map == &tmK))) {
+            mbar_arrive(&ctl->kv_full[stage]);
+            if (++stage == NS) {
+              stage = 0;
+              phase ^= 1;
+            }
+            return;
+          }
+          mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            tma_load_4d(dst + c * BC * 128, map, &ctl->kv_full[stage], c * 64, row, unit.kvh, unit.b, pol_kv);
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+        };
+        auto load_s_operand = [&](int g) {
+          if (g < nchunks)
+            load_tile(&tmR, g * BC);
+          else
+            load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
+        };
+        // the MMA warp's consumption order: S-op(0); per g: [V(g)], S-op(g+1)
+        load_s_operand(0);
+        for (int g = 0; g < G; ++g) {
+          if (g >= nchunks) {
+            load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+            VFA_TRACE_EVENT(a, g - nchunks, 15);
+          }
+          if (g + 1 < G) {
+            load_s_operand(g + 1);
+            if (g >= nchunks) VFA_TRACE_EVENT(a, g - nchunks, 16);
+          }
+        }
+      }
+    } else if (warp <= C::kMmaWarp + 1) {
+      // ============================ MMA issuers (one per query tile) ============================
+      // Warp 12 + t issues tile t's MMAs: QK_t(0); per sequence element g: PV_t(g) (after the
+      // softmax's P hand-off), QK_t(g+1). Two issuers let one tile's barrier waits (a TRYWAIT costs
+      // ~90 cycles even when the phase is complete) overlap the other tile's issue, so the short
+      // tcgen05 queue does not drain between MMA groups. Both consume the same K/V ring stages;
+      // a stage is released when both issuers' MMAs on it complete (kv_empty counts 2 commits).
+      VFA_WS_SETUP();
+      const int t = warp - C::kMmaWarp;
+      constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
+      constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+      constexpr uint32_t kLboK = 1u << 16;
+      constexpr uint32_t kLboV = static_cast<uint32_t>((BC * 128) >> 4) << 16;
+      const uint32_t q_lo = (smem_u32(sQ) >> 4) + t * (C::kQBytes >> 4) + kLboK;
+      const uint32_t kv_lo = smem_u32(sKV) >> 4;
+      const uint32_t tS = tbase + C::s_off(t), tO = tbase + C::o_off(t);
+      int stage = 0;
+      uint32_t phase = 0;
+      auto acquire = [&]() -> int {
+        mbar_wait(&ctl->kv_full[stage], phase);
+        if (VFA_WS_ACQ_FENCE) tc_fence_after();
+        const int st = stage;
+        if (++stage == NS) {
+          stage = 0;
+          phase ^= 1;
+        }
+        return st;
+      };
+      auto release = [&](int st) {
+        if (elect_one()) mma_commit(&ctl->kv_empty[st]);
+        __syncwarp();
+      };
+      auto issue_qk = [&](int st) {
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+            const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + off);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + off);
+            mma_ss(tS, da, db, kIdescQK, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&ctl->s_full[t]);
+        }
+        __syncwarp();
+      };
+      // PV K-steps [k_lo, k_hi) (16 keys each; P K-step k in TMEM columns [8k, 8k + 8))
+      auto issue_pv = [&](int st, int k_lo, int k_hi, bool first) {
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = k_lo; kk < k_hi; ++kk) {
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
+            mma_ts(tO, tS + kk * 8, db, kIdescPV, (first && kk == k_lo) ? 0u : 1u);
+          }
+        }
+        __syncwarp();
+      };
+      // turn-taking: the tensor pipe sees PV_0(g) QK_0(g+1) PV_1(g) QK_1(g+1) ... as with one
+      // issuer (tile 1's MMAs run under tile 0's softmax and vice versa), but each issuer's
+      // barrier waits happen while the other issuer's MMAs fill the queue
+      uint32_t tok_ph = 0;
+      auto take_turn = [&]() {
+        if (VFA_WS_TOKEN) {
+          mbar_wait(&ctl->tok[t], tok_ph);
+          tok_ph ^= 1u;
+        }
+      };
+      auto pass_turn = [&]() {
+        if (VFA_WS_TOKEN) {
+          if (elect_one()) mbar_arrive(&ctl->tok[1 - t]);
+          __syncwarp();
+        }
+      };
+      mbar_wait(&ctl->q_full[t], 0);
+      tc_fence_after();
+      {
+        const int st = acquire();
+        if (t == 1) take_turn();
+        issue_qk(st);
+        pass_turn();
+        release(st);
+      }
+      bool o_init = false;
+      uint32_t p_ph = 0, or_ph = 0;
+      for (int g = 0; g < G; ++g) {
+        const bool main_blk = g >= nchunks;
+        const int pos = g - nchunks;
+        if (main_blk) {
+          const int vs = acquire();
+          if (t == 0 && lane == 0) VFA_TRACE_EVENT(a, pos, 17);
+          mbar_wait(&ctl->p_full[t][0], p_ph);
+          tc_fence_after();
+          if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
+          const bool skip = skips(MODE) && ctl->skip[t] != 0;
+          if (pos > 0 && exact_at(sched, pos)) {  // O_t rescaled by the correction warps
+            mbar_wait(&ctl->o_ready[t], or_ph);
+            or_ph ^= 1u;
+            tc_fence_after();
+          }
+          take_turn();
+          if (!skip) issue_pv(vs, 0, 2 * VFA_WS_HANDOFF, !o_init);
+          mbar_wait(&ctl->p_full[t][1], p_ph);
+          tc_fence_after();
+          if (lane == 0) VFA_TRACE_EVENT(a, pos, 8 + 2 * t);
+          if (!skip) issue_pv(vs, 2 * VFA_WS_HANDOFF, BC / 16, false);
+          if (lane == 0) VFA_TRACE_EVENT(a, pos, 9 + 2 * t);
+          p_ph ^= 1u;
+          o_init = o_init || !skip;
+          if (g + 1 == G) pass_turn();  // the last element has no QK: hand the turn over here
+          release(vs);
+        }
+        if (g + 1 < G) {
+          const int ks = acquire();
+          if (main_blk && t == 0 && lane == 0) VFA_TRACE_EVENT(a, pos, 12);
+          if (g < nchunks) {  // the softmax must have read m-init chunk g out of S_t
+            mbar_wait(&ctl->s_free[t], g & 1);
+            tc_fence_after();
+            take_turn();
+          }
+          issue_qk(ks);
+          if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 5 + 2 * t);
+          pass_turn();
+          release(ks);
+          if (main_blk && t == 1 && lane == 0) VFA_TRACE_EVENT(a, pos, 20);
+        }
+      }
+      if (elect_one()) mma_commit(&ctl->o_final[t]);
+      __syncwarp();
+    }
+  } else if (warp >= C::kCorrWarp0) {
+    // ============================ correction + epilogue ============================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VFA_WS_REGS_CORR));
+    VFA_WS_SETUP();
+    const int r = tid & 127;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int pos = 1; pos < N; ++pos) {
+      if (!exact_at(sched, pos)) continue;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        named_bar_sync(1 + t, 256);
+        const float f = ctl->scale[t][r];
+        if (!__all_sync(0xffffffffu, f == 1.0f)) {
+          tc_fence_after();
+          const float2 f2 = make_float2(f, f);
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float o[32];
+            tmem_ld32(tbase + C::o_off(t) + c * 32 + lane_off, o);
+            tmem_wait_ld();
+            reg_fence32(o);
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+              o[e] = x.x;
+              o[e + 1] = x.y;
+            }
+            tmem_st32(tbase + C::o_off(t) + c * 32 + lane_off, reinterpret_cast<const uint32_t*>(o));
+          }
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->o_ready[t]);
+      }
+    }
+    // epilogue: O / l (src/core.py:101-109)
+    bool any_nonfinite = false;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      named_bar_sync(3 + t, 256);
+      const float lsum = ctl->fin_l[t][r];
+      mbar_wait(&ctl->o_final[t], 0);
+      tc_fence_after();
+      const float inv = 1.0f / lsum;
+      const int h = unit.h0 + t;
+      const int R = unit.qt * kBR + r;
+      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr;
+      bool finite = true;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        float v[32];
+        tmem_ld32(tbase + C::o_off(t) + c * 32 + lane_off, v);
+        tmem_wait_ld();
+        reg_fence32(v);
+        uint32_t u[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
+          finite = finite && isfinite(o0) && isfinite(o1);
+          u[e >> 1] = pack_bf16x2(o0, o1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+        dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+        dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+        dst[2] = make_uint4(u[8], u[9], u[10], u[11]);
+        dst[3] = make_uint4(u[12], u[13], u[14], u[15]);
+      }
+      if (a.status && !finite) {
+        any_nonfinite = true;
+        atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+      }
+    }
+    if (any_nonfinite) atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
+  } else {
+    // ============================ softmax (one warpgroup per query tile) ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VFA_WS_REGS_SOFTMAX));
+    VFA_WS_SETUP();
+    const int t = warp >> 2;
+    const int r = tid & 127;
+    const int h = unit.h0 + t;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tbase + C::s_off(t) + lane_off;
+    const int R = unit.qt * kBR + r;
+    const float cs = a.c_scale;
+    float m2 = -INFINITY, l = 0.f;
+    int stab = sched_block(sched, 0);
+    auto wait_s = [&](int g) {
+      mbar_wait(&ctl->s_full[t], g & 1);
+      tc_fence_after();
+    };
+    auto load_s = [&](float* v) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) reg_fence32(v + c * 32);
+    };
+    // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
+    if (nchunks > 0) {
+      float mx = -INFINITY;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        wait_s(ch);
+        float v[128];
+        load_s(v);
+        const int valid = nrep - ch * BC;
+#pragma unroll
+        for (int e = 0; e < 128; ++e)
+          if (e < valid) mx = fmaxf(mx, v[e]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->s_free[t]);
+      }
+      m2 = mx * cs;
+    }
+    if ((MODE == kVFA || MODE == kVSA) && a.use_m_init && a.m0_tile != nullptr)
+      m2 = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt] * cs;
+
+    int n_skipped = 0, n_skipped_special = 0;
+    const float2 cs2 = make_float2(cs, cs);
+    for (int pos = 0; pos < N; ++pos) {
+      const int j = sched_block(sched, pos);
+      const bool special = all_exact(MODE) || sched_is_special(sched, j);
+      const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
+      if (r == 0) VFA_TRACE_EVENT(a, pos, 13 + t);
+      wait_s(nchunks + pos);
+      if (r == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
+      if (r == 0 && t == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
+      float v[128];
+      load_s(v);
+      if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
+        const int lim = R - (j - 1) * BC;
+#pragma unroll
+        for (int e = 0; e < 128; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+      }
+      bool skipped = false;
+      if (MODE == kVSA && !special) {
+        // VSA frozen block: only the skip test (src/sparse.py:296-304); frozen max unchanged
+        const float pm2 = part_max<128>(v) * cs;
+        const bool below = (pm2 - fmaxf(m2, pm2) < a.log2_lambda) ||
+                           (pm2 == -INFINITY && m2 == -INFINITY && a.log2_lambda != -INFINITY);
+        skipped = named_bar_and(5 + t, 128, below);
+      } else if (special) {
+        // exact update: rowmax (src/vfa.py:202-208), threshold test for the skip variants
+        const float mt2 = part_max<128>(v) * cs;
+        const float m2n = fmaxf(m2, mt2);
+        if (skips(MODE)) {
+          const bool below = (mt2 - m2n < a.log2_lambda) ||
+                             (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
+          skipped = named_bar_and(5 + t, 128, below);
+        }
+        float f = 1.0f;
+        if (skipped) {
+          ++n_skipped;
+          ++n_skipped_special;
+        } else {
+          f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
+          if (m2n > m2) stab = j;
+          m2 = m2n;
+          l = __fmul_rn(l, f);
+        }
+        if (pos > 0) {  // the correction warps rescale O_t by f before PV(pos) (src/core.py:91)
+          ctl->scale[t][r] = f;
+          named_bar_arrive(1 + t, 256);
+        }
+      }
+      if (MODE == kVSA && !special && skipped) ++n_skipped;
+      if (skips(MODE) && r == 0) ctl->skip[t] = skipped ? 1u : 0u;
+      if (a.skip_trace && r == 0)
+        a.skip_trace[((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos] = skipped ? 2 : 1;
+#ifndef VFA_WS_DBG_FASTSM
+#define VFA_WS_DBG_FASTSM 0  // timing experiment only (wrong results): no exponentials, P hand-off at once
+#endif
+      if (VFA_WS_DBG_FASTSM) {
+        l += v[0] + v[127];
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&ctl->p_full[t][0]);
+          mbar_arrive(&ctl->p_full[t][1]);
+        }
+      } else if (!skipped) {
+        const float nm = (m2 == -INFINITY ? 0.f : -m2);
+        const float2 nmu2 = make_float2(nm, nm);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 x = __ffma2_rn(make_float2(v[c * 32 + e], v[c * 32 + e + 1]), cs2, nmu2);
+            float2 p;
+            if (((VFA_WS_EMU_CHUNKS >> c) & 1) && ((e >> 1) & 7) >= 8 - VFA_WS_EMU) {
+              p = ex2_poly3(x);
+            } else {
+              p.x = ex2_approx(x.x);
+              p.y = ex2_approx(x.y);
+            }
+            v[c * 32 + e] = p.x;
+            v[c * 32 + e + 1] = p.y;
+            u[e >> 1] = pack_bf16x2(p.x, p.y);
+          }
+          tmem_st16(tS + c * 16, u);
+          if (c == VFA_WS_HANDOFF - 1 || c == 3) {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->p_full[t][c == 3 ? 1 : 0]);
+            if (r == 0) VFA_TRACE_EVENT(a, pos, c == 3 ? 2 * t + 1 : 18 + t);
+          }
+        }
+        // row sum after the hand-off (src/tensor.py:81-89), two packed accumulators
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int e = 0; e < 128; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
+        l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
+      } else {
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&ctl->p_full[t][0]);
+          mbar_arrive(&ctl->p_full[t][1]);
+        }
+      }
+    }
+    if (r == 0 && t == 1) VFA_TRACE_UNIT(a, 2);
+    // ---- finalize (src/core.py:101-109): l to the correction warps, LSE / status here
+    ctl->fin_l[t][r] = l;
+    named_bar_arrive(3 + t, 256);
+    const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
+    const unsigned srow = static_cast<unsigned>(lrow + a.row_base);
+    if (a.lse) a.lse[lrow] = (l == 0.f && m2 != -INFINITY) ? m2 * kLn2 : (m2 + __log2f(l)) * kLn2;
+    if (a.stab) a.stab[lrow] = stab;
+    if (a.status && l == 0.f) {
+      if (m2 == -INFINITY) {
+        atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
+        atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
+      } else {
+        atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
+        atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+      }
+    }
+    if (a.stats && r == 0) {
+      const int n_exact = all_exact(MODE) ? N : sched.n_spec;
+      atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
+      atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
+      atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_exact - n_skipped_special));
+      atomicAdd(&a.stats[VFA_STAT_FROZEN],
+                static_cast<unsigned long long>((N - n_exact) - (n_skipped - n_skipped_special)));
+    }
+  }
+#undef VFA_WS_SETUP
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) VFA_TRACE_UNIT(a, 3);
+  if (warp == C::kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc<512>(ctl->tmem_base);
+  }
+}
+
+}  // namespace vfa

@@ -27,8 +27,11 @@ ap.add_argument("--sink", type=float, default=0.0, help="planted-sink boost (C3 
 ap.add_argument("--lam", type=float, default=1e-2)
 ap.add_argument("--pair", type=int, default=0, help="cta_pair (2 = CTA pairs)")
 ap.add_argument("--split", type=int, default=0, help="softmax_split (0: per-variant default)")
+ap.add_argument("--seq", type=int, default=0, help="sequence length override (C2 heads / head dim)")
 a = ap.parse_args()
-cfg = CONFIGS["c2"]
+cfg = dict(CONFIGS["c2"])
+if a.seq:
+    cfg["L"] = a.seq
 dev = torch.device("cuda", 0)
 q, k, v = make_inputs(cfg, dev)
 if a.sink:
@@ -40,7 +43,8 @@ r.p.softmax_split = a.split
 T = cfg["L"] // a.k_block
 # CTAs: one per unit (two heads); CTA pairs cover four heads per cluster when the group allows
 units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
-buf = torch.zeros(T * 20 + units * 4, dtype=torch.int64, device=dev)
+NS_ = 32  # vfa_kernel.cuh kTraceSlots
+buf = torch.zeros(T * NS_ + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
 r.krepr(sh)
 r.attn(sh)  # warm-up
@@ -50,7 +54,7 @@ r.attn(sh)
 torch.cuda.synchronize()
 r.lib.vfa_debug_trace(None)
 allbuf = buf.cpu().numpy()
-ut = allbuf[T * 20:].reshape(units, 4).astype(np.float64)
+ut = allbuf[T * NS_:].reshape(units, 4).astype(np.float64)
 ok = (ut > 0).all(axis=1)
 ut = ut[ok]
 dur = ut[:, 3] - ut[:, 0]
@@ -58,7 +62,7 @@ pro = ut[:, 1] - ut[:, 0]
 epi = ut[:, 3] - ut[:, 2]
 print(f"units {ok.sum()}: mean cycles {dur.mean():.0f}; prologue (entry -> first S) {pro.mean():.0f} "
       f"({pro.sum() / dur.sum():.1%}), epilogue (last P -> exit) {epi.mean():.0f} ({epi.sum() / dur.sum():.1%})")
-tr = allbuf[: T * 20].reshape(T, 20).astype(np.float64)
+tr = allbuf[: T * NS_].reshape(T, NS_).astype(np.float64)
 n = int((tr[:, 1] > 0).sum())
 tr = tr[:n]
 t0 = tr[tr > 0].min()
@@ -76,6 +80,11 @@ for t in (0, 1):
           f" p90 {np.nanpercentile(busy[sl], 90):.0f}); softmax waits for S {np.nanmedian(wait_s[sl]):.0f};"
           f" MMA sees P after {np.nanmedian(seen[sl]):.0f}; S ready {np.nanmedian(qk_to_s[sl]):.0f} after QK issue;"
           f" period {np.nanmedian(np.diff(s_ready)[sl]):.0f}")
+    if np.isfinite(tr[:, 18 + t]).any():  # warp-specialised kernel: first P chunk hand-off
+        print(f"   tile {t}: first P chunk handed off {np.nanmedian((tr[:, 18 + t] - s_ready)[sl]):.0f} after S;"
+              f" MMA sees it +{np.nanmedian((tr[:, 4 + 2 * t] - tr[:, 18 + t])[sl]):.0f};"
+              f" last P chunk seen +{np.nanmedian((tr[:, 8 + 2 * t] - p_done)[sl]):.0f} after P done,"
+              f" PV issued +{np.nanmedian((tr[:, 9 + 2 * t] - p_done)[sl]):.0f}")
 print("blocks 20-25 (cycles rel. start): [sm0 S, sm0 P, sm1 S, sm1 P, mma0 P, mma0 QK, mma1 P, mma1 QK,"
       " mma0 lastP, mma0 PVdone, mma1 lastP, mma1 PVdone, K acq, sm0 enter, sm1 enter]")
 for i in range(20, min(26, n)):
@@ -84,6 +93,11 @@ print("producer / V: [V(g) TMA issued, K(g+1) TMA issued, MMA acquired V(g)]")
 for i in range(20, min(26, n)):
     print(" ", np.round(tr[i, 15:18]).astype(int).tolist())
 sl = slice(4, n - 4)
+if np.isfinite(tr[:, 20]).any():  # warp-specialised kernel: MMA-side detail
+    print(f" MMA: QK1 issued -> kv_empty commit done {np.nanmedian((tr[:, 20] - tr[:, 7])[sl]):.0f}; "
+          f"-> V(g+1) acquired {np.nanmedian((tr[1:, 17] - tr[:-1, 20])[sl]):.0f}; "
+          f"PV0 issued -> K acquired {np.nanmedian((tr[:, 12] - tr[:, 9])[sl]):.0f}; "
+          f"K acquired -> QK0 issued {np.nanmedian((tr[:, 5] - tr[:, 12])[sl]):.0f}")
 print(f" V TMA issue -> MMA acquires V: median {np.nanmedian((tr[:, 17] - tr[:, 15])[sl]):.0f}; "
       f"K(g+1) TMA issue -> K acquired (next block's slot 12): {np.nanmedian((tr[1:, 12] - tr[:-1, 16])[sl]):.0f}")
 for t in (0, 1):

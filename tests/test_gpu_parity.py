@@ -373,7 +373,10 @@ def test_softmax_splits_agree_with_oracle(variant, d, bc):
         _compare(out, lse, ref_o, ref_lse, f"{kw} split={split}")
         assert st["visited"] == ref_st["visited"]
         outs[split] = out
-    assert any(torch.equal(outs[0], outs[sp]) for sp in (1, 2, 4))
+    # the default (0) runs the warp-specialised kernel at d = Bc = 128 (its own layout, checked
+    # against the oracle above), and one of the explicit layouts elsewhere
+    if (d, bc) != (128, 128):
+        assert any(torch.equal(outs[0], outs[sp]) for sp in (1, 2, 4))
 
 
 def test_deterministic_and_head_sharding_invariant():
