@@ -24,7 +24,7 @@ static int launch_ws_mode(const CUtensorMap& mq, const CUtensorMap& mk, const CU
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return fail(VFA_ERR_CUDA, std::string("cudaFuncGetAttributes: ") + cudaGetErrorString(e));
-    constexpr int kBudget = (2 * VFA_WS_REGS_SOFTMAX + VFA_WS_REGS_CORR + VFA_WS_REGS_OTHER) * 128;
+    constexpr int kBudget = C::kRegBudget;
     if (kBudget > fa.numRegs * C::kThreads)
       return fail(VFA_ERR_CUDA, "setmaxnreg budget " + std::to_string(kBudget) + " exceeds the launch allocation " +
                                     std::to_string(fa.numRegs * C::kThreads) + " (would deadlock)");

@@ -116,7 +116,7 @@ size_t ws_m0_bytes(const VfaParams* p) { return static_cast<size_t>(p->batch * p
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
 #ifndef VFA_WS_ENABLE
-#define VFA_WS_ENABLE 0  // 1: the warp-specialised kernel serves its shapes (in development)
+#define VFA_WS_ENABLE 1  // 0: every shape on vfa_fwd_kernel (experiments)
 #endif
 #ifndef VFA_PAIR_NQ2
 #define VFA_PAIR_NQ2 1

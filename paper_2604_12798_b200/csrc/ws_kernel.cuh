@@ -2,36 +2,34 @@
 // 128-key blocks, 128-row query blocks, two query heads of one GQA group per CTA.
 //
 // Same work unit, schedule, m-init prologue and per-block math as vfa_fwd_kernel
-// (vfa_kernel.cuh; reference map there), with the roles split so that no role sits on
-// another's critical path:
-//   warps 0-3   softmax of query tile 0, one thread per row (TMEM lane = row)
-//   warps 4-7   softmax of query tile 1
-//   warps 8-11  correction: rescales O in TMEM on exact-update blocks (src/core.py:91) while
-//               the softmax already computes the block's exponentials, and the epilogue
-//               (O / l, src/core.py:101-109) while the softmax publishes LSE / status
-//   warps 12-13 MMA issuers, one per query tile (converged warps, elect.sync); 12 allocates TMEM
-//   warp 14     TMA producer
-//   warp 15     idle (completes the last warpgroup)
+// (vfa_kernel.cuh; reference map there), with the roles arranged so that no role waits on
+// another's latency:
+//   warps 0-7   softmax of query tile 0: two warps per sub-partition, two threads per row
+//               (TMEM lane = row, 64 S columns each); they also rescale O on exact-update
+//               blocks (src/core.py:91) and run the epilogue (O / l, LSE, src/core.py:101-109)
+//   warps 8-15  softmax of query tile 1
+//   warps 16-17 MMA issuers, one per query tile (converged warps, elect.sync), taking turns;
+//               16 allocates TMEM
+//   warp 18     TMA producer
+//   warp 19     idle (completes the last warpgroup)
 // TMEM (512 columns): S_t at t*128 (P_t as packed bf16 over its first 64 columns), O_t at
-// 256 + t*128. Per key block and tile the tensor pipe runs PV_t, QK_t(next); the two tiles'
-// chains interleave on the pipe, each tile's softmax runs under the other tile's MMAs.
+// 256 + t*128. Per key block and tile the tensor pipe runs PV_t, QK_t(next); the issuers'
+// turn-taking keeps the order PV_0 QK_0 PV_1 QK_1, so each tile's softmax runs under the other
+// tile's MMAs.
 // Exponentials: exp2 on MUFU.EX2 for most element pairs and a degree-3 polynomial on the FMA
-// pipe for kWsEmu of every 8 pairs in the middle two 32-column chunks, so the XU (16 exp2 per
-// SM-cycle = exactly the tensor pipe's rate at d = 128) is not the bound. Row sums are taken
-// after the P hand-off (off the S -> P -> PV chain).
+// pipe for VFA_WS_EMU of every 8 pairs, so the XU (16 exp2 per SM-cycle = exactly the tensor
+// pipe's rate at d = 128) is not the bound. Row sums are taken after the P hand-off (off the
+// S -> P -> PV chain).
 #pragma once
 #include "vfa_kernel.cuh"
 
 namespace vfa {
 
 #ifndef VFA_WS_EMU
-#define VFA_WS_EMU 2  // element pairs (of 8) on the FMA-pipe exp2 in chunks 1 and 2
+#define VFA_WS_EMU 1  // element pairs (of 8) on the FMA-pipe exp2 in the chunks VFA_WS_EMU_CHUNKS
 #endif
 #ifndef VFA_WS_EMU_CHUNKS
-#define VFA_WS_EMU_CHUNKS 0x6  // bit c: chunk c (32 columns) uses the FMA-pipe exp2 for VFA_WS_EMU pairs
-#endif
-#ifndef VFA_WS_HANDOFF
-#define VFA_WS_HANDOFF 3  // 32-column chunks before the first P hand-off (PV K-steps 0 .. 2*HANDOFF-1)
+#define VFA_WS_EMU_CHUNKS 0x3  // bit c: a thread's 32-column chunk c uses the FMA-pipe exp2
 #endif
 #ifndef VFA_WS_ACQ_FENCE
 #define VFA_WS_ACQ_FENCE 1  // tcgen05 fence after the K/V full wait (experiments: 0)
@@ -40,10 +38,7 @@ namespace vfa {
 #define VFA_WS_TOKEN 1  // MMA issuers take turns (0: free-running, the tiles drift into phase)
 #endif
 #ifndef VFA_WS_REGS_SOFTMAX
-#define VFA_WS_REGS_SOFTMAX 184
-#endif
-#ifndef VFA_WS_REGS_CORR
-#define VFA_WS_REGS_CORR 80
+#define VFA_WS_REGS_SOFTMAX 104
 #endif
 #ifndef VFA_WS_REGS_OTHER
 #define VFA_WS_REGS_OTHER 64
@@ -51,25 +46,24 @@ namespace vfa {
 
 struct WsCfg {
   static constexpr int D = 128, BC = 128, NQ = 2;
-  static constexpr int kThreads = 512;
-  static constexpr int kCorrWarp0 = 8;
-  static constexpr int kMmaWarp = 12;   // and 13: one MMA issuer per query tile
-  static constexpr int kLoadWarp = 14;
+  static constexpr int kThreads = 640;  // 16 softmax warps + 2 MMA issuers + TMA + 1 idle
+  static constexpr int kMmaWarp = 16;   // and 17: one MMA issuer per query tile
+  static constexpr int kLoadWarp = 18;
   static constexpr int kQBytes = kBR * D * 2;    // 32 KB
   static constexpr int kKVBytes = BC * D * 2;    // 32 KB
 #ifndef VFA_WS_STAGES
-#define VFA_WS_STAGES 5
+#define VFA_WS_STAGES 4
 #endif
-  // K/V ring: the MMA holds V(g) and K(g+1); the other stages are loads in flight, which must
-  // cover the L2 -> smem latency of a 32 KB tile under full load (~2 us measured, more than a
-  // block's period: 4 stages left the MMA waiting on V)
+  // K/V ring: the MMA issuers hold V(g) and K(g+1); the other stages are loads in flight
   static constexpr int kStages = VFA_WS_STAGES;
-  static constexpr int kCtlBytes = 3072;  // control block first, tiles from the next 1 KB boundary
+  static constexpr int kCtlBytes = 8192;  // control block first, tiles from the next 1 KB boundary
   static constexpr int kSmem = kCtlBytes + NQ * kQBytes + kStages * kKVBytes;
   static __device__ __forceinline__ uint32_t s_off(int t) { return static_cast<uint32_t>(t * 128); }
   static __device__ __forceinline__ uint32_t o_off(int t) { return static_cast<uint32_t>(256 + t * 128); }
   static_assert(kSmem <= kMaxSmem, "shared memory");
-  static_assert((2 * VFA_WS_REGS_SOFTMAX + VFA_WS_REGS_CORR + VFA_WS_REGS_OTHER) * 128 <= 65536, "register budget");
+  // setmaxnreg pool = the launch allocation (640 threads x 96 registers)
+  static constexpr int kRegBudget = (4 * VFA_WS_REGS_SOFTMAX + VFA_WS_REGS_OTHER) * 128;
+  static_assert(kRegBudget <= 640 * 96, "register budget");
 };
 
 struct __align__(16) WsCtl {
@@ -79,13 +73,14 @@ struct __align__(16) WsCtl {
   uint64_t s_full[2];     // MMA -> softmax t: S_t of sequence element g ready (parity g & 1)
   uint64_t s_free[2];     // softmax t -> MMA: m-init chunk read, S_t may be overwritten
   uint64_t p_full[2][2];  // softmax t -> MMA: P chunk c in TMEM (or the block skipped)
-  uint64_t o_ready[2];    // correction -> MMA: O_t rescaled for the current exact block
   uint64_t o_final[2];    // MMA -> correction: last PV_t complete
   uint64_t tok[2];        // MMA issuer 1-t -> issuer t: your turn to enqueue (keeps the tiles in anti-phase)
   uint32_t tmem_base;
   uint32_t skip[2];
-  float scale[2][kBR];    // softmax t -> correction: rescale factor of the current exact block
-  float fin_l[2][kBR];    // softmax t -> correction: final row sums
+  float zero;             // 0.0f: read back (volatile) to order softmax chunks, see chunk_bias
+  float xmax[2][2][kBR];  // [tile][half][row]: row-max exchange between the two halves of a row
+  float xl[2][2][kBR];    // [tile][half][row]: final partial row sums
+  uint8_t xfin[2][2][kBR];  // [tile][half][row]: output finite flags
 };
 static_assert(sizeof(WsCtl) <= WsCfg::kCtlBytes, "control block");
 
@@ -116,13 +111,13 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
 
   if (tid == 0) {
     VFA_TRACE_UNIT(a, 0);
+    ctl->zero = 0.f;
     for (int t = 0; t < 2; ++t) {
       mbar_init(&ctl->q_full[t], 1);
       mbar_init(&ctl->s_full[t], 1);
-      mbar_init(&ctl->s_free[t], 4);
-      mbar_init(&ctl->p_full[t][0], 4);
-      mbar_init(&ctl->p_full[t][1], 4);
-      mbar_init(&ctl->o_ready[t], 4);
+      mbar_init(&ctl->s_free[t], 8);
+      mbar_init(&ctl->p_full[t][0], 8);
+      mbar_init(&ctl->p_full[t][1], 8);
       mbar_init(&ctl->o_final[t], 1);
       mbar_init(&ctl->tok[t], 1);
     }
@@ -265,14 +260,16 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         }
         __syncwarp();
       };
-      // PV K-steps [k_lo, k_hi) (16 keys each; P K-step k in TMEM columns [8k, 8k + 8))
-      auto issue_pv = [&](int st, int k_lo, int k_hi, bool first) {
+      // PV of P chunk c: each half's 32-column chunk c = K-steps {2c, 2c+1} of half 0 and
+      // {4+2c, 5+2c} of half 1 (16 keys per K-step; P K-step k in TMEM columns [8k, 8k + 8))
+      auto issue_pv = [&](int st, int c, bool first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
         if (elect_one()) {
 #pragma unroll
-          for (int kk = k_lo; kk < k_hi; ++kk) {
+          for (int i = 0; i < 4; ++i) {
+            const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
-            mma_ts(tO, tS + kk * 8, db, kIdescPV, (first && kk == k_lo) ? 0u : 1u);
+            mma_ts(tO, tS + kk * 8, db, kIdescPV, (first && i == 0) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -303,7 +300,7 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         release(st);
       }
       bool o_init = false;
-      uint32_t p_ph = 0, or_ph = 0;
+      uint32_t p_ph = 0;
       for (int g = 0; g < G; ++g) {
         const bool main_blk = g >= nchunks;
         const int pos = g - nchunks;
@@ -314,17 +311,12 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
           tc_fence_after();
           if (lane == 0) VFA_TRACE_EVENT(a, pos, 4 + 2 * t);
           const bool skip = skips(MODE) && ctl->skip[t] != 0;
-          if (pos > 0 && exact_at(sched, pos)) {  // O_t rescaled by the correction warps
-            mbar_wait(&ctl->o_ready[t], or_ph);
-            or_ph ^= 1u;
-            tc_fence_after();
-          }
           take_turn();
-          if (!skip) issue_pv(vs, 0, 2 * VFA_WS_HANDOFF, !o_init);
+          if (!skip) issue_pv(vs, 0, !o_init);
           mbar_wait(&ctl->p_full[t][1], p_ph);
           tc_fence_after();
           if (lane == 0) VFA_TRACE_EVENT(a, pos, 8 + 2 * t);
-          if (!skip) issue_pv(vs, 2 * VFA_WS_HANDOFF, BC / 16, false);
+          if (!skip) issue_pv(vs, 1, false);
           if (lane == 0) VFA_TRACE_EVENT(a, pos, 9 + 2 * t);
           p_ph ^= 1u;
           o_init = o_init || !skip;
@@ -349,89 +341,23 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
       if (elect_one()) mma_commit(&ctl->o_final[t]);
       __syncwarp();
     }
-  } else if (warp >= C::kCorrWarp0) {
-    // ============================ correction + epilogue ============================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VFA_WS_REGS_CORR));
-    VFA_WS_SETUP();
-    const int r = tid & 127;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    for (int pos = 1; pos < N; ++pos) {
-      if (!exact_at(sched, pos)) continue;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        named_bar_sync(1 + t, 256);
-        const float f = ctl->scale[t][r];
-        if (!__all_sync(0xffffffffu, f == 1.0f)) {
-          tc_fence_after();
-          const float2 f2 = make_float2(f, f);
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float o[32];
-            tmem_ld32(tbase + C::o_off(t) + c * 32 + lane_off, o);
-            tmem_wait_ld();
-            reg_fence32(o);
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
-              o[e] = x.x;
-              o[e + 1] = x.y;
-            }
-            tmem_st32(tbase + C::o_off(t) + c * 32 + lane_off, reinterpret_cast<const uint32_t*>(o));
-          }
-          tmem_wait_st();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ctl->o_ready[t]);
-      }
-    }
-    // epilogue: O / l (src/core.py:101-109)
-    bool any_nonfinite = false;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      named_bar_sync(3 + t, 256);
-      const float lsum = ctl->fin_l[t][r];
-      mbar_wait(&ctl->o_final[t], 0);
-      tc_fence_after();
-      const float inv = 1.0f / lsum;
-      const int h = unit.h0 + t;
-      const int R = unit.qt * kBR + r;
-      __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr;
-      bool finite = true;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        float v[32];
-        tmem_ld32(tbase + C::o_off(t) + c * 32 + lane_off, v);
-        tmem_wait_ld();
-        reg_fence32(v);
-        uint32_t u[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float o0 = v[e] * inv, o1 = v[e + 1] * inv;
-          finite = finite && isfinite(o0) && isfinite(o1);
-          u[e >> 1] = pack_bf16x2(o0, o1);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-        dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
-        dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
-        dst[2] = make_uint4(u[8], u[9], u[10], u[11]);
-        dst[3] = make_uint4(u[12], u[13], u[14], u[15]);
-      }
-      if (a.status && !finite) {
-        any_nonfinite = true;
-        atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
-      }
-    }
-    if (any_nonfinite) atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
   } else {
-    // ============================ softmax (one warpgroup per query tile) ============================
+    // ============================ softmax: 8 warps per query tile ============================
+    // warps 8t .. 8t+7 serve tile t; warp w handles TMEM lanes 32*(w&3) .. +31 (rows) and half
+    // hf = (w>>2)&1 of every S row (64 columns), so each sub-partition runs two warps per tile:
+    // one warp's dependency stalls are covered by the other's MUFU / FMA work. Both halves see
+    // the same running max (exchanged through shared memory on exact-update blocks, which are
+    // the only ones that need it); each keeps its part of the normalizer.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VFA_WS_REGS_SOFTMAX));
     VFA_WS_SETUP();
-    const int t = warp >> 2;
+    const int t = warp >> 3;
+    const int hf = (warp >> 2) & 1;
     const int r = tid & 127;
     const int h = unit.h0 + t;
+    constexpr int CP = 64;  // S columns per thread
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tbase + C::s_off(t) + lane_off;
+    const uint32_t tO = tbase + C::o_off(t) + hf * CP + lane_off;
     const int R = unit.qt * kBR + r;
     const float cs = a.c_scale;
     float m2 = -INFINITY, l = 0.f;
@@ -441,28 +367,36 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
       tc_fence_after();
     };
     auto load_s = [&](float* v) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, v + c * 32);
+      tmem_ld32(tS + hf * CP, v);
+      tmem_ld32(tS + hf * CP + 32, v + 32);
       tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) reg_fence32(v + c * 32);
+      reg_fence32(v);
+      reg_fence32(v + 32);
+    };
+    // row max over both halves (named barrier 1 + t over the tile's 256 threads); single-buffered:
+    // a half rewrites its slot only after S of a later block, i.e. after the MMA consumed both
+    // halves' P of this block, which they hand over after reading the exchanged value
+    auto row_max = [&](float mine) -> float {
+      ctl->xmax[t][hf][r] = mine;
+      named_bar_sync(1 + t, 256);
+      return fmaxf(ctl->xmax[t][0][r], ctl->xmax[t][1][r]);
     };
     // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
     if (nchunks > 0) {
       float mx = -INFINITY;
       for (int ch = 0; ch < nchunks; ++ch) {
         wait_s(ch);
-        float v[128];
+        float v[CP];
         load_s(v);
-        const int valid = nrep - ch * BC;
+        const int valid = nrep - ch * BC - hf * CP;
 #pragma unroll
-        for (int e = 0; e < 128; ++e)
+        for (int e = 0; e < CP; ++e)
           if (e < valid) mx = fmaxf(mx, v[e]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctl->s_free[t]);
       }
-      m2 = mx * cs;
+      m2 = row_max(mx) * cs;
     }
     if ((MODE == kVFA || MODE == kVSA) && a.use_m_init && a.m0_tile != nullptr)
       m2 = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt] * cs;
@@ -473,34 +407,53 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
       const int j = sched_block(sched, pos);
       const bool special = all_exact(MODE) || sched_is_special(sched, j);
       const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
-      if (r == 0) VFA_TRACE_EVENT(a, pos, 13 + t);
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 13 + t);
       wait_s(nchunks + pos);
-      if (r == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
-      if (r == 0 && t == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
-      float v[128];
-      load_s(v);
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 2 * t);
+      if (r == 0 && hf == 0 && t == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
+      float v[CP];
+      // VFA frozen blocks need no row statistic before the exponentials: load the first 32
+      // columns, start the second load, and let chunk 0's P go out while it lands
+      const bool split = MODE == kVFA && !special;
+      if (split) {
+        tmem_ld32(tS + hf * CP, v);
+        tmem_wait_ld();
+        reg_fence32(v);
+        tmem_ld32(tS + hf * CP + 32, v + 32);
+      } else {
+        load_s(v);
+      }
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 21 + 4 * t);
+      const int lim = R - (j - 1) * BC - hf * CP;  // this half's columns > lim are masked
       if (mask) {  // entrywise causal mask (src/reference.py:93-96): exact zeros after exp2
-        const int lim = R - (j - 1) * BC;
 #pragma unroll
-        for (int e = 0; e < 128; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        for (int e = 0; e < 32; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        if (!split) {
+#pragma unroll
+          for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        }
       }
       bool skipped = false;
+      float f = 1.0f;
+      bool rescale = false;
       if (MODE == kVSA && !special) {
-        // VSA frozen block: only the skip test (src/sparse.py:296-304); frozen max unchanged
-        const float pm2 = part_max<128>(v) * cs;
+        // VSA frozen block: only the skip test (src/sparse.py:296-304). A row is below the
+        // threshold iff both halves' maxima are, so one AND over the tile decides without
+        // exchanging maxima; the frozen max is not updated.
+        const float pm2 = part_max<CP>(v) * cs;
         const bool below = (pm2 - fmaxf(m2, pm2) < a.log2_lambda) ||
                            (pm2 == -INFINITY && m2 == -INFINITY && a.log2_lambda != -INFINITY);
-        skipped = named_bar_and(5 + t, 128, below);
+        skipped = named_bar_and(1 + t, 256, below);
+        if (skipped) ++n_skipped;
       } else if (special) {
         // exact update: rowmax (src/vfa.py:202-208), threshold test for the skip variants
-        const float mt2 = part_max<128>(v) * cs;
+        const float mt2 = row_max(part_max<CP>(v)) * cs;
         const float m2n = fmaxf(m2, mt2);
         if (skips(MODE)) {
           const bool below = (mt2 - m2n < a.log2_lambda) ||
                              (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
-          skipped = named_bar_and(5 + t, 128, below);
+          skipped = named_bar_and(1 + t, 256, below);
         }
-        float f = 1.0f;
         if (skipped) {
           ++n_skipped;
           ++n_skipped_special;
@@ -509,21 +462,36 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
           if (m2n > m2) stab = j;
           m2 = m2n;
           l = __fmul_rn(l, f);
-        }
-        if (pos > 0) {  // the correction warps rescale O_t by f before PV(pos) (src/core.py:91)
-          ctl->scale[t][r] = f;
-          named_bar_arrive(1 + t, 256);
+          rescale = pos > 0 && !__all_sync(0xffffffffu, f == 1.0f);
         }
       }
-      if (MODE == kVSA && !special && skipped) ++n_skipped;
-      if (skips(MODE) && r == 0) ctl->skip[t] = skipped ? 1u : 0u;
-      if (a.skip_trace && r == 0)
+      if (skips(MODE) && r == 0 && hf == 0) ctl->skip[t] = skipped ? 1u : 0u;
+      if (a.skip_trace && r == 0 && hf == 0)
         a.skip_trace[((static_cast<size_t>(unit.b) * a.Hq + h) * a.Tr + unit.qt) * a.Tc + pos] = skipped ? 2 : 1;
+      if (rescale) {
+        // O_t is quiescent (S_t(pos) complete => PV_t(pos-1) complete): rescale this half of the
+        // row before PV(pos) accumulates into it (src/core.py:91)
+        const float2 f2 = make_float2(f, f);
+#pragma unroll 1
+        for (int c = 0; c < CP / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+          reg_fence16(o);
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+            o[e] = x.x;
+            o[e + 1] = x.y;
+          }
+          tmem_st16(tO + c * 16, reinterpret_cast<const uint32_t*>(o));
+        }
+      }
 #ifndef VFA_WS_DBG_FASTSM
 #define VFA_WS_DBG_FASTSM 0  // timing experiment only (wrong results): no exponentials, P hand-off at once
 #endif
       if (VFA_WS_DBG_FASTSM) {
-        l += v[0] + v[127];
+        l += v[0] + v[CP - 1];
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -532,9 +500,26 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         }
       } else if (!skipped) {
         const float nm = (m2 == -INFINITY ? 0.f : -m2);
-        const float2 nmu2 = make_float2(nm, nm);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < CP / 32; ++c) {
+          // chunk c > 0 starts after chunk c-1's hand-off: its bias goes through a volatile
+          // shared-memory read issued after that hand-off, so the compiler cannot hoist its
+          // exponentials above the earlier chunk's P store (which would delay the hand-off)
+          float nmc = nm;
+          if (c > 0) {
+            float z;
+            asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(z) : "r"(smem_u32(&ctl->zero)) : "memory");
+            nmc = nm + z;
+            if (split) {
+              tmem_wait_ld();
+              reg_fence32(v + 32);
+              if (mask) {
+#pragma unroll
+                for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+              }
+            }
+          }
+          const float2 nmu2 = make_float2(nmc, nmc);
           uint32_t u[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -550,21 +535,24 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
             v[c * 32 + e + 1] = p.y;
             u[e >> 1] = pack_bf16x2(p.x, p.y);
           }
-          tmem_st16(tS + c * 16, u);
-          if (c == VFA_WS_HANDOFF - 1 || c == 3) {
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ctl->p_full[t][c == 3 ? 1 : 0]);
-            if (r == 0) VFA_TRACE_EVENT(a, pos, c == 3 ? 2 * t + 1 : 18 + t);
-          }
+          // P of this half's 32-column chunk c: PV K-steps 4*hf + 2c, 4*hf + 2c + 1
+          tmem_st16(tS + hf * (CP / 2) + c * 16, u);
+          if (r == 0 && hf == 0 && c == 0) VFA_TRACE_EVENT(a, pos, 22 + 4 * t);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
+          if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, c == 1 ? 2 * t + 1 : 18 + t);
         }
         // row sum after the hand-off (src/tensor.py:81-89), two packed accumulators
         float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int e = 0; e < 128; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
+        for (int e = 0; e < CP; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
         l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 23 + 4 * t);
       } else {
+        if (rescale) tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&ctl->p_full[t][0]);
@@ -572,24 +560,60 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         }
       }
     }
-    if (r == 0 && t == 1) VFA_TRACE_UNIT(a, 2);
-    // ---- finalize (src/core.py:101-109): l to the correction warps, LSE / status here
-    ctl->fin_l[t][r] = l;
-    named_bar_arrive(3 + t, 256);
+    if (r == 0 && hf == 0 && t == 1) VFA_TRACE_UNIT(a, 2);
+    // ---- finalize (src/core.py:101-109): l = half 0 + half 1, O / l, LSE, status
+    ctl->xl[t][hf][r] = l;
+    named_bar_sync(1 + t, 256);
+    const float lsum = __fadd_rn(ctl->xl[t][0][r], ctl->xl[t][1][r]);
     const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + h) * a.Lq + R;
     const unsigned srow = static_cast<unsigned>(lrow + a.row_base);
-    if (a.lse) a.lse[lrow] = (l == 0.f && m2 != -INFINITY) ? m2 * kLn2 : (m2 + __log2f(l)) * kLn2;
-    if (a.stab) a.stab[lrow] = stab;
-    if (a.status && l == 0.f) {
-      if (m2 == -INFINITY) {
-        atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
-        atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
-      } else {
-        atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
-        atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+    if (hf == 0) {
+      if (a.lse) a.lse[lrow] = (lsum == 0.f && m2 != -INFINITY) ? m2 * kLn2 : (m2 + __log2f(lsum)) * kLn2;
+      if (a.stab) a.stab[lrow] = stab;
+      if (a.status && lsum == 0.f) {
+        if (m2 == -INFINITY) {
+          atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
+          atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
+        } else {
+          atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
+          atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+        }
       }
     }
-    if (a.stats && r == 0) {
+    mbar_wait(&ctl->o_final[t], 0);
+    tc_fence_after();
+    const float inv = 1.0f / lsum;
+    __nv_bfloat16* orow = a.o + unit.b * a.o_sb + h * a.o_sh + static_cast<long long>(R) * a.o_sr + hf * CP;
+    bool finite = true;
+#pragma unroll
+    for (int c = 0; c < CP / 32; ++c) {
+      float o[32];
+      tmem_ld32(tO + c * 32, o);
+      tmem_wait_ld();
+      reg_fence32(o);
+      uint32_t u[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float o0 = o[e] * inv, o1 = o[e + 1] * inv;
+        finite = finite && isfinite(o0) && isfinite(o1);
+        u[e >> 1] = pack_bf16x2(o0, o1);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+      dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+      dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+      dst[2] = make_uint4(u[8], u[9], u[10], u[11]);
+      dst[3] = make_uint4(u[12], u[13], u[14], u[15]);
+    }
+    if (a.status) {
+      // a row is non-finite if either half is: combine through shared memory, count it once
+      ctl->xfin[t][hf][r] = finite ? 1 : 0;
+      named_bar_sync(1 + t, 256);
+      if (hf == 0 && !(ctl->xfin[t][0][r] && ctl->xfin[t][1][r])) {
+        atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+        atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
+      }
+    }
+    if (a.stats && r == 0 && hf == 0) {
       const int n_exact = all_exact(MODE) ? N : sched.n_spec;
       atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
       atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));

@@ -98,6 +98,12 @@ if np.isfinite(tr[:, 20]).any():  # warp-specialised kernel: MMA-side detail
           f"-> V(g+1) acquired {np.nanmedian((tr[1:, 17] - tr[:-1, 20])[sl]):.0f}; "
           f"PV0 issued -> K acquired {np.nanmedian((tr[:, 12] - tr[:, 9])[sl]):.0f}; "
           f"K acquired -> QK0 issued {np.nanmedian((tr[:, 5] - tr[:, 12])[sl]):.0f}")
+for t in (0, 1):
+    if np.isfinite(tr[:, 21 + 4 * t]).any():  # warp-specialised kernel: inside one softmax block
+        s0 = tr[:, 2 * t]
+        print(f" tile {t} softmax: S loaded +{np.nanmedian((tr[:, 21 + 4 * t] - s0)[sl]):.0f}, chunk-0 P stored "
+              f"+{np.nanmedian((tr[:, 22 + 4 * t] - s0)[sl]):.0f}, chunk-0 handed off +{np.nanmedian((tr[:, 18 + t] - s0)[sl]):.0f}, "
+              f"chunk-1 handed off +{np.nanmedian((tr[:, 1 + 2 * t] - s0)[sl]):.0f}, row sum +{np.nanmedian((tr[:, 23 + 4 * t] - s0)[sl]):.0f}")
 print(f" V TMA issue -> MMA acquires V: median {np.nanmedian((tr[:, 17] - tr[:, 15])[sl]):.0f}; "
       f"K(g+1) TMA issue -> K acquired (next block's slot 12): {np.nanmedian((tr[1:, 12] - tr[:-1, 16])[sl]):.0f}")
 for t in (0, 1):
