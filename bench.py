@@ -464,7 +464,9 @@ def main_ours(args):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(),
-                         "kernel": f"vfa_fwd_kernel<{d},{args.k_block},2,VFA> (per rank)",
+                         "kernel": ("vfa_ws_kernel<VFA> (warp-specialised, d=128, Bc=128, two query tiles per CTA)"
+                                    if (d, args.k_block) == (128, 128) and Hq // Hkv % 2 == 0
+                                    else f"vfa_fwd_kernel<{d},{args.k_block},2,VFA>") + " (per rank)",
                          "peak_source": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",
                          "frac_of_sustained": round(achieved / peak_sus, 4) if peak_sus else None},
             "ablation": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}

@@ -34,6 +34,15 @@ namespace vfa {
 #ifndef VFA_WS_ACQ_FENCE
 #define VFA_WS_ACQ_FENCE 1  // tcgen05 fence after the K/V full wait (experiments: 0)
 #endif
+#ifndef VFA_WS_NCH
+#define VFA_WS_NCH 2  // P hand-off chunks per thread (2: 32 columns each, 4: 16 columns each)
+#endif
+constexpr int kNCH = VFA_WS_NCH;
+constexpr int kCW = 64 / kNCH;  // columns per P chunk
+static_assert(kNCH == 2 || kNCH == 4, "P hand-off in 2 or 4 chunks");
+#ifndef VFA_WS_POLY3
+#define VFA_WS_POLY3 0  // 1: degree-3 FMA-pipe exp2 (fewer instructions, 8.6e-5 relative error)
+#endif
 #ifndef VFA_WS_TOKEN
 #define VFA_WS_TOKEN 1  // MMA issuers take turns (0: free-running, the tiles drift into phase)
 #endif
@@ -72,7 +81,7 @@ struct __align__(16) WsCtl {
   uint64_t kv_empty[WsCfg::kStages];
   uint64_t s_full[2];     // MMA -> softmax t: S_t of sequence element g ready (parity g & 1)
   uint64_t s_free[2];     // softmax t -> MMA: m-init chunk read, S_t may be overwritten
-  uint64_t p_full[2][2];  // softmax t -> MMA: P chunk c in TMEM (or the block skipped)
+  uint64_t p_full[2][4];  // softmax t -> MMA: P chunk c in TMEM (or the block skipped)
   uint64_t o_final[2];    // MMA -> correction: last PV_t complete
   uint64_t tok[2];        // MMA issuer 1-t -> issuer t: your turn to enqueue (keeps the tiles in anti-phase)
   uint32_t tmem_base;
@@ -116,8 +125,7 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
       mbar_init(&ctl->q_full[t], 1);
       mbar_init(&ctl->s_full[t], 1);
       mbar_init(&ctl->s_free[t], 8);
-      mbar_init(&ctl->p_full[t][0], 8);
-      mbar_init(&ctl->p_full[t][1], 8);
+      for (int c = 0; c < 4; ++c) mbar_init(&ctl->p_full[t][c], 8);
       mbar_init(&ctl->o_final[t], 1);
       mbar_init(&ctl->tok[t], 1);
     }
@@ -260,14 +268,15 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         }
         __syncwarp();
       };
-      // PV of P chunk c: each half's 32-column chunk c = K-steps {2c, 2c+1} of half 0 and
-      // {4+2c, 5+2c} of half 1 (16 keys per K-step; P K-step k in TMEM columns [8k, 8k + 8))
+      // PV of P chunk c: each half's chunk c = K-steps 4*hf + c*kCW/16 .. + kCW/16 (16 keys per
+      // K-step; P K-step k in TMEM columns [8k, 8k + 8))
       auto issue_pv = [&](int st, int c, bool first) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
+        constexpr int kKS = kCW / 16;  // K-steps per half and chunk
         if (elect_one()) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
+          for (int i = 0; i < 2 * kKS; ++i) {
+            const int kk = (i / kKS) * 4 + c * kKS + (i % kKS);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
             mma_ts(tO, tS + kk * 8, db, kIdescPV, (first && i == 0) ? 0u : 1u);
           }
@@ -313,10 +322,13 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
           const bool skip = skips(MODE) && ctl->skip[t] != 0;
           take_turn();
           if (!skip) issue_pv(vs, 0, !o_init);
-          mbar_wait(&ctl->p_full[t][1], p_ph);
-          tc_fence_after();
-          if (lane == 0) VFA_TRACE_EVENT(a, pos, 8 + 2 * t);
-          if (!skip) issue_pv(vs, 1, false);
+#pragma unroll
+          for (int c = 1; c < kNCH; ++c) {
+            mbar_wait(&ctl->p_full[t][c], p_ph);
+            tc_fence_after();
+            if (c == kNCH - 1 && lane == 0) VFA_TRACE_EVENT(a, pos, 8 + 2 * t);
+            if (!skip) issue_pv(vs, c, false);
+          }
           if (lane == 0) VFA_TRACE_EVENT(a, pos, 9 + 2 * t);
           p_ph ^= 1u;
           o_init = o_init || !skip;
@@ -494,14 +506,12 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         l += v[0] + v[CP - 1];
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&ctl->p_full[t][0]);
-          mbar_arrive(&ctl->p_full[t][1]);
-        }
+        if (lane == 0)
+          for (int c = 0; c < kNCH; ++c) mbar_arrive(&ctl->p_full[t][c]);
       } else if (!skipped) {
         const float nm = (m2 == -INFINITY ? 0.f : -m2);
 #pragma unroll
-        for (int c = 0; c < CP / 32; ++c) {
+        for (int c = 0; c < kNCH; ++c) {
           // chunk c > 0 starts after chunk c-1's hand-off: its bias goes through a volatile
           // shared-memory read issued after that hand-off, so the compiler cannot hoist its
           // exponentials above the earlier chunk's P store (which would delay the hand-off)
@@ -510,7 +520,7 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
             float z;
             asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(z) : "r"(smem_u32(&ctl->zero)) : "memory");
             nmc = nm + z;
-            if (split) {
+            if (split && c * kCW == 32) {  // the second 32-column load has landed by now
               tmem_wait_ld();
               reg_fence32(v + 32);
               if (mask) {
@@ -520,29 +530,38 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
             }
           }
           const float2 nmu2 = make_float2(nmc, nmc);
-          uint32_t u[16];
+          uint32_t u[kCW / 2];
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float2 x = __ffma2_rn(make_float2(v[c * 32 + e], v[c * 32 + e + 1]), cs2, nmu2);
+          for (int e = 0; e < kCW; e += 2) {
+            const float2 x = __ffma2_rn(make_float2(v[c * kCW + e], v[c * kCW + e + 1]), cs2, nmu2);
             float2 p;
             if (((VFA_WS_EMU_CHUNKS >> c) & 1) && ((e >> 1) & 7) >= 8 - VFA_WS_EMU) {
-              p = ex2_poly3(x);
+              // degree-4 polynomial (|rel err| < 3e-6): the degree-3 form's 8.6e-5 showed up as
+              // ~4e-5 in LSE on rows dominated by one emulated element
+              p = VFA_WS_POLY3 ? ex2_poly3(x) : ex2_poly2(x);
             } else {
               p.x = ex2_approx(x.x);
               p.y = ex2_approx(x.y);
             }
-            v[c * 32 + e] = p.x;
-            v[c * 32 + e + 1] = p.y;
+            v[c * kCW + e] = p.x;
+            v[c * kCW + e + 1] = p.y;
             u[e >> 1] = pack_bf16x2(p.x, p.y);
           }
-          // P of this half's 32-column chunk c: PV K-steps 4*hf + 2c, 4*hf + 2c + 1
-          tmem_st16(tS + hf * (CP / 2) + c * 16, u);
+          // P of this half's chunk c (packed bf16, kCW/2 TMEM columns): PV K-steps
+          // 4*hf + c*kCW/16 .. +kCW/16
+          if constexpr (kCW == 32)
+            tmem_st16(tS + hf * (CP / 2) + c * (kCW / 2), u);
+          else
+            tmem_st8(tS + hf * (CP / 2) + c * (kCW / 2), u);
           if (r == 0 && hf == 0 && c == 0) VFA_TRACE_EVENT(a, pos, 22 + 4 * t);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&ctl->p_full[t][c]);
-          if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, c == 1 ? 2 * t + 1 : 18 + t);
+          if (r == 0 && hf == 0) {
+            if (c == 0) VFA_TRACE_EVENT(a, pos, 18 + t);
+            if (c == kNCH - 1) VFA_TRACE_EVENT(a, pos, 2 * t + 1);
+          }
         }
         // row sum after the hand-off (src/tensor.py:81-89), two packed accumulators
         float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -554,10 +573,8 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
         if (rescale) tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&ctl->p_full[t][0]);
-          mbar_arrive(&ctl->p_full[t][1]);
-        }
+        if (lane == 0)
+          for (int c = 0; c < kNCH; ++c) mbar_arrive(&ctl->p_full[t][c]);
       }
     }
     if (r == 0 && hf == 0 && t == 1) VFA_TRACE_UNIT(a, 2);
