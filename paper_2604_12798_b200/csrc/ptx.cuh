@@ -377,4 +377,25 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   while (!mbar_try_wait_cluster(bar, parity)) {
   }
 }
+
+// 4-D tiled TMA load multicast to the CTAs of `cta_mask` in the cluster: the tile lands at the
+// same shared-memory offset in each of them and each one's mbarrier (same offset) counts the bytes
+__device__ __forceinline__ void tma_load_4d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               int c2, int c3, uint16_t cta_mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7, %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "h"(cta_mask),
+      "l"(cache_hint)
+      : "memory");
+}
+// arrive on the same-offset mbarrier of every CTA in `cta_mask` once this thread's prior
+// tcgen05 operations (cta_group::1) complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
 }  // namespace vfa

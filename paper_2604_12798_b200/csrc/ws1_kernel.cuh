@@ -1,0 +1,629 @@
+// B200 (sm_100a) attention forward with a decoupled softmax: one 128-row query tile per CTA,
+// three S buffers in TMEM, K/V shared by a 2-CTA cluster through TMA multicast.
+//
+// Shape: head_dim 128, 128-key blocks, 128-row query blocks, GQA group even. A cluster is one
+// work unit of vfa_fwd_kernel (b, KV head, two query heads of its group, one query tile): CTA r
+// of the pair computes query head h0 + r. Both CTAs visit the same key blocks in the same
+// order (same rows, same schedule), so each loads half of every K / V tile and multicasts it to
+// both: per-SM L2 -> smem traffic equals the two-tiles-per-CTA kernels', while each CTA has the
+// TMEM for three S buffers.
+//
+// Per CTA (640 threads):
+//   warps 0-7   softmax group 0: sequence elements g = 0, 2, 4, ...   (two threads per row,
+//   warps 8-15  softmax group 1: sequence elements g = 1, 3, 5, ...    64 S columns each)
+//   warp 16     QK^T issuer (converged, elect.sync), TMEM allocator
+//   warp 17     TMA producer
+//   warp 18     PV issuer
+//   warp 19     idle
+// TMEM: S buffers at 0 / 128 / 256 (P packed bf16 over the first 64 columns of its S buffer),
+// O at 384. The MMA issues QK for element g + 3 as soon as PV(g) is issued, so S is up to
+// three blocks ahead and the two groups' exponentials run back to back: the softmax is never
+// waiting on a P -> PV -> QK -> S round trip (the limit of the ping-pong kernels).
+//
+// Running max across the two groups (src/vfa.py:199-215, src/core.py:76-98): exact-update
+// positions are processed in schedule order; the group that finishes one publishes the row max
+// as a new "version" (a ring of kVer slots with one mbarrier each) and a group needing the max
+// after the e-th exact position waits for version e. VFA's frozen blocks (all but sink / local)
+// need the seed / frozen max only, so after the specials the groups never wait on each other.
+// Each group keeps its part of the normalizer relative to the max it last saw; the parts are
+// rescaled to the final max at the end. O is rescaled (src/core.py:91) by the group that raised
+// the max, after PV of the previous position completed (pv_done) and before its own P hand-off.
+#pragma once
+#include "vfa_kernel.cuh"
+
+namespace vfa {
+
+#ifndef VFA_WS1_STAGES
+#define VFA_WS1_STAGES 5
+#endif
+#ifndef VFA_WS1_EMU
+#define VFA_WS1_EMU 1  // element pairs (of 8) per 32-column chunk on the FMA-pipe exp2
+#endif
+#ifndef VFA_WS1_REGS_SOFTMAX
+#define VFA_WS1_REGS_SOFTMAX 104
+#endif
+#ifndef VFA_WS1_REGS_OTHER
+#define VFA_WS1_REGS_OTHER 64
+#endif
+
+struct Ws1Cfg {
+  static constexpr int D = 128, BC = 128;
+  static constexpr int kThreads = 640;
+  static constexpr int kMmaWarp = 16;  // QK issuer, TMEM allocator
+  static constexpr int kLoadWarp = 17;
+  static constexpr int kPvWarp = 18;   // PV issuer
+  static constexpr int kSB = 3;     // S buffers
+  static constexpr int kVer = 6;    // running-max version ring
+  static constexpr int kQBytes = kBR * D * 2;  // 32 KB
+  static constexpr int kKVBytes = BC * D * 2;  // 32 KB (each CTA loads half and multicasts it)
+  static constexpr int kStages = VFA_WS1_STAGES;
+  static constexpr int kCtlBytes = 16 * 1024;
+  static constexpr int kSmem = kCtlBytes + kQBytes + kStages * kKVBytes;
+  static constexpr int kRegBudget = (4 * VFA_WS1_REGS_SOFTMAX + VFA_WS1_REGS_OTHER) * 128;
+  static_assert(kSmem <= kMaxSmem, "shared memory");
+  static_assert(kRegBudget <= kThreads * 96, "register budget (640 threads x 96 registers)");
+  static __device__ __forceinline__ uint32_t s_off(int b) { return static_cast<uint32_t>(b * 128); }
+  static constexpr uint32_t kOOff = 384;
+};
+
+struct __align__(16) Ws1Ctl {
+  uint64_t q_full;
+  uint64_t kv_full[Ws1Cfg::kStages];
+  uint64_t kv_empty[Ws1Cfg::kStages];  // both CTAs' MMAs consumed the stage (multicast commits)
+  uint64_t s_full[Ws1Cfg::kSB];
+  uint64_t p_full[Ws1Cfg::kSB][2];     // P chunk c of the element in buffer b (or S consumed)
+  uint64_t pv_done[2];                 // [pos & 1]: PV of visit position pos completed
+  uint64_t o_final;
+  uint64_t pv_issued[Ws1Cfg::kSB];     // PV issuer -> QK issuer: PV of the element in buffer b enqueued
+  uint64_t mver[Ws1Cfg::kVer];         // running-max version v published (slot v % kVer)
+  uint32_t tmem_base;
+  uint32_t skip[Ws1Cfg::kSB];
+  float zero;
+  float m_pub[Ws1Cfg::kVer][kBR];      // version's running max (log2 units), per row
+  int stab_pub[Ws1Cfg::kVer][kBR];     // version's StateTrace stabilisation block, per row
+  float xmax[2][2][2][kBR];            // [group][exact parity][half][row]: row-max exchange
+  float xinit[2][2][kBR];              // [group][half][row]: m-init partial maxima
+  float xl[2][2][kBR];                 // [group][half][row]: final partial row sums
+  uint8_t xfin[4][kBR];                // [column quarter][row]: output finite flags
+};
+static_assert(sizeof(Ws1Ctl) <= Ws1Cfg::kCtlBytes, "control block");
+
+// exact-update positions before visit position pos (schedule order, src/vfa.py:146-153)
+template <int MODE>
+__device__ __forceinline__ int exact_before(const TileSchedule& s, int pos) {
+  if (all_exact(MODE)) return pos;
+  if (s.reorder) return pos < s.n_spec ? pos : s.n_spec;
+  int c = pos < s.a ? pos : s.a;
+  if (s.b0 <= s.b1 && pos >= s.b0) c += (pos < s.b1 ? pos : s.b1) - s.b0 + 1;
+  return c;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
+    vfa_ws1_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmR,
+                   const FwdArgs a) {
+  using C = Ws1Cfg;
+  constexpr int D = C::D, BC = C::BC, NS = C::kStages, SB = C::kSB, NV = C::kVer;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+  Ws1Ctl* ctl = reinterpret_cast<Ws1Ctl*>(smem_raw);
+  uint8_t* sQ = smem_raw + C::kCtlBytes;
+  uint8_t* sKV = sQ + C::kQBytes;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const uint32_t crank = cluster_ctarank();
+
+  if (tid == 0) {
+    VFA_TRACE_UNIT(a, 0);
+    ctl->zero = 0.f;
+    mbar_init(&ctl->q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&ctl->kv_full[s], 1);
+      mbar_init(&ctl->kv_empty[s], 2);
+    }
+    for (int b = 0; b < SB; ++b) {
+      mbar_init(&ctl->s_full[b], 1);
+      mbar_init(&ctl->p_full[b][0], 8);
+      mbar_init(&ctl->p_full[b][1], 8);
+    }
+    mbar_init(&ctl->pv_done[0], 1);
+    mbar_init(&ctl->pv_done[1], 1);
+    mbar_init(&ctl->o_final, 1);
+    for (int b = 0; b < SB; ++b) mbar_init(&ctl->pv_issued[b], 1);
+    for (int v = 0; v < NV; ++v) mbar_init(&ctl->mver[v], 8);
+    fence_barrier_init();
+  }
+  if (warp == C::kLoadWarp && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmR);
+  }
+  if (warp == C::kMmaWarp) tmem_alloc<512>(&ctl->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's barriers are initialised before any multicast lands
+  tc_fence_after();
+
+#define VFA_WS1_SETUP()                                                  \
+  const uint32_t tbase = ctl->tmem_base;                                 \
+  const Unit unit = decode_unit(a, blockIdx.x >> 1);                     \
+  const int head = unit.h0 + static_cast<int>(crank);                   \
+  const TileSchedule sched = unit_schedule<MODE>(a, unit.qt, BC);        \
+  const int N = sched.vmax;                                              \
+  int nrep = 0;                                                          \
+  const int nchunks = minit_chunks<MODE>(a, sched, BC, &nrep);           \
+  const int G = nchunks + N;                                             \
+  (void)tbase; (void)nrep; (void)G; (void)head
+
+  if (warp >= C::kMmaWarp) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VFA_WS1_REGS_OTHER));
+    if (warp == C::kLoadWarp) {
+      // ============================ TMA producer ============================
+      if (lane == 0) {
+        VFA_WS1_SETUP();
+        const uint64_t pol_q = policy_evict_first();
+        const uint64_t pol_kv = policy_evict_last();
+        mbar_arrive_expect_tx(&ctl->q_full, C::kQBytes);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tma_load_4d(sQ + c * kBR * 128, &tmQ, &ctl->q_full, c * 64, unit.qt * kBR, head, unit.b, pol_q);
+        int stage = 0;
+        uint32_t phase = 0;
+        // each CTA loads 64-column chunk `crank` of the tile (K: dims, V: head-dim columns) and
+        // multicasts it to both CTAs; each CTA's kv_full counts both halves
+        auto load_tile = [&](const CUtensorMap* map, int row) {
+          mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
+          tma_load_4d_mc(sKV + stage * C::kKVBytes + crank * (BC * 128), map, &ctl->kv_full[stage],
+                         static_cast<int>(crank) * 64, row, unit.kvh, unit.b, static_cast<uint16_t>(3), pol_kv);
+          if (++stage == NS) {
+            stage = 0;
+            phase ^= 1;
+          }
+        };
+        auto load_s_operand = [&](int g) {
+          if (g < nchunks)
+            load_tile(&tmR, g * BC);
+          else
+            load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
+        };
+        // the MMA warp's consumption order: S-op(0 .. SB-1); per g: [V(g)], S-op(g + SB)
+        for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
+        for (int g = 0; g < G; ++g) {
+          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+          if (g + SB < G) load_s_operand(g + SB);
+        }
+      }
+    } else if (warp == C::kMmaWarp || warp == C::kPvWarp) {
+      // ============================ MMA issuers ============================
+      // warp 16 issues the QK^T MMAs, warp 18 the PV MMAs: each one's barrier waits (~90
+      // cycles a TRYWAIT, even when the phase is complete) overlap the other's queued MMAs,
+      // where a single issuer's serial waits let the short tcgen05 queue run dry. QK(g + SB)
+      // overwrites the S / P buffer of element g, so the QK issuer enqueues it only after the
+      // PV issuer enqueued PV(g) (pv_issued; the tensor pipe runs MMAs in enqueue order).
+      VFA_WS1_SETUP();
+      const bool is_qk = warp == C::kMmaWarp;
+      constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
+      constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+      constexpr uint32_t kLboK = 1u << 16;
+      constexpr uint32_t kLboV = static_cast<uint32_t>((BC * 128) >> 4) << 16;
+      // UMMA descriptors take the 18-bit shared::cta offset (14 bits of 16-byte units); in a
+      // cluster launch the shared window address also carries the CTA rank (bit 24), masked off
+      const uint32_t q_lo = ((smem_u32(sQ) >> 4) & 0x3FFFu) + kLboK;
+      const uint32_t kv_lo = (smem_u32(sKV) >> 4) & 0x3FFFu;
+      const uint32_t tO = tbase + C::kOOff;
+      // both issuers walk the producer's load sequence (S-op(0 .. SB-1); per g: [V(g)],
+      // [S-op(g + SB)]) and consume only their own tiles
+      int stage = 0;
+      uint32_t phase = 0;
+      auto skip_tile = [&]() {
+        if (++stage == NS) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      auto acquire = [&]() -> int {
+        mbar_wait(&ctl->kv_full[stage], phase);
+        const int st = stage;
+        skip_tile();
+        return st;
+      };
+      auto release = [&](int st) {  // this CTA's MMAs on the stage done -> both producers
+        if (elect_one()) mma_commit_mc(&ctl->kv_empty[st], static_cast<uint16_t>(3));
+        __syncwarp();
+      };
+      auto issue_qk = [&](int b, int st) {
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+            const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + off);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + off);
+            mma_ss(tbase + C::s_off(b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&ctl->s_full[b]);
+        }
+        __syncwarp();
+      };
+      // PV of P chunk c: K-steps {2c, 2c+1} (half 0) and {4+2c, 5+2c} (half 1)
+      auto issue_pv = [&](int b, int st, int c, bool first) {
+        const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
+        const uint32_t tP = tbase + C::s_off(b);
+        if (elect_one()) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
+            mma_ts(tO, tP + kk * 8, db, kIdescPV, (first && i == 0) ? 0u : 1u);
+          }
+        }
+        __syncwarp();
+      };
+      if (is_qk) {
+        mbar_wait(&ctl->q_full, 0);
+        tc_fence_after();
+        for (int g = 0; g < G; ++g) {
+          if (g >= SB) {  // PV(g - SB) enqueued (element g - SB's S / P buffer consumed)
+            mbar_wait(&ctl->pv_issued[g % SB], ((g - SB) / SB) & 1);
+            tc_fence_after();
+          } else if (g > 0 && g - 1 >= nchunks) {
+            // (prologue: nothing to order against)
+          }
+          const int st = acquire();
+          issue_qk(g % SB, st);
+          if (g >= SB && g - SB >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - SB - nchunks, 5);
+          release(st);
+          // skip the V tiles of the load sequence up to the next S operand
+          if (g >= SB - 1 && g + 1 < G) {
+            const int ge = g - (SB - 1);  // element whose V precedes S-op(g + 1) in the sequence
+            if (ge >= nchunks) skip_tile();
+          }
+        }
+      } else {
+        bool o_init = false;
+        // the load sequence starts with min(SB, G) S operands
+        for (int i = 0; i < SB && i < G; ++i) skip_tile();
+        for (int g = 0; g < G; ++g) {
+          const int b = g % SB;
+          const uint32_t ph = (g / SB) & 1;
+          const bool main_blk = g >= nchunks;
+          const int pos = g - nchunks;
+          const int vs = main_blk ? acquire() : -1;
+          if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 7);  // V acquired
+          mbar_wait(&ctl->p_full[b][0], ph);
+          tc_fence_after();
+          if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 4);  // MMA saw P chunk 0
+          const bool skip = skips(MODE) && ctl->skip[b] != 0;
+          if (main_blk && !skip) issue_pv(b, vs, 0, !o_init);
+          mbar_wait(&ctl->p_full[b][1], ph);
+          tc_fence_after();
+          if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 8);  // MMA saw P chunk 1
+          if (main_blk) {
+            if (!skip) issue_pv(b, vs, 1, false);
+            if (lane == 0) VFA_TRACE_EVENT(a, pos, 6);  // PV issued
+            o_init = o_init || !skip;
+            if (elect_one()) mma_commit(&ctl->pv_done[pos & 1]);
+            __syncwarp();
+            release(vs);
+          }
+          if (g + SB < G) {
+            // QK(g + SB) may now overwrite this buffer; skip its S operand in the sequence
+            if (elect_one()) mbar_arrive(&ctl->pv_issued[b]);
+            __syncwarp();
+            skip_tile();
+          }
+        }
+        if (elect_one()) mma_commit(&ctl->o_final);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ============================ softmax groups ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VFA_WS1_REGS_SOFTMAX));
+    VFA_WS1_SETUP();
+    const int gi = warp >> 3;         // group: elements g with g % 2 == gi
+    const int hf = (warp >> 2) & 1;   // half of every S row (64 columns)
+    const int r = tid & 127;
+    constexpr int CP = 64;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tO = tbase + C::kOOff + hf * CP + lane_off;
+    const int R = unit.qt * kBR + r;
+    const float cs = a.c_scale;
+    const float2 cs2 = make_float2(cs, cs);
+    auto tS = [&](int b) { return tbase + C::s_off(b) + lane_off; };
+    auto wait_s = [&](int g) {
+      mbar_wait(&ctl->s_full[g % SB], (g / SB) & 1);
+      tc_fence_after();
+    };
+    auto consumed = [&](int g) {  // S of element g read (m-init chunk) or handed over as P
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&ctl->p_full[g % SB][0]);
+        mbar_arrive(&ctl->p_full[g % SB][1]);
+      }
+    };
+    // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
+    float m2 = -INFINITY;  // running max this group's normalizer part is relative to (log2 units)
+    if (nchunks > 0) {
+      float mx = -INFINITY;
+      for (int g = gi; g < nchunks; g += 2) {
+        wait_s(g);
+        float v[CP];
+        tmem_ld32(tS(g % SB) + hf * CP, v);
+        tmem_ld32(tS(g % SB) + hf * CP + 32, v + 32);
+        tmem_wait_ld();
+        reg_fence32(v);
+        reg_fence32(v + 32);
+        const int valid = nrep - g * BC - hf * CP;
+#pragma unroll
+        for (int e = 0; e < CP; ++e)
+          if (e < valid) mx = fmaxf(mx, v[e]);
+        consumed(g);
+      }
+      ctl->xinit[gi][hf][r] = mx;
+      named_bar_sync(3, 512);
+      m2 = fmaxf(fmaxf(ctl->xinit[0][0][r], ctl->xinit[0][1][r]), fmaxf(ctl->xinit[1][0][r], ctl->xinit[1][1][r])) * cs;
+    }
+    if ((MODE == kVFA || MODE == kVSA) && a.use_m_init && a.m0_tile != nullptr)
+      m2 = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + head) * a.Tr + unit.qt] * cs;
+
+    float l = 0.f;
+    int stab = sched_block(sched, 0);
+    int ver = 0;   // running-max versions (exact positions) this group has incorporated
+    int n_ex = 0;  // exact positions this group processed (row-max exchange buffer parity)
+    int n_visit = 0, n_skipped = 0, n_skipped_special = 0;
+    // bring m2 / l / stab up to version v (published by the other group)
+    auto catch_up = [&](int v) {
+      if (v <= ver) return;
+      const int slot = (v - 1) % NV;
+      mbar_wait(&ctl->mver[slot], ((v - 1) / NV) & 1);
+      const float mn = ctl->m_pub[slot][r];
+      stab = ctl->stab_pub[slot][r];
+      if (mn != m2) {
+        l = __fmul_rn(l, ex2_approx(m2 - mn));  // (m2 = -inf: l is 0, the factor 0)
+        m2 = mn;
+      }
+      ver = v;
+    };
+    for (int g = nchunks + (((gi - nchunks) % 2) + 2) % 2; g < G; g += 2) {
+      const int pos = g - nchunks;
+      const int b = g % SB;
+      const int j = sched_block(sched, pos);
+      const bool special = all_exact(MODE) || sched_is_special(sched, j);
+      const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
+      const int E = exact_before<MODE>(sched, pos);
+      ++n_visit;
+      catch_up(E);  // the running max after every exact position before this one
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 3);  // (ws1 slots: see scripts/trace_timeline.py --ws1)
+      wait_s(g);
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 0);
+      if (r == 0 && hf == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
+      float v[CP];
+      const bool split = MODE == kVFA && !special;  // no row statistic before the exponentials
+      tmem_ld32(tS(b) + hf * CP, v);
+      if (split) {
+        tmem_wait_ld();
+        reg_fence32(v);
+        tmem_ld32(tS(b) + hf * CP + 32, v + 32);
+      } else {
+        tmem_ld32(tS(b) + hf * CP + 32, v + 32);
+        tmem_wait_ld();
+        reg_fence32(v);
+        reg_fence32(v + 32);
+      }
+      const int lim = R - (j - 1) * BC - hf * CP;
+      if (mask) {  // entrywise causal mask (src/reference.py:93-96)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        if (!split) {
+#pragma unroll
+          for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        }
+      }
+      bool skipped = false;
+      bool rescale = false;
+      float f = 1.0f;
+      if (MODE == kVSA && !special) {
+        // VSA frozen block: the skip test only (src/sparse.py:296-304), against the frozen max
+        const float pm2 = part_max<CP>(v) * cs;
+        const bool below = (pm2 - fmaxf(m2, pm2) < a.log2_lambda) ||
+                           (pm2 == -INFINITY && m2 == -INFINITY && a.log2_lambda != -INFINITY);
+        skipped = named_bar_and(1 + gi, 256, below);
+        if (skipped) ++n_skipped;
+      } else if (special) {
+        // exact update (src/vfa.py:202-208): row max over both halves, then publish version E+1
+        const int xp = n_ex & 1;
+        ctl->xmax[gi][xp][hf][r] = part_max<CP>(v);
+        named_bar_sync(1 + gi, 256);
+        const float mt2 = fmaxf(ctl->xmax[gi][xp][0][r], ctl->xmax[gi][xp][1][r]) * cs;
+        ++n_ex;
+        const float m2n = fmaxf(m2, mt2);
+        if (skips(MODE)) {
+          const bool below = (mt2 - m2n < a.log2_lambda) ||
+                             (mt2 == -INFINITY && m2n == -INFINITY && a.log2_lambda != -INFINITY);
+          skipped = named_bar_and(1 + gi, 256, below);
+        }
+        if (skipped) {
+          ++n_skipped;
+          ++n_skipped_special;
+        } else {
+          f = (m2n == -INFINITY) ? 1.0f : ex2_approx(m2 - m2n);
+          if (m2n > m2) stab = j;
+          m2 = m2n;
+          l = __fmul_rn(l, f);
+          rescale = pos > 0 && !__all_sync(0xffffffffu, f == 1.0f);
+        }
+        const int slot = E % NV;
+        if (hf == 0) {
+          ctl->m_pub[slot][r] = m2;
+          ctl->stab_pub[slot][r] = stab;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl->mver[slot]);
+        ver = E + 1;
+      }
+      if (skips(MODE) && r == 0 && hf == 0) ctl->skip[b] = skipped ? 1u : 0u;
+      if (a.skip_trace && r == 0 && hf == 0)
+        a.skip_trace[((static_cast<size_t>(unit.b) * a.Hq + head) * a.Tr + unit.qt) * a.Tc + pos] = skipped ? 2 : 1;
+      if (rescale) {
+        // O holds PV of every earlier position once PV(pos-1) completed (S(pos) ready implies
+        // PV(pos-3) did, and PV(pos) waits for this group's P, so pv_done[(pos-1) & 1] is in or
+        // just past phase (pos-1) >> 1): wait for it, then rescale this half of the row
+        mbar_wait(&ctl->pv_done[(pos - 1) & 1], ((pos - 1) >> 1) & 1);
+        tc_fence_after();
+        const float2 f2 = make_float2(f, f);
+#pragma unroll 1
+        for (int c = 0; c < CP / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+          reg_fence16(o);
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const float2 x = __fmul2_rn(make_float2(o[e], o[e + 1]), f2);
+            o[e] = x.x;
+            o[e + 1] = x.y;
+          }
+          tmem_st16(tO + c * 16, reinterpret_cast<const uint32_t*>(o));
+        }
+        tmem_wait_st();
+      }
+      if (!skipped) {
+        const float nm = (m2 == -INFINITY ? 0.f : -m2);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float nmc = nm;
+          if (c > 0) {  // ordered after chunk 0's hand-off (see ws_kernel.cuh)
+            float z;
+            asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(z) : "r"(smem_u32(&ctl->zero)) : "memory");
+            nmc = nm + z;
+            if (split) {
+              tmem_wait_ld();
+              reg_fence32(v + 32);
+              if (mask) {
+#pragma unroll
+                for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+              }
+            }
+          }
+          const float2 nmu2 = make_float2(nmc, nmc);
+          uint32_t u[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float2 x = __ffma2_rn(make_float2(v[c * 32 + e], v[c * 32 + e + 1]), cs2, nmu2);
+            float2 p;
+            if (((e >> 1) & 7) >= 8 - VFA_WS1_EMU) {
+              p = ex2_poly2(x);  // degree 4, |rel err| < 3e-6
+            } else {
+              p.x = ex2_approx(x.x);
+              p.y = ex2_approx(x.y);
+            }
+            v[c * 32 + e] = p.x;
+            v[c * 32 + e + 1] = p.y;
+            u[e >> 1] = pack_bf16x2(p.x, p.y);
+          }
+          tmem_st16(tS(b) + hf * (CP / 2) + c * 16, u);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->p_full[b][c]);
+          if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, c == 0 ? 2 : 1);
+        }
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int e = 0; e < CP; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
+        l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
+      } else {
+        if (split) tmem_wait_ld();
+        consumed(g);
+      }
+    }
+    if (r == 0 && hf == 0 && gi == 1) VFA_TRACE_UNIT(a, 2);
+    // ---- finalize (src/core.py:101-109): both groups' parts relative to the final max
+    catch_up(exact_before<MODE>(sched, N));
+    ctl->xl[gi][hf][r] = l;
+    named_bar_sync(3, 512);
+    const float lsum = __fadd_rn(__fadd_rn(ctl->xl[0][0][r], ctl->xl[0][1][r]), __fadd_rn(ctl->xl[1][0][r], ctl->xl[1][1][r]));
+    const int qq = warp >> 2;  // this thread's 32-column quarter of the O row
+    const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + head) * a.Lq + R;
+    const unsigned srow = static_cast<unsigned>(lrow + a.row_base);
+    if (qq == 0) {
+      if (a.lse) a.lse[lrow] = (lsum == 0.f && m2 != -INFINITY) ? m2 * kLn2 : (m2 + __log2f(lsum)) * kLn2;
+      if (a.stab) a.stab[lrow] = stab;
+      if (a.status && lsum == 0.f) {
+        if (m2 == -INFINITY) {
+          atomicOr(&a.status[VFA_STATUS_FLAGS], 1u);
+          atomicMin(&a.status[VFA_STATUS_MASKED_ROW], srow);
+        } else {
+          atomicOr(&a.status[VFA_STATUS_FLAGS], 2u);
+          atomicMin(&a.status[VFA_STATUS_UNDERFLOW_ROW], srow);
+        }
+      }
+    }
+    mbar_wait(&ctl->o_final, 0);
+    tc_fence_after();
+    const float inv = 1.0f / lsum;
+    __nv_bfloat16* orow = a.o + unit.b * a.o_sb + head * a.o_sh + static_cast<long long>(R) * a.o_sr + qq * 32;
+    bool finite = true;
+    {
+      float o[32];
+      tmem_ld32(tbase + C::kOOff + qq * 32 + lane_off, o);
+      tmem_wait_ld();
+      reg_fence32(o);
+      uint32_t u[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float o0 = o[e] * inv, o1 = o[e + 1] * inv;
+        finite = finite && isfinite(o0) && isfinite(o1);
+        u[e >> 1] = pack_bf16x2(o0, o1);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(orow);
+      dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+      dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
+      dst[2] = make_uint4(u[8], u[9], u[10], u[11]);
+      dst[3] = make_uint4(u[12], u[13], u[14], u[15]);
+    }
+    if (a.status) {
+      ctl->xfin[qq][r] = finite ? 1 : 0;
+      named_bar_sync(3, 512);
+      if (qq == 0 && !(ctl->xfin[0][r] && ctl->xfin[1][r] && ctl->xfin[2][r] && ctl->xfin[3][r])) {
+        atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
+        atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
+      }
+    }
+    if (a.stats && r == 0 && hf == 0) {
+      const int n_exact = all_exact(MODE) ? N : sched.n_spec;
+      if (gi == 0) {
+        atomicAdd(&a.stats[VFA_STAT_VISITED], static_cast<unsigned long long>(N));
+        atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(n_exact));
+        atomicAdd(&a.stats[VFA_STAT_FROZEN], static_cast<unsigned long long>(N - n_exact));
+      }
+      if (n_skipped) {
+        atomicAdd(&a.stats[VFA_STAT_SKIPPED], static_cast<unsigned long long>(n_skipped));
+        // skipped blocks leave their class (counted once per tile, as in vfa_fwd_kernel)
+        atomicAdd(&a.stats[VFA_STAT_SPECIAL], static_cast<unsigned long long>(-n_skipped_special));
+        atomicAdd(&a.stats[VFA_STAT_FROZEN], static_cast<unsigned long long>(-(n_skipped - n_skipped_special)));
+      }
+    }
+    (void)n_visit;
+  }
+#undef VFA_WS1_SETUP
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer may still multicast into / commit onto this CTA's shared memory
+  if (tid == 0) VFA_TRACE_UNIT(a, 3);
+  if (warp == C::kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc<512>(ctl->tmem_base);
+  }
+}
+
+}  // namespace vfa

@@ -27,6 +27,7 @@ ap.add_argument("--sink", type=float, default=0.0, help="planted-sink boost (C3 
 ap.add_argument("--lam", type=float, default=1e-2)
 ap.add_argument("--pair", type=int, default=0, help="cta_pair (2 = CTA pairs)")
 ap.add_argument("--split", type=int, default=0, help="softmax_split (0: per-variant default)")
+ap.add_argument("--ws1", action="store_true", help="the decoupled one-tile kernel's slot layout")
 ap.add_argument("--seq", type=int, default=0, help="sequence length override (C2 heads / head dim)")
 a = ap.parse_args()
 cfg = dict(CONFIGS["c2"])
@@ -43,6 +44,8 @@ r.p.softmax_split = a.split
 T = cfg["L"] // a.k_block
 # CTAs: one per unit (two heads); CTA pairs cover four heads per cluster when the group allows
 units = cfg["B"] * cfg["Hkv"] * (cfg["L"] // 128) * (cfg["Hq"] // cfg["Hkv"] // 2)
+if a.ws1:
+    units *= 2  # one CTA per query tile
 NS_ = 32  # vfa_kernel.cuh kTraceSlots
 buf = torch.zeros(T * NS_ + units * 4, dtype=torch.int64, device=dev)
 sh = torch.cuda.current_stream().cuda_stream
@@ -67,6 +70,19 @@ n = int((tr[:, 1] > 0).sum())
 tr = tr[:n]
 t0 = tr[tr > 0].min()
 tr = np.where(tr > 0, tr - t0, np.nan)
+if a.ws1:
+    sl = slice(4, n - 4)
+    print(f"variant={a.variant} visited={n} total={np.nanmax(tr):.0f} cycles -> {np.nanmax(tr) / n:.0f} cycles per block")
+    S, P, P0, E, seen0, qk, pv, vacq, seen1 = (tr[:, i] for i in (0, 1, 2, 3, 4, 5, 6, 7, 8))
+    med = lambda x: np.nanmedian(x[sl])  # noqa: E731
+    print(f" softmax: waits for S {med(S - E):.0f}; S -> chunk-0 P {med(P0 - S):.0f}; S -> P done {med(P - S):.0f};"
+          f" per-group period (pos -> pos+2) {med(S[2:] - S[:-2]):.0f}; next S after P done {med(S[2:] - P[:-2]):.0f}")
+    print(f" MMA: V acquired {med(vacq - P0):.0f} after chunk-0 P; sees chunk 0 +{med(seen0 - P0):.0f}, chunk 1 +{med(seen1 - P):.0f};"
+          f" PV issued +{med(pv - P):.0f} after P done; QK(g+3) issued +{med(qk - pv):.0f} after PV;"
+          f" PV period {med(np.diff(pv)):.0f}")
+    for i in range(20, min(26, n)):
+        print(" ", np.round(tr[i, :9]).astype(int).tolist())
+    sys.exit(0)
 print(f"variant={a.variant} k_block={a.k_block} visited={n} total={np.nanmax(tr):.0f} cycles "
       f"-> {np.nanmax(tr) / n:.0f} cycles per block (both query tiles)")
 for t in (0, 1):
