@@ -464,7 +464,8 @@ def main_ours(args):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(),
-                         "kernel": ("vfa_ws_kernel<VFA> (warp-specialised, d=128, Bc=128, two query tiles per CTA)"
+                         "kernel": ("vfa_ws1_kernel<VFA> (decoupled softmax, one query tile per CTA, K/V "
+                                    "multicast over 2-CTA clusters)"
                                     if (d, args.k_block) == (128, 128) and Hq // Hkv % 2 == 0
                                     else f"vfa_fwd_kernel<{d},{args.k_block},2,VFA>") + " (per rank)",
                          "peak_source": f"{peak_kind} burst bf16 (MEASURED_PEAKS.json)",

@@ -288,6 +288,12 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
   __syncwarp();
 }
 
+// Two threads per S row (the warp-specialised kernels): the thread owning half hf of a row
+// (keys 64*hf .. 64*hf + 63) stores its packed-bf16 P over the first 32 of its own 64 S
+// columns, which it has already loaded -- never over the other half's columns, which that
+// thread may still be loading. TMEM column (relative to the S buffer) of PV K-step kk's P:
+__host__ __device__ constexpr uint32_t p_col(int kk) { return static_cast<uint32_t>((kk >> 2) * 64 + (kk & 3) * 8); }
+
 // ------------------------------------------------------------------------------------
 // Softmax element math. x = s * (scale*log2 e) - m2 in packed pairs (FFMA2); P = exp2(x)
 // on MUFU.EX2 for most pairs and on the FMA pipe (degree-4 polynomial, |rel err| < 3e-6)

@@ -15,7 +15,7 @@
 //   warp 17     TMA producer
 //   warp 18     PV issuer
 //   warp 19     idle
-// TMEM: S buffers at 0 / 128 / 256 (P packed bf16 over the first 64 columns of its S buffer),
+// TMEM: S buffers at 0 / 128 / 256 (P packed bf16 in columns 0-31 / 64-95 of its S buffer, see p_col),
 // O at 384. The MMA issues QK for element g + 3 as soon as PV(g) is issued, so S is up to
 // three blocks ahead and the two groups' exponentials run back to back: the softmax is never
 // waiting on a P -> PV -> QK -> S round trip (the limit of the ping-pong kernels).
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           for (int i = 0; i < 4; ++i) {
             const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
-            mma_ts(tO, tP + kk * 8, db, kIdescPV, (first && i == 0) ? 0u : 1u);
+            mma_ts(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             v[c * 32 + e + 1] = p.y;
             u[e >> 1] = pack_bf16x2(p.x, p.y);
           }
-          tmem_st16(tS(b) + hf * (CP / 2) + c * 16, u);
+          tmem_st16(tS(b) + hf * CP + c * 16, u);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();

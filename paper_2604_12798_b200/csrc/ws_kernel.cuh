@@ -12,7 +12,7 @@
 //               16 allocates TMEM
 //   warp 18     TMA producer
 //   warp 19     idle (completes the last warpgroup)
-// TMEM (512 columns): S_t at t*128 (P_t as packed bf16 over its first 64 columns), O_t at
+// TMEM (512 columns): S_t at t*128 (P_t packed bf16 in its columns 0-31 / 64-95, see p_col), O_t at
 // 256 + t*128. Per key block and tile the tensor pipe runs PV_t, QK_t(next); the issuers'
 // turn-taking keeps the order PV_0 QK_0 PV_1 QK_1, so each tile's softmax runs under the other
 // tile's MMAs.
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
           for (int i = 0; i < 2 * kKS; ++i) {
             const int kk = (i / kKS) * 4 + c * kKS + (i % kKS);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
-            mma_ts(tO, tS + kk * 8, db, kIdescPV, (first && i == 0) ? 0u : 1u);
+            mma_ts(tO, tS + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -550,9 +550,9 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
           // P of this half's chunk c (packed bf16, kCW/2 TMEM columns): PV K-steps
           // 4*hf + c*kCW/16 .. +kCW/16
           if constexpr (kCW == 32)
-            tmem_st16(tS + hf * (CP / 2) + c * (kCW / 2), u);
+            tmem_st16(tS + hf * CP + c * (kCW / 2), u);
           else
-            tmem_st8(tS + hf * (CP / 2) + c * (kCW / 2), u);
+            tmem_st8(tS + hf * CP + c * (kCW / 2), u);
           if (r == 0 && hf == 0 && c == 0) VFA_TRACE_EVENT(a, pos, 22 + 4 * t);
           tmem_wait_st();
           tc_fence_before();

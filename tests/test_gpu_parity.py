@@ -478,6 +478,24 @@ def test_host_pipeline_bitwise_equals_device_path(variant, chunk, qchunk, b):
     assert torch.equal(o3, o2) and torch.equal(l3, l2)
 
 
+@pytest.mark.parametrize("variant", ["vfa", "vsa", "fa"])
+def test_long_rows_host_pipeline_and_reruns_bitwise(variant):
+    # long rows (128 key blocks per query tile at the end) through the warp-specialised kernels:
+    # reruns and the host pipeline (kernels on two overlapping streams) are bitwise equal to the
+    # device path -- a cross-thread TMEM hazard between the two halves of an S row (P of one half
+    # stored over S columns the other half was still loading) showed up only this way
+    from paper_2604_12798_b200 import attention_forward
+    L, Hq, Hkv = 16384, 4, 1
+    q, k, v = _rand((1, Hq, L, 128), 201), _rand((1, Hkv, L, 128), 202), _rand((1, Hkv, L, 128), 203)
+    kw = dict(variant=variant, causal=True, lam=1e-2 if variant == "vsa" else None)
+    o1, l1, _, _ = _run_gpu(q, k, v, **kw)
+    o2, l2, _, _ = _run_gpu(q, k, v, **kw)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    o3, l3, _ = attention_forward(qh, kh, vh, **kw)
+    assert torch.equal(o3, o1.cpu()) and torch.equal(l3, l1.cpu())
+
+
 @pytest.mark.parametrize("qkind", ["q_absmax", "q_mean", "q_sabsmax"])
 @pytest.mark.parametrize("variant", ["vfa", "vsa"])
 def test_host_pipeline_blockwise_qkind_gqa4(qkind, variant):
