@@ -117,8 +117,11 @@ typedef struct VfaParams {
   int32_t monitor;      /* count exp-argument overflows (OverflowMonitor, src/vfa.py:109-128) */
   double lam;           /* VSA threshold lambda in (0, 1]; <= 0 disables skipping (SkipConfig.lam=None) */
   int32_t krepr_precomputed; /* 1: workspace already holds vfa_krepr() output for this K; skip recomputing */
-  int32_t softmax_split; /* threads sharing one row of a query tile: 0 = per-variant default,
-                           1 = a softmax warpgroup per query tile (one thread per row),
+  int32_t softmax_split; /* 0 = default kernel choice: at d = 128 with 128-row blocks and an even
+                           GQA group the warp-specialised kernels (two threads per row; VFA / VSA
+                           the decoupled one-tile kernel, FA the ping-pong kernel), elsewhere the
+                           general kernel's per-variant layout. An explicit layout runs the general
+                           kernel: 1 = a softmax warpgroup per query tile (one thread per row),
                            2 = per-tile warp sets, 4 = all softmax warps serve both tiles */
   double tau;           /* BLASST-FA4 rescale elision: max increase <= tau * ln 2 (SkipConfig.tau) */
   int32_t cta_pair;     /* 0 = default, 1 = one CTA per unit, 2 = CTA pairs (even GQA group, d = 128):
