@@ -175,8 +175,20 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         uint32_t phase = 0;
         // each CTA loads 64-column chunk `crank` of the tile (K: dims, V: head-dim columns) and
         // multicasts it to both CTAs; each CTA's kv_full counts both halves
+#ifndef VFA_WS1_DBG_SKIP
+#define VFA_WS1_DBG_SKIP 0  // timing experiments only (wrong results): 1 = no V transfers
+#endif
+        int nload = 0;
         auto load_tile = [&](const CUtensorMap* map, int row) {
           mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+          if (VFA_WS1_DBG_SKIP && nload++ >= 8 && map == &tmV) {
+            mbar_arrive(&ctl->kv_full[stage]);
+            if (++stage == NS) {
+              stage = 0;
+              phase ^= 1;
+            }
+            return;
+          }
           mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
           tma_load_4d_mc(sKV + stage * C::kKVBytes + crank * (BC * 128), map, &ctl->kv_full[stage],
                          static_cast<int>(crank) * 64, row, unit.kvh, unit.b, static_cast<uint16_t>(3), pol_kv);

@@ -65,7 +65,7 @@ struct WsCfg {
 #endif
   // K/V ring: the MMA issuers hold V(g) and K(g+1); the other stages are loads in flight
   static constexpr int kStages = VFA_WS_STAGES;
-  static constexpr int kCtlBytes = 8192;  // control block first, tiles from the next 1 KB boundary
+  static constexpr int kCtlBytes = 8192;  // control block after the tiles
   static constexpr int kSmem = kCtlBytes + NQ * kQBytes + kStages * kKVBytes;
   static __device__ __forceinline__ uint32_t s_off(int t) { return static_cast<uint32_t>(t * 128); }
   static __device__ __forceinline__ uint32_t o_off(int t) { return static_cast<uint32_t>(256 + t * 128); }
@@ -110,9 +110,10 @@ __global__ void __launch_bounds__(WsCfg::kThreads, 1)
   // the dynamic shared window starts 1 KB aligned (no static shared memory): control block,
   // then the SWIZZLE_128B tiles at a 1 KB boundary
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
-  WsCtl* ctl = reinterpret_cast<WsCtl*>(smem_raw);
-  uint8_t* sQ = smem_raw + C::kCtlBytes;
+  // SWIZZLE_128B tiles from the (1 KB aligned) start of the window, control block after them
+  uint8_t* sQ = smem_raw;
   uint8_t* sKV = sQ + 2 * C::kQBytes;
+  WsCtl* ctl = reinterpret_cast<WsCtl*>(sKV + NS * C::kKVBytes);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
