@@ -756,7 +756,7 @@ def main():
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--e2e-chunk", type=int, default=1, help="KV heads per pipelined host chunk")
     ap.add_argument("--e2e-qchunk", type=int, default=2, help="query heads per pipelined sub-chunk (0: all)")
     ap.add_argument("--no-sweeps", action="store_true", help="skip the C3 / C5 / vendor extra keys")

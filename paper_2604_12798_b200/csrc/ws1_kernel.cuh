@@ -39,6 +39,9 @@ namespace vfa {
 #ifndef VFA_WS1_EMU
 #define VFA_WS1_EMU 1  // element pairs (of 8) per 32-column chunk on the FMA-pipe exp2
 #endif
+#ifndef VFA_WS1_PREFETCH
+#define VFA_WS1_PREFETCH 0  // 1: load the next element's first S columns before finishing this one (measured 7 % slower: spills)
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -249,8 +252,16 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         if (elect_one()) mma_commit_mc(&ctl->kv_empty[st], static_cast<uint16_t>(3));
         __syncwarp();
       };
+#ifndef VFA_WS1_DBG_NOMMA
+#define VFA_WS1_DBG_NOMMA 0  // timing experiments only (wrong results): no MMAs, barriers only
+#endif
       auto issue_qk = [&](int b, int st) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
+        if (VFA_WS1_DBG_NOMMA) {
+          if (elect_one()) mma_commit(&ctl->s_full[b]);
+          __syncwarp();
+          return;
+        }
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -265,6 +276,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       };
       // PV of P chunk c: K-steps {2c, 2c+1} (half 0) and {4+2c, 5+2c} (half 1)
       auto issue_pv = [&](int b, int st, int c, bool first) {
+        if (VFA_WS1_DBG_NOMMA) return;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
         const uint32_t tP = tbase + C::s_off(b);
         if (elect_one()) {
@@ -404,6 +416,11 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       }
       ver = v;
     };
+    // S of the group's next element is usually ready long before this one is done (QK runs up
+    // to three elements ahead): its first 32 columns are loaded right after this element's last
+    // P hand-off, so the TMEM load latency overlaps the tail of this element and the loop
+    float v[CP];
+    bool prefetched = false;  // chunk 0 of element g is already loading into v[0 .. 31]
     for (int g = nchunks + (((gi - nchunks) % 2) + 2) % 2; g < G; g += 2) {
       const int pos = g - nchunks;
       const int b = g % SB;
@@ -413,13 +430,14 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       const int E = exact_before<MODE>(sched, pos);
       ++n_visit;
       catch_up(E);  // the running max after every exact position before this one
-      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 3);  // (ws1 slots: see scripts/trace_timeline.py --ws1)
-      wait_s(g);
-      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 0);
+      if (!prefetched) {
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 3);  // (ws1 slots: see scripts/trace_timeline.py --ws1)
+        wait_s(g);
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 0);
+        tmem_ld32(tS(b) + hf * CP, v);
+      }
       if (r == 0 && hf == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
-      float v[CP];
       const bool split = MODE == kVFA && !special;  // no row statistic before the exponentials
-      tmem_ld32(tS(b) + hf * CP, v);
       if (split) {
         tmem_wait_ld();
         reg_fence32(v);
@@ -509,6 +527,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       }
       if (!skipped) {
         const float nm = (m2 == -INFINITY ? 0.f : -m2);
+        // row sum (src/tensor.py:81-89) in two packed accumulators, pairs in column order
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           float nmc = nm;
@@ -537,8 +557,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
               p.x = ex2_approx(x.x);
               p.y = ex2_approx(x.y);
             }
-            v[c * 32 + e] = p.x;
-            v[c * 32 + e + 1] = p.y;
+            acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], p);
             u[e >> 1] = pack_bf16x2(p.x, p.y);
           }
           tmem_st16(tS(b) + hf * CP + c * 16, u);
@@ -548,13 +567,18 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           if (lane == 0) mbar_arrive(&ctl->p_full[b][c]);
           if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, c == 0 ? 2 : 1);
         }
-        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int e = 0; e < CP; e += 2) acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], make_float2(v[e], v[e + 1]));
         l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
       } else {
         if (split) tmem_wait_ld();
         consumed(g);
+      }
+      // start loading the group's next element (v is free: the row sum was taken on the fly)
+      prefetched = VFA_WS1_PREFETCH && g + 2 < G;
+      if (prefetched) {
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos + 2, 3);
+        wait_s(g + 2);
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos + 2, 0);
+        tmem_ld32(tS((g + 2) % SB) + hf * CP, v);
       }
     }
     if (r == 0 && hf == 0 && gi == 1) VFA_TRACE_UNIT(a, 2);
