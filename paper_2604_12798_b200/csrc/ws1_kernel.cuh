@@ -42,6 +42,12 @@ namespace vfa {
 #ifndef VFA_WS1_PREFETCH
 #define VFA_WS1_PREFETCH 0  // 1: load the next element's first S columns before finishing this one (measured 7 % slower: spills)
 #endif
+#ifndef VFA_WS1_QK_PROBE
+#define VFA_WS1_QK_PROBE 0  // QK k-steps issued before probing the next element's waits (0: no probe; 2 / 4 / 6 measured 3-8 % slower)
+#endif
+#ifndef VFA_WS1_PV_SKIPFIRST
+#define VFA_WS1_PV_SKIPFIRST 0  // 1: PV issuer frees a skipped element's buffer before its V lands (no gain, -3 % dense VSA)
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -100,6 +106,21 @@ __device__ __forceinline__ int exact_before(const TileSchedule& s, int pos) {
   if (s.b0 <= s.b1 && pos >= s.b0) c += (pos < s.b1 ? pos : s.b1) - s.b0 + 1;
   return c;
 }
+
+#ifndef VFA_WS1_FASTWAIT
+#define VFA_WS1_FASTWAIT 0  // bit 0: issuer / producer waits, bit 1: softmax waits probe the phase first
+#endif
+// mbarrier wait that first probes the phase (test_wait never suspends): a try_wait costs ~90
+// cycles even on a completed phase, which the MMA issuers pay on every element
+template <int BIT>
+__device__ __forceinline__ void ws1_wait(uint64_t* bar, uint32_t parity) {
+  if ((VFA_WS1_FASTWAIT >> BIT) & 1) {
+    if (mbar_test_wait(bar, parity)) return;
+  }
+  mbar_wait(bar, parity);
+}
+#define iwait ws1_wait<0>
+#define swait ws1_wait<1>
 
 template <int MODE>
 __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
@@ -183,7 +204,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
 #endif
         int nload = 0;
         auto load_tile = [&](const CUtensorMap* map, int row) {
-          mbar_wait(&ctl->kv_empty[stage], phase ^ 1);
+          iwait(&ctl->kv_empty[stage], phase ^ 1);
           if (VFA_WS1_DBG_SKIP && nload++ >= 8 && map == &tmV) {
             mbar_arrive(&ctl->kv_full[stage]);
             if (++stage == NS) {
@@ -209,8 +230,14 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         // the MMA warp's consumption order: S-op(0 .. SB-1); per g: [V(g)], S-op(g + SB)
         for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
         for (int g = 0; g < G; ++g) {
-          if (g >= nchunks) load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
-          if (g + SB < G) load_s_operand(g + SB);
+          if (g >= nchunks) {
+            load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
+            VFA_TRACE_EVENT(a, g - nchunks, 12);  // V(g) TMA issued
+          }
+          if (g + SB < G) {
+            load_s_operand(g + SB);
+            if (g + SB >= nchunks) VFA_TRACE_EVENT(a, g + SB - nchunks, 11);  // K(g + SB) TMA issued
+          }
         }
       }
     } else if (warp == C::kMmaWarp || warp == C::kPvWarp) {
@@ -243,7 +270,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         }
       };
       auto acquire = [&]() -> int {
-        mbar_wait(&ctl->kv_full[stage], phase);
+        iwait(&ctl->kv_full[stage], phase);
         const int st = stage;
         skip_tile();
         return st;
@@ -255,22 +282,24 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
 #ifndef VFA_WS1_DBG_NOMMA
 #define VFA_WS1_DBG_NOMMA 0  // timing experiments only (wrong results): no MMAs, barriers only
 #endif
-      auto issue_qk = [&](int b, int st) {
+      // QK MMAs k-steps [k0, k1) into S buffer b; the commit to s_full after the last
+      auto issue_qk = [&](int b, int st, int k0, int k1) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
         if (VFA_WS1_DBG_NOMMA) {
-          if (elect_one()) mma_commit(&ctl->s_full[b]);
+          if (k1 == D / 16 && elect_one()) mma_commit(&ctl->s_full[b]);
           __syncwarp();
           return;
         }
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
+            if (kk < k0 || kk >= k1) continue;
             const uint32_t off = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
             const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + off);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + off);
             mma_ss(tbase + C::s_off(b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
           }
-          mma_commit(&ctl->s_full[b]);
+          if (k1 == D / 16) mma_commit(&ctl->s_full[b]);
         }
         __syncwarp();
       };
@@ -292,22 +321,47 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       if (is_qk) {
         mbar_wait(&ctl->q_full, 0);
         tc_fence_after();
+        // the V tile of the load sequence between S-op(g) and S-op(g + 1), if any
+        auto skip_v = [&](int g) {
+          if (g >= SB - 1 && g + 1 < G && g - (SB - 1) >= nchunks) skip_tile();
+        };
+        // Both waits of element g + 1 (its buffer's PV issued, its K landed) are probed while
+        // QK(g)'s first k-steps are queued: when both are already complete (S far ahead of the
+        // softmax, e.g. VSA skipping most blocks) QK(g + 1) follows QK(g) with no pipe bubble; a
+        // blocking wait after QK(g)'s last k-step would let the three-deep MMA queue drain.
+        int pre = -1;  // stage of S-op(g), acquired by the probe during QK(g - 1)
         for (int g = 0; g < G; ++g) {
-          if (g >= SB) {  // PV(g - SB) enqueued (element g - SB's S / P buffer consumed)
-            mbar_wait(&ctl->pv_issued[g % SB], ((g - SB) / SB) & 1);
-            tc_fence_after();
-          } else if (g > 0 && g - 1 >= nchunks) {
-            // (prologue: nothing to order against)
+          int st = pre;
+          if (pre < 0) {
+            if (g >= SB) {  // PV(g - SB) enqueued (element g - SB's S / P buffer consumed)
+              iwait(&ctl->pv_issued[g % SB], ((g - SB) / SB) & 1);
+            }
+            if (g >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - nchunks, 14);  // buffer free
+            st = acquire();
+            skip_v(g);
           }
-          const int st = acquire();
-          issue_qk(g % SB, st);
+          tc_fence_after();
+          pre = -1;
+          if (g >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - nchunks, 13);  // K acquired
+          constexpr int kProbe = VFA_WS1_QK_PROBE;
+          if (kProbe > 0) {
+            issue_qk(g % SB, st, 0, kProbe);
+            if (g + 1 < G) {
+              bool ok = g + 1 < SB || mbar_test_wait(&ctl->pv_issued[(g + 1) % SB], ((g + 1 - SB) / SB) & 1);
+              ok = ok && mbar_test_wait(&ctl->kv_full[stage], phase);
+              if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
+                if (g + 1 >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g + 1 - nchunks, 14);
+                pre = stage;
+                skip_tile();
+                skip_v(g + 1);
+              }
+            }
+            issue_qk(g % SB, st, kProbe, D / 16);
+          } else {
+            issue_qk(g % SB, st, 0, D / 16);
+          }
           if (g >= SB && g - SB >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - SB - nchunks, 5);
           release(st);
-          // skip the V tiles of the load sequence up to the next S operand
-          if (g >= SB - 1 && g + 1 < G) {
-            const int ge = g - (SB - 1);  // element whose V precedes S-op(g + 1) in the sequence
-            if (ge >= nchunks) skip_tile();
-          }
         }
       } else {
         bool o_init = false;
@@ -318,14 +372,36 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           const uint32_t ph = (g / SB) & 1;
           const bool main_blk = g >= nchunks;
           const int pos = g - nchunks;
+          if (VFA_WS1_PV_SKIPFIRST && skips(MODE) && main_blk) {
+            // a skipped element frees its S / P buffer as soon as the softmax read S: tell the
+            // QK issuer before waiting for the element's (unused) V tile
+            iwait(&ctl->p_full[b][0], ph);
+            if (ctl->skip[b] != 0) {
+              if (lane == 0) VFA_TRACE_EVENT(a, pos, 4);
+              iwait(&ctl->p_full[b][1], ph);
+              if (g + SB < G) {
+                if (elect_one()) mbar_arrive(&ctl->pv_issued[b]);
+                __syncwarp();
+              }
+              const int vs = acquire();
+              if (lane == 0) VFA_TRACE_EVENT(a, pos, 7);
+              if (lane == 0) VFA_TRACE_EVENT(a, pos, 8);
+              if (lane == 0) VFA_TRACE_EVENT(a, pos, 6);
+              if (elect_one()) mma_commit(&ctl->pv_done[pos & 1]);
+              __syncwarp();
+              release(vs);
+              if (g + SB < G) skip_tile();
+              continue;
+            }
+          }
           const int vs = main_blk ? acquire() : -1;
           if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 7);  // V acquired
-          mbar_wait(&ctl->p_full[b][0], ph);
+          iwait(&ctl->p_full[b][0], ph);
           tc_fence_after();
           if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 4);  // MMA saw P chunk 0
           const bool skip = skips(MODE) && ctl->skip[b] != 0;
           if (main_blk && !skip) issue_pv(b, vs, 0, !o_init);
-          mbar_wait(&ctl->p_full[b][1], ph);
+          iwait(&ctl->p_full[b][1], ph);
           tc_fence_after();
           if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 8);  // MMA saw P chunk 1
           if (main_blk) {
@@ -362,7 +438,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     const float2 cs2 = make_float2(cs, cs);
     auto tS = [&](int b) { return tbase + C::s_off(b) + lane_off; };
     auto wait_s = [&](int g) {
-      mbar_wait(&ctl->s_full[g % SB], (g / SB) & 1);
+      swait(&ctl->s_full[g % SB], (g / SB) & 1);
       tc_fence_after();
     };
     auto consumed = [&](int g) {  // S of element g read (m-init chunk) or handed over as P
@@ -407,7 +483,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     auto catch_up = [&](int v) {
       if (v <= ver) return;
       const int slot = (v - 1) % NV;
-      mbar_wait(&ctl->mver[slot], ((v - 1) / NV) & 1);
+      swait(&ctl->mver[slot], ((v - 1) / NV) & 1);
       const float mn = ctl->m_pub[slot][r];
       stab = ctl->stab_pub[slot][r];
       if (mn != m2) {
@@ -448,6 +524,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         reg_fence32(v);
         reg_fence32(v + 32);
       }
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 15);  // S (first chunk) in registers
       const int lim = R - (j - 1) * BC - hf * CP;
       if (mask) {  // entrywise causal mask (src/reference.py:93-96)
 #pragma unroll
@@ -465,7 +542,9 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         const float pm2 = part_max<CP>(v) * cs;
         const bool below = (pm2 - fmaxf(m2, pm2) < a.log2_lambda) ||
                            (pm2 == -INFINITY && m2 == -INFINITY && a.log2_lambda != -INFINITY);
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 9);  // S in registers, max taken
         skipped = named_bar_and(1 + gi, 256, below);
+        if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 10);  // skip decided
         if (skipped) ++n_skipped;
       } else if (special) {
         // exact update (src/vfa.py:202-208): row max over both halves, then publish version E+1
@@ -506,7 +585,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         // O holds PV of every earlier position once PV(pos-1) completed (S(pos) ready implies
         // PV(pos-3) did, and PV(pos) waits for this group's P, so pv_done[(pos-1) & 1] is in or
         // just past phase (pos-1) >> 1): wait for it, then rescale this half of the row
-        mbar_wait(&ctl->pv_done[(pos - 1) & 1], ((pos - 1) >> 1) & 1);
+        swait(&ctl->pv_done[(pos - 1) & 1], ((pos - 1) >> 1) & 1);
         tc_fence_after();
         const float2 f2 = make_float2(f, f);
 #pragma unroll 1
@@ -571,6 +650,10 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       } else {
         if (split) tmem_wait_ld();
         consumed(g);
+        if (r == 0 && hf == 0) {
+          VFA_TRACE_EVENT(a, pos, 2);
+          VFA_TRACE_EVENT(a, pos, 1);
+        }
       }
       // start loading the group's next element (v is free: the row sum was taken on the fly)
       prefetched = VFA_WS1_PREFETCH && g + 2 < G;
@@ -661,5 +744,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     tmem_dealloc<512>(ctl->tmem_base);
   }
 }
+
+#undef iwait
+#undef swait
 
 }  // namespace vfa

@@ -80,8 +80,22 @@ if a.ws1:
     print(f" MMA: V acquired {med(vacq - P0):.0f} after chunk-0 P; sees chunk 0 +{med(seen0 - P0):.0f}, chunk 1 +{med(seen1 - P):.0f};"
           f" PV issued +{med(pv - P):.0f} after P done; QK(g+3) issued +{med(qk - pv):.0f} after PV;"
           f" PV period {med(np.diff(pv)):.0f}")
+    Ktma, Vtma, Kacq, bfree, mx, dec = (tr[:, i] for i in (11, 12, 13, 14, 9, 10))
+    print(f" QK: buffer free (PV(g-3) issued) -> K acquired {med(Kacq - bfree):.0f}; K TMA issue -> K acquired"
+          f" {med(Kacq - Ktma):.0f}; K TMA issued {med(Ktma - bfree):.0f} after buffer free; K acquired -> S ready"
+          f" {med(S - Kacq):.0f}")
+    print(f" V: TMA issue -> V acquired {med(vacq - Vtma):.0f}; V TMA issued {med(Vtma - S):.0f} after S ready")
+    print(f" S (first chunk) in registers {med(tr[:, 15] - S):.0f} after S ready")
+    qk_end = np.concatenate([qk[3:], np.full(3, np.nan)])  # QK(p) enqueued (slot 5 of element p - 3)
+    qk_end = np.roll(qk, 3)  # element p: slot 5 of p - 3 is the end of QK(p)'s issue
+    qk_end[:3] = np.nan
+    print(f" QK issuer: issue call {med(qk_end - Kacq):.0f}; previous issue end -> buffer free {med(bfree[1:] - qk_end[:-1]):.0f};"
+          f" buffer free -> K acquired {med(Kacq - bfree):.0f}; PV issuer saw element p-3 -> buffer free(p)"
+          f" {med(bfree[3:] - seen0[:-3]):.0f}; K acquired -> S {med(S - Kacq):.0f}")
+    if np.isfinite(mx).any():
+        print(f" VSA frozen: S -> max taken {med(mx - S):.0f}; -> skip decided {med(dec - S):.0f}; -> consumed {med(P - S):.0f}")
     for i in range(20, min(26, n)):
-        print(" ", np.round(tr[i, :9]).astype(int).tolist())
+        print(" ", np.round(tr[i, :15]).astype(int).tolist())
     sys.exit(0)
 print(f"variant={a.variant} k_block={a.k_block} visited={n} total={np.nanmax(tr):.0f} cycles "
       f"-> {np.nanmax(tr) / n:.0f} cycles per block (both query tiles)")
