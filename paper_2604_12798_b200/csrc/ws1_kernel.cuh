@@ -48,6 +48,9 @@ namespace vfa {
 #ifndef VFA_WS1_PV_SKIPFIRST
 #define VFA_WS1_PV_SKIPFIRST 0  // 1: PV issuer frees a skipped element's buffer before its V lands (no gain, -3 % dense VSA)
 #endif
+#ifndef VFA_WS1_PIPE
+#define VFA_WS1_PIPE 0  // 1: next position's schedule facts computed during this one's S load (spills; VFA 1244 vs 1301)
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -497,13 +500,31 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     // P hand-off, so the TMEM load latency overlaps the tail of this element and the loop
     float v[CP];
     bool prefetched = false;  // chunk 0 of element g is already loading into v[0 .. 31]
-    for (int g = nchunks + (((gi - nchunks) % 2) + 2) % 2; g < G; g += 2) {
+    // per-position schedule facts (key block, exact / masked, exact positions before it); with
+    // VFA_WS1_PIPE the next position's are computed while this position's S loads from TMEM, so
+    // the integer chains of the schedule are off the group's per-block critical path
+    struct Step {
+      int j, E;
+      bool special, mask;
+    };
+    auto step_at = [&](int pos) {
+      Step st;
+      st.j = sched_block(sched, pos);
+      st.special = all_exact(MODE) || sched_is_special(sched, st.j);
+      st.mask = sched_needs_mask(unit.qt + 1, st.j, kBR, BC, a.causal != 0);
+      st.E = exact_before<MODE>(sched, pos);
+      return st;
+    };
+    const int g_first = nchunks + (((gi - nchunks) % 2) + 2) % 2;
+    Step nxt = step_at(g_first - nchunks);
+    for (int g = g_first; g < G; g += 2) {
       const int pos = g - nchunks;
       const int b = g % SB;
-      const int j = sched_block(sched, pos);
-      const bool special = all_exact(MODE) || sched_is_special(sched, j);
-      const bool mask = sched_needs_mask(unit.qt + 1, j, kBR, BC, a.causal != 0);
-      const int E = exact_before<MODE>(sched, pos);
+      const Step cur = VFA_WS1_PIPE ? nxt : step_at(pos);
+      const int j = cur.j;
+      const bool special = cur.special;
+      const bool mask = cur.mask;
+      const int E = cur.E;
       ++n_visit;
       catch_up(E);  // the running max after every exact position before this one
       if (!prefetched) {
@@ -512,6 +533,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 0);
         tmem_ld32(tS(b) + hf * CP, v);
       }
+      if (VFA_WS1_PIPE && g + 2 < G) nxt = step_at(pos + 2);
       if (r == 0 && hf == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
       const bool split = MODE == kVFA && !special;  // no row statistic before the exponentials
       if (split) {
