@@ -14,7 +14,7 @@
 //   warp 16     QK^T issuer (converged, elect.sync), TMEM allocator
 //   warp 17     TMA producer
 //   warp 18     PV issuer
-//   warp 19     idle
+//   warp 19     idle (QK^T issuer of odd elements with VFA_WS1_QK2=1; warp 16 then even ones)
 // TMEM: S buffers at 0 / 128 / 256 (P packed bf16 in columns 0-31 / 64-95 of its S buffer, see p_col),
 // O at 384. The MMA issues QK for element g + 3 as soon as PV(g) is issued, so S is up to
 // three blocks ahead and the two groups' exponentials run back to back: the softmax is never
@@ -42,8 +42,8 @@ namespace vfa {
 #ifndef VFA_WS1_PREFETCH
 #define VFA_WS1_PREFETCH 0  // 1: load the next element's first S columns before finishing this one (measured 7 % slower: spills)
 #endif
-#ifndef VFA_WS1_QK_PROBE
-#define VFA_WS1_QK_PROBE 0  // QK k-steps issued before probing the next element's waits (0: no probe; 2 / 4 / 6 measured 3-8 % slower)
+#ifndef VFA_WS1_QK2
+#define VFA_WS1_QK2 0  // 1: two QK issuer warps (16, 19) on alternate elements (measured 1-3 % slower)
 #endif
 #ifndef VFA_WS1_PV_SKIPFIRST
 #define VFA_WS1_PV_SKIPFIRST 0  // 1: PV issuer frees a skipped element's buffer before its V lands (no gain, -3 % dense VSA)
@@ -64,6 +64,7 @@ struct Ws1Cfg {
   static constexpr int kMmaWarp = 16;  // QK issuer, TMEM allocator
   static constexpr int kLoadWarp = 17;
   static constexpr int kPvWarp = 18;   // PV issuer
+  static constexpr int kQk2Warp = 19;  // second QK issuer (VFA_WS1_QK2)
   static constexpr int kSB = 3;     // S buffers
   static constexpr int kVer = 6;    // running-max version ring
   static constexpr int kQBytes = kBR * D * 2;  // 32 KB
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           }
         }
       }
-    } else if (warp == C::kMmaWarp || warp == C::kPvWarp) {
+    } else if (warp == C::kMmaWarp || warp == C::kPvWarp || (VFA_WS1_QK2 && warp == C::kQk2Warp)) {
       // ============================ MMA issuers ============================
       // warp 16 issues the QK^T MMAs, warp 18 the PV MMAs: each one's barrier waits (~90
       // cycles a TRYWAIT, even when the phase is complete) overlap the other's queued MMAs,
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       // overwrites the S / P buffer of element g, so the QK issuer enqueues it only after the
       // PV issuer enqueued PV(g) (pv_issued; the tensor pipe runs MMAs in enqueue order).
       VFA_WS1_SETUP();
-      const bool is_qk = warp == C::kMmaWarp;
+      const bool is_qk = warp != C::kPvWarp;
       constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
       constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
       constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
@@ -328,41 +329,26 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         auto skip_v = [&](int g) {
           if (g >= SB - 1 && g + 1 < G && g - (SB - 1) >= nchunks) skip_tile();
         };
-        // Both waits of element g + 1 (its buffer's PV issued, its K landed) are probed while
-        // QK(g)'s first k-steps are queued: when both are already complete (S far ahead of the
-        // softmax, e.g. VSA skipping most blocks) QK(g + 1) follows QK(g) with no pipe bubble; a
-        // blocking wait after QK(g)'s last k-step would let the three-deep MMA queue drain.
-        int pre = -1;  // stage of S-op(g), acquired by the probe during QK(g - 1)
+        // VFA_WS1_QK2: warps 16 and 19 issue the QK MMAs of alternate elements, so one issuer's
+        // barrier waits and stage release after its eight k-steps overlap the other's queued
+        // MMAs (a single issuer lets the three-deep MMA queue drain there, which is the rate
+        // limit when the softmax is fast, e.g. VSA skipping most blocks)
+        const int qk_par = (VFA_WS1_QK2 && warp != C::kMmaWarp) ? 1 : 0;
         for (int g = 0; g < G; ++g) {
-          int st = pre;
-          if (pre < 0) {
-            if (g >= SB) {  // PV(g - SB) enqueued (element g - SB's S / P buffer consumed)
-              iwait(&ctl->pv_issued[g % SB], ((g - SB) / SB) & 1);
-            }
-            if (g >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - nchunks, 14);  // buffer free
-            st = acquire();
+          if (VFA_WS1_QK2 && (g & 1) != qk_par) {  // the other issuer's element
+            skip_tile();
             skip_v(g);
+            continue;
           }
+          if (g >= SB) {  // PV(g - SB) enqueued (element g - SB's S / P buffer consumed)
+            iwait(&ctl->pv_issued[g % SB], ((g - SB) / SB) & 1);
+          }
+          if (g >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - nchunks, 14);  // buffer free
+          const int st = acquire();
+          skip_v(g);
           tc_fence_after();
-          pre = -1;
           if (g >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - nchunks, 13);  // K acquired
-          constexpr int kProbe = VFA_WS1_QK_PROBE;
-          if (kProbe > 0) {
-            issue_qk(g % SB, st, 0, kProbe);
-            if (g + 1 < G) {
-              bool ok = g + 1 < SB || mbar_test_wait(&ctl->pv_issued[(g + 1) % SB], ((g + 1 - SB) / SB) & 1);
-              ok = ok && mbar_test_wait(&ctl->kv_full[stage], phase);
-              if (__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) {
-                if (g + 1 >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g + 1 - nchunks, 14);
-                pre = stage;
-                skip_tile();
-                skip_v(g + 1);
-              }
-            }
-            issue_qk(g % SB, st, kProbe, D / 16);
-          } else {
-            issue_qk(g % SB, st, 0, D / 16);
-          }
+          issue_qk(g % SB, st, 0, D / 16);
           if (g >= SB && g - SB >= nchunks && lane == 0) VFA_TRACE_EVENT(a, g - SB - nchunks, 5);
           release(st);
         }
