@@ -389,6 +389,13 @@ __device__ __forceinline__ void tma_load_4d_mc(void* dst, const CUtensorMap* map
       "l"(cache_hint)
       : "memory");
 }
+// L2 prefetch of a 4-D TMA box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 // arrive on the same-offset mbarrier of every CTA in `cta_mask` once this thread's prior
 // tcgen05 operations (cta_group::1) complete
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) {

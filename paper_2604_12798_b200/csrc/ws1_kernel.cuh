@@ -51,6 +51,12 @@ namespace vfa {
 #ifndef VFA_WS1_PIPE
 #define VFA_WS1_PIPE 0  // 1: next position's schedule facts computed during this one's S load (spills; VFA 1244 vs 1301)
 #endif
+#ifndef VFA_WS1_VPREF
+#define VFA_WS1_VPREF 0  // 1: L2 prefetch of V(g) when K(g) is loaded (dense same, skip mode -12 %)
+#endif
+#ifndef VFA_WS1_MC
+#define VFA_WS1_MC 1  // 1: each CTA loads half of every K / V tile and multicasts it to the pair; 0: full tiles per CTA
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     mbar_init(&ctl->q_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&ctl->kv_full[s], 1);
-      mbar_init(&ctl->kv_empty[s], 2);
+      mbar_init(&ctl->kv_empty[s], VFA_WS1_MC ? 2 : 1);
     }
     for (int b = 0; b < SB; ++b) {
       mbar_init(&ctl->s_full[b], 1);
@@ -218,8 +224,15 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             return;
           }
           mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
-          tma_load_4d_mc(sKV + stage * C::kKVBytes + crank * (BC * 128), map, &ctl->kv_full[stage],
-                         static_cast<int>(crank) * 64, row, unit.kvh, unit.b, static_cast<uint16_t>(3), pol_kv);
+          if (VFA_WS1_MC) {
+            tma_load_4d_mc(sKV + stage * C::kKVBytes + crank * (BC * 128), map, &ctl->kv_full[stage],
+                           static_cast<int>(crank) * 64, row, unit.kvh, unit.b, static_cast<uint16_t>(3), pol_kv);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              tma_load_4d(sKV + stage * C::kKVBytes + h * (BC * 128), map, &ctl->kv_full[stage], h * 64, row, unit.kvh,
+                          unit.b, pol_kv);
+          }
           if (++stage == NS) {
             stage = 0;
             phase ^= 1;
@@ -240,7 +253,14 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           }
           if (g + SB < G) {
             load_s_operand(g + SB);
-            if (g + SB >= nchunks) VFA_TRACE_EVENT(a, g + SB - nchunks, 11);  // K(g + SB) TMA issued
+            if (g + SB >= nchunks) {
+              VFA_TRACE_EVENT(a, g + SB - nchunks, 11);  // K(g + SB) TMA issued
+              // V(g + SB) enters the ring only when K(g + SB)'s MMAs are done (5 stages), then
+              // its TMA latency is on the PV path: warm L2 with it now
+              if (VFA_WS1_VPREF)
+                tma_prefetch_4d(&tmV, static_cast<int>(crank) * 64, (sched_block(sched, g + SB - nchunks) - 1) * BC,
+                                unit.kvh, unit.b);
+            }
           }
         }
       }
@@ -280,7 +300,12 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         return st;
       };
       auto release = [&](int st) {  // this CTA's MMAs on the stage done -> both producers
-        if (elect_one()) mma_commit_mc(&ctl->kv_empty[st], static_cast<uint16_t>(3));
+        if (elect_one()) {
+          if (VFA_WS1_MC)
+            mma_commit_mc(&ctl->kv_empty[st], static_cast<uint16_t>(3));
+          else
+            mma_commit(&ctl->kv_empty[st]);
+        }
         __syncwarp();
       };
 #ifndef VFA_WS1_DBG_NOMMA
