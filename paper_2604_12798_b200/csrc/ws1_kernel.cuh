@@ -57,6 +57,9 @@ namespace vfa {
 #ifndef VFA_WS1_MC
 #define VFA_WS1_MC 1  // 1: each CTA loads half of every K / V tile and multicasts it to the pair; 0: full tiles per CTA
 #endif
+#ifndef VFA_WS1_LA
+#define VFA_WS1_LA 3  // K/V load sequence: S-op(0 .. LA-1), then per element V(g), S-op(g + LA)
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -139,6 +142,10 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
                    const FwdArgs a) {
   using C = Ws1Cfg;
   constexpr int D = C::D, BC = C::BC, NS = C::kStages, SB = C::kSB, NV = C::kVer;
+  // K tiles ahead of V(g) in the load sequence (SB: as many as S buffers; fewer lets V(g) take
+  // an older ring stage, K(g + SB) a younger one)
+  constexpr int LA = VFA_WS1_LA;
+  static_assert(LA >= 1 && LA <= SB, "load look-ahead");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   Ws1Ctl* ctl = reinterpret_cast<Ws1Ctl*>(smem_raw);
@@ -244,21 +251,21 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           else
             load_tile(&tmK, (sched_block(sched, g - nchunks) - 1) * BC);
         };
-        // the MMA warp's consumption order: S-op(0 .. SB-1); per g: [V(g)], S-op(g + SB)
-        for (int g = 0; g < SB && g < G; ++g) load_s_operand(g);
+        // the MMA warps' consumption order: S-op(0 .. LA-1); per g: [V(g)], S-op(g + LA)
+        for (int g = 0; g < LA && g < G; ++g) load_s_operand(g);
         for (int g = 0; g < G; ++g) {
           if (g >= nchunks) {
             load_tile(&tmV, (sched_block(sched, g - nchunks) - 1) * BC);
             VFA_TRACE_EVENT(a, g - nchunks, 12);  // V(g) TMA issued
           }
-          if (g + SB < G) {
-            load_s_operand(g + SB);
-            if (g + SB >= nchunks) {
-              VFA_TRACE_EVENT(a, g + SB - nchunks, 11);  // K(g + SB) TMA issued
+          if (g + LA < G) {
+            load_s_operand(g + LA);
+            if (g + LA >= nchunks) {
+              VFA_TRACE_EVENT(a, g + LA - nchunks, 11);  // K(g + LA) TMA issued
               // V(g + SB) enters the ring only when K(g + SB)'s MMAs are done (5 stages), then
               // its TMA latency is on the PV path: warm L2 with it now
               if (VFA_WS1_VPREF)
-                tma_prefetch_4d(&tmV, static_cast<int>(crank) * 64, (sched_block(sched, g + SB - nchunks) - 1) * BC,
+                tma_prefetch_4d(&tmV, static_cast<int>(crank) * 64, (sched_block(sched, g + LA - nchunks) - 1) * BC,
                                 unit.kvh, unit.b);
             }
           }
@@ -283,8 +290,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       const uint32_t q_lo = ((smem_u32(sQ) >> 4) & 0x3FFFu) + kLboK;
       const uint32_t kv_lo = (smem_u32(sKV) >> 4) & 0x3FFFu;
       const uint32_t tO = tbase + C::kOOff;
-      // both issuers walk the producer's load sequence (S-op(0 .. SB-1); per g: [V(g)],
-      // [S-op(g + SB)]) and consume only their own tiles
+      // both issuers walk the producer's load sequence (S-op(0 .. LA-1); per g: [V(g)],
+      // [S-op(g + LA)]) and consume only their own tiles
       int stage = 0;
       uint32_t phase = 0;
       auto skip_tile = [&]() {
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         tc_fence_after();
         // the V tile of the load sequence between S-op(g) and S-op(g + 1), if any
         auto skip_v = [&](int g) {
-          if (g >= SB - 1 && g + 1 < G && g - (SB - 1) >= nchunks) skip_tile();
+          if (g >= LA - 1 && g + 1 < G && g - (LA - 1) >= nchunks) skip_tile();
         };
         // VFA_WS1_QK2: warps 16 and 19 issue the QK MMAs of alternate elements, so one issuer's
         // barrier waits and stage release after its eight k-steps overlap the other's queued
@@ -379,8 +386,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         }
       } else {
         bool o_init = false;
-        // the load sequence starts with min(SB, G) S operands
-        for (int i = 0; i < SB && i < G; ++i) skip_tile();
+        // the load sequence starts with min(LA, G) S operands
+        for (int i = 0; i < LA && i < G; ++i) skip_tile();
         for (int g = 0; g < G; ++g) {
           const int b = g % SB;
           const uint32_t ph = (g / SB) & 1;
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
               if (elect_one()) mma_commit(&ctl->pv_done[pos & 1]);
               __syncwarp();
               release(vs);
-              if (g + SB < G) skip_tile();
+              if (g + LA < G) skip_tile();
               continue;
             }
           }
@@ -426,12 +433,11 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             __syncwarp();
             release(vs);
           }
-          if (g + SB < G) {
-            // QK(g + SB) may now overwrite this buffer; skip its S operand in the sequence
+          if (g + SB < G) {  // QK(g + SB) may now overwrite this buffer
             if (elect_one()) mbar_arrive(&ctl->pv_issued[b]);
             __syncwarp();
-            skip_tile();
           }
+          if (g + LA < G) skip_tile();  // S-op(g + LA) in the load sequence
         }
         if (elect_one()) mma_commit(&ctl->o_final);
         __syncwarp();
