@@ -85,14 +85,10 @@ static int launch_ws1_mode(const CUtensorMap& mq, const CUtensorMap& mk, const C
 // (ws1_kernel.cuh: its two softmax groups only synchronise on exact-update blocks, the few
 // sink / local ones); FA, where every block is an exact update that would serialise those
 // groups, runs the ping-pong kernel (ws_kernel.cuh). profiles/ab_r02_ws1.txt.
-#ifndef VFA_WS_KIND
-#define VFA_WS_KIND -1  // -1: per variant as above; 0: ping-pong for all; 1: decoupled for all
-#endif
 
 int launch_ws(const VfaParams* p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
               const CUtensorMap& mr, const vfa::FwdArgs& a, cudaStream_t st) {
-  const int kind = VFA_WS_KIND >= 0 ? VFA_WS_KIND : (p->variant == VFA_VARIANT_FA ? 0 : 1);
-  if (kind == 1) {
+  if (ws_uses_ws1(p)) {
     switch (p->variant) {
       case VFA_VARIANT_FA:
         return launch_ws1_mode<vfa::kFA>(mq, mk, mv, mr, a, st);

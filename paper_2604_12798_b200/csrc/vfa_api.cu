@@ -288,14 +288,17 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   // tensor pipe as in the single-CTA kernel) when the GQA group allows, else one
   const int pair_nq = (VFA_PAIR_NQ2 && group % 4 == 0) ? 2 : 1;
 
+  // warp-specialised kernels (d = Bc = 128, two query tiles per unit); the decoupled kernel's
+  // pair-MMA build splits K-like tiles by rows between the two CTAs
+  const bool ws_path = ws_eligible(p) && nq == 2 && pair == 1 && !m_trace && !row_bias;
+  const int kbox = (ws_path && VFA_WS1_PAIR && vfa_host::ws_uses_ws1(p)) ? BC / 2 : BC / pair;
   CUtensorMap mq, mk, mv, mr;
   if (!make_map(&mq, q, p->batch, p->heads_q, p->seq_q, D, p->q_stride[0], p->q_stride[1], p->q_stride[2], 128) ||
-      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2],
-                BC / pair) ||
+      !make_map(&mk, k, p->batch, p->heads_kv, p->seq_k, D, p->k_stride[0], p->k_stride[1], p->k_stride[2], kbox) ||
       !make_map(&mv, v, p->batch, p->heads_kv, p->seq_k, D, p->v_stride[0], p->v_stride[1], p->v_stride[2], BC))
     return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   if (minit) {
-    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, BC / pair))
+    if (!make_map(&mr, workspace, p->batch, p->heads_kv, nrep, D, p->heads_kv * nrep * D, nrep * D, D, kbox))
       return fail(VFA_ERR_CUDA, "cuTensorMapEncodeTiled failed (krepr)");
     if (!p->krepr_precomputed) {
       rc = launch_krepr(p, k, workspace, st);
@@ -382,8 +385,7 @@ int forward_impl(const VfaParams* p, const void* q, const void* k, const void* v
   a.trace = g_debug_trace;
 
   // the warp-specialised kernel serves the headline shape (default layout, no debug outputs)
-  if (ws_eligible(p) && nq == 2 && pair == 1 && !m_trace && !row_bias)
-    return vfa_host::launch_ws(p, mq, mk, mv, mr, a, st);
+  if (ws_path) return vfa_host::launch_ws(p, mq, mk, mv, mr, a, st);
   static const vfa_host::LaunchFn kLaunch[] = {vfa_host::launch_fa,     vfa_host::launch_vfa,
                                                vfa_host::launch_vsa,    vfa_host::launch_blasst,
                                                vfa_host::launch_blasst_fa4, vfa_host::launch_blasst_rowskip};

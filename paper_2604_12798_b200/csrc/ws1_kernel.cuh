@@ -33,8 +33,11 @@
 
 namespace vfa {
 
+#ifndef VFA_WS1_PAIR
+#define VFA_WS1_PAIR 0
+#endif
 #ifndef VFA_WS1_STAGES
-#define VFA_WS1_STAGES 5
+#define VFA_WS1_STAGES (VFA_WS1_PAIR ? 10 : 5)
 #endif
 #ifndef VFA_WS1_EMU
 #define VFA_WS1_EMU 1  // element pairs (of 8) per 32-column chunk on the FMA-pipe exp2
@@ -46,7 +49,7 @@ namespace vfa {
 #define VFA_WS1_QK2 0  // 1: two QK issuer warps (16, 19) on alternate elements (measured 1-3 % slower)
 #endif
 #ifndef VFA_WS1_PV_SKIPFIRST
-#define VFA_WS1_PV_SKIPFIRST 0  // 1: PV issuer frees a skipped element's buffer before its V lands (no gain, -3 % dense VSA)
+#define VFA_WS1_PV_SKIPFIRST 0  // (not with VFA_WS1_PAIR)  // 1: PV issuer frees a skipped element's buffer before its V lands (no gain, -3 % dense VSA)
 #endif
 #ifndef VFA_WS1_PIPE
 #define VFA_WS1_PIPE 0  // 1: next position's schedule facts computed during this one's S load (spills; VFA 1244 vs 1301)
@@ -77,7 +80,10 @@ struct Ws1Cfg {
   static constexpr int kSB = 3;     // S buffers
   static constexpr int kVer = 6;    // running-max version ring
   static constexpr int kQBytes = kBR * D * 2;  // 32 KB
-  static constexpr int kKVBytes = BC * D * 2;  // 32 KB (each CTA loads half and multicasts it)
+  static constexpr int kPair = VFA_WS1_PAIR ? 2 : 1;
+  // per stage and CTA: a whole K / V tile (32 KB, each CTA loads half and multicasts it), or with
+  // pair MMAs this CTA's half (K-like tiles: BC / 2 key rows; V tiles: D / 2 columns)
+  static constexpr int kKVBytes = BC * D * 2 / kPair;
   static constexpr int kStages = VFA_WS1_STAGES;
   static constexpr int kCtlBytes = 16 * 1024;
   static constexpr int kSmem = kCtlBytes + kQBytes + kStages * kKVBytes;
@@ -100,6 +106,7 @@ struct __align__(16) Ws1Ctl {
   uint64_t mver[Ws1Cfg::kVer];         // running-max version v published (slot v % kVer)
   uint32_t tmem_base;
   uint32_t skip[Ws1Cfg::kSB];
+  uint32_t skip2[Ws1Cfg::kSB][2];      // pair: both CTAs' skip decisions (on the leader)
   float zero;
   float m_pub[Ws1Cfg::kVer][kBR];      // version's running max (log2 units), per row
   int stab_pub[Ws1Cfg::kVer][kBR];     // version's StateTrace stabilisation block, per row
@@ -142,6 +149,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
                    const FwdArgs a) {
   using C = Ws1Cfg;
   constexpr int D = C::D, BC = C::BC, NS = C::kStages, SB = C::kSB, NV = C::kVer;
+  constexpr bool PR = C::kPair == 2;  // pair MMAs: the leader (rank 0) issues every MMA for both CTAs
   // K tiles ahead of V(g) in the load sequence (SB: as many as S buffers; fewer lets V(g) take
   // an older ring stage, K(g + SB) a younger one)
   constexpr int LA = VFA_WS1_LA;
@@ -163,12 +171,12 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     mbar_init(&ctl->q_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&ctl->kv_full[s], 1);
-      mbar_init(&ctl->kv_empty[s], VFA_WS1_MC ? 2 : 1);
+      mbar_init(&ctl->kv_empty[s], (VFA_WS1_MC && !PR) ? 2 : 1);
     }
     for (int b = 0; b < SB; ++b) {
       mbar_init(&ctl->s_full[b], 1);
-      mbar_init(&ctl->p_full[b][0], 8);
-      mbar_init(&ctl->p_full[b][1], 8);
+      mbar_init(&ctl->p_full[b][0], 8 * C::kPair);  // (a pair's leader counts both CTAs' warps)
+      mbar_init(&ctl->p_full[b][1], 8 * C::kPair);
     }
     mbar_init(&ctl->pv_done[0], 1);
     mbar_init(&ctl->pv_done[1], 1);
@@ -183,7 +191,12 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmR);
   }
-  if (warp == C::kMmaWarp) tmem_alloc<512>(&ctl->tmem_base);
+  if (warp == C::kMmaWarp) {
+    if constexpr (PR)
+      tmem_alloc_pair<512>(&ctl->tmem_base);
+    else
+      tmem_alloc<512>(&ctl->tmem_base);
+  }
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // the peer's barriers are initialised before any multicast lands
@@ -208,10 +221,18 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         VFA_WS1_SETUP();
         const uint64_t pol_q = policy_evict_first();
         const uint64_t pol_kv = policy_evict_last();
-        mbar_arrive_expect_tx(&ctl->q_full, C::kQBytes);
+        if constexpr (PR) {
+          // both CTAs' Q tiles count on the leader's barrier (the pair MMAs read both)
+          if (crank == 0) mbar_arrive_expect_tx(&ctl->q_full, 2 * C::kQBytes);
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          tma_load_4d(sQ + c * kBR * 128, &tmQ, &ctl->q_full, c * 64, unit.qt * kBR, head, unit.b, pol_q);
+          for (int c = 0; c < 2; ++c)
+            tma_load_4d_pair(sQ + c * kBR * 128, &tmQ, &ctl->q_full, c * 64, unit.qt * kBR, head, unit.b, pol_q);
+        } else {
+          mbar_arrive_expect_tx(&ctl->q_full, C::kQBytes);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            tma_load_4d(sQ + c * kBR * 128, &tmQ, &ctl->q_full, c * 64, unit.qt * kBR, head, unit.b, pol_q);
+        }
         int stage = 0;
         uint32_t phase = 0;
         // each CTA loads 64-column chunk `crank` of the tile (K: dims, V: head-dim columns) and
@@ -230,11 +251,26 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             }
             return;
           }
-          mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
-          if (VFA_WS1_MC) {
+          if constexpr (PR) {
+            // this CTA's half, counted on the leader's barrier: K-like tiles rows
+            // [crank * BC/2, +BC/2) (both 64-column chunks), V tiles columns [crank * 64, +64)
+            uint8_t* dst = sKV + stage * C::kKVBytes;
+            if (crank == 0) mbar_arrive_expect_tx(&ctl->kv_full[stage], 2 * C::kKVBytes);
+            if (map == &tmV) {
+              tma_load_4d_pair(dst, map, &ctl->kv_full[stage], static_cast<int>(crank) * 64, row, unit.kvh, unit.b,
+                               pol_kv);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                tma_load_4d_pair(dst + c * (BC / 2) * 128, map, &ctl->kv_full[stage], c * 64,
+                                 row + static_cast<int>(crank) * (BC / 2), unit.kvh, unit.b, pol_kv);
+            }
+          } else if (VFA_WS1_MC) {
+            mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
             tma_load_4d_mc(sKV + stage * C::kKVBytes + crank * (BC * 128), map, &ctl->kv_full[stage],
                            static_cast<int>(crank) * 64, row, unit.kvh, unit.b, static_cast<uint16_t>(3), pol_kv);
           } else {
+            mbar_arrive_expect_tx(&ctl->kv_full[stage], C::kKVBytes);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               tma_load_4d(sKV + stage * C::kKVBytes + h * (BC * 128), map, &ctl->kv_full[stage], h * 64, row, unit.kvh,
@@ -271,7 +307,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           }
         }
       }
-    } else if (warp == C::kMmaWarp || warp == C::kPvWarp || (VFA_WS1_QK2 && warp == C::kQk2Warp)) {
+    } else if ((!PR || crank == 0) &&
+               (warp == C::kMmaWarp || warp == C::kPvWarp || (VFA_WS1_QK2 && warp == C::kQk2Warp))) {
       // ============================ MMA issuers ============================
       // warp 16 issues the QK^T MMAs, warp 18 the PV MMAs: each one's barrier waits (~90
       // cycles a TRYWAIT, even when the phase is complete) overlap the other's queued MMAs,
@@ -280,8 +317,15 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       // PV issuer enqueued PV(g) (pv_issued; the tensor pipe runs MMAs in enqueue order).
       VFA_WS1_SETUP();
       const bool is_qk = warp != C::kPvWarp;
-      constexpr uint32_t kIdescQK = make_idesc_bf16(128, BC, false, false);
-      constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t kIdescQK = make_idesc_bf16(128 * C::kPair, BC, false, false);
+      constexpr uint32_t kIdescPV = make_idesc_bf16(128 * C::kPair, D, false, true);
+      // completion signal: this CTA's barrier, or (pair) the same barrier of both CTAs
+      auto commit_to = [&](uint64_t* bar) {
+        if constexpr (PR)
+          mma_commit_pair(bar);
+        else
+          mma_commit(bar);
+      };
       constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
       constexpr uint32_t kLboK = 1u << 16;
       constexpr uint32_t kLboV = static_cast<uint32_t>((BC * 128) >> 4) << 16;
@@ -308,7 +352,9 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       };
       auto release = [&](int st) {  // this CTA's MMAs on the stage done -> both producers
         if (elect_one()) {
-          if (VFA_WS1_MC)
+          if (PR)
+            mma_commit_pair(&ctl->kv_empty[st]);
+          else if (VFA_WS1_MC)
             mma_commit_mc(&ctl->kv_empty[st], static_cast<uint16_t>(3));
           else
             mma_commit(&ctl->kv_empty[st]);
@@ -322,7 +368,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       auto issue_qk = [&](int b, int st, int k0, int k1) {
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboK;
         if (VFA_WS1_DBG_NOMMA) {
-          if (k1 == D / 16 && elect_one()) mma_commit(&ctl->s_full[b]);
+          if (k1 == D / 16 && elect_one()) commit_to(&ctl->s_full[b]);
           __syncwarp();
           return;
         }
@@ -331,11 +377,15 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             if (kk < k0 || kk >= k1) continue;
             const uint32_t off = ((kk >> 2) * (kBR * 128) + (kk & 3) * 32) >> 4;
+            const uint32_t offk = ((kk >> 2) * ((BC / C::kPair) * 128) + (kk & 3) * 32) >> 4;
             const uint64_t da = (static_cast<uint64_t>(kHi) << 32) | (q_lo + off);
-            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + off);
-            mma_ss(tbase + C::s_off(b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+            const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + offk);
+            if constexpr (PR)
+              mma_ss_pair(tbase + C::s_off(b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
+            else
+              mma_ss(tbase + C::s_off(b), da, db, kIdescQK, kk > 0 ? 1u : 0u);
           }
-          if (k1 == D / 16) mma_commit(&ctl->s_full[b]);
+          if (k1 == D / 16) commit_to(&ctl->s_full[b]);
         }
         __syncwarp();
       };
@@ -349,7 +399,10 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           for (int i = 0; i < 4; ++i) {
             const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
-            mma_ts(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
+            if constexpr (PR)
+              mma_ts_pair(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
+            else
+              mma_ts(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -408,7 +461,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
               if (lane == 0) VFA_TRACE_EVENT(a, pos, 7);
               if (lane == 0) VFA_TRACE_EVENT(a, pos, 8);
               if (lane == 0) VFA_TRACE_EVENT(a, pos, 6);
-              if (elect_one()) mma_commit(&ctl->pv_done[pos & 1]);
+              if (elect_one()) commit_to(&ctl->pv_done[pos & 1]);
               __syncwarp();
               release(vs);
               if (g + LA < G) skip_tile();
@@ -417,10 +470,14 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           }
           const int vs = main_blk ? acquire() : -1;
           if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 7);  // V acquired
-          iwait(&ctl->p_full[b][0], ph);
+          if constexpr (PR && skips(MODE))  // pairs with the follower's release (its skip flag)
+            mbar_wait_cluster(&ctl->p_full[b][0], ph);
+          else
+            iwait(&ctl->p_full[b][0], ph);
           tc_fence_after();
           if (main_blk && lane == 0) VFA_TRACE_EVENT(a, pos, 4);  // MMA saw P chunk 0
-          const bool skip = skips(MODE) && ctl->skip[b] != 0;
+          // (pair: the PV is one MMA for both CTAs; a CTA that skips hands over P = 0)
+          const bool skip = skips(MODE) && (PR ? (ctl->skip2[b][0] != 0 && ctl->skip2[b][1] != 0) : ctl->skip[b] != 0);
           if (main_blk && !skip) issue_pv(b, vs, 0, !o_init);
           iwait(&ctl->p_full[b][1], ph);
           tc_fence_after();
@@ -429,7 +486,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             if (!skip) issue_pv(b, vs, 1, false);
             if (lane == 0) VFA_TRACE_EVENT(a, pos, 6);  // PV issued
             o_init = o_init || !skip;
-            if (elect_one()) mma_commit(&ctl->pv_done[pos & 1]);
+            if (elect_one()) commit_to(&ctl->pv_done[pos & 1]);
             __syncwarp();
             release(vs);
           }
@@ -439,7 +496,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           }
           if (g + LA < G) skip_tile();  // S-op(g + LA) in the load sequence
         }
-        if (elect_one()) mma_commit(&ctl->o_final);
+        if (elect_one()) commit_to(&ctl->o_final);
         __syncwarp();
       }
     }
@@ -461,12 +518,29 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       swait(&ctl->s_full[g % SB], (g / SB) & 1);
       tc_fence_after();
     };
+    // P hand-offs arrive on the MMA-issuing CTA's barrier (a pair's leader); the TMEM data is
+    // ordered by tcgen05 fences, so a follower's remote arrive is relaxed except for the one
+    // that also publishes the skip flag (lane 0 of warps 0 / 8: cluster-scope release)
+    auto arrive_p = [&](uint64_t* bar, bool flag) {
+      if constexpr (PR) {
+        if (crank == 0)
+          mbar_arrive(bar);
+        else if (flag)
+          mbar_arrive_cluster(mapa_shared(bar, 0));
+        else
+          mbar_arrive_cluster_relaxed(mapa_shared(bar, 0));
+      } else {
+        (void)flag;
+        mbar_arrive(bar);
+      }
+    };
+    const bool flag_writer = skips(MODE) && (warp & 7) == 0;  // lane 0 of it writes the skip flag
     auto consumed = [&](int g) {  // S of element g read (m-init chunk) or handed over as P
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&ctl->p_full[g % SB][0]);
-        mbar_arrive(&ctl->p_full[g % SB][1]);
+        arrive_p(&ctl->p_full[g % SB][0], flag_writer);
+        arrive_p(&ctl->p_full[g % SB][1], false);
       }
     };
     // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
@@ -617,7 +691,12 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         if (lane == 0) mbar_arrive(&ctl->mver[slot]);
         ver = E + 1;
       }
-      if (skips(MODE) && r == 0 && hf == 0) ctl->skip[b] = skipped ? 1u : 0u;
+      if (skips(MODE) && r == 0 && hf == 0) {
+        if constexpr (PR)  // the leader's PV issuer needs both CTAs' decisions
+          st_cluster_u32(mapa_shared(&ctl->skip2[b][crank], 0), skipped ? 1u : 0u);
+        else
+          ctl->skip[b] = skipped ? 1u : 0u;
+      }
       if (a.skip_trace && r == 0 && hf == 0)
         a.skip_trace[((static_cast<size_t>(unit.b) * a.Hq + head) * a.Tr + unit.qt) * a.Tc + pos] = skipped ? 2 : 1;
       if (rescale) {
@@ -682,12 +761,21 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->p_full[b][c]);
+          if (lane == 0) arrive_p(&ctl->p_full[b][c], flag_writer && c == 0);
           if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, c == 0 ? 2 : 1);
         }
         l = __fadd_rn(l, __fadd_rn(__fadd_rn(acc[0].x, acc[0].y), __fadd_rn(acc[1].x, acc[1].y)));
       } else {
         if (split) tmem_wait_ld();
+        if constexpr (PR) {
+          // the pair's PV runs unless both CTAs skip: this CTA's P of the block must be zero
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = 0u;
+          tmem_st16(tS(b) + hf * CP, z);
+          tmem_st16(tS(b) + hf * CP + 16, z);
+          tmem_wait_st();
+        }
         consumed(g);
         if (r == 0 && hf == 0) {
           VFA_TRACE_EVENT(a, pos, 2);
@@ -780,7 +868,10 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
   if (tid == 0) VFA_TRACE_UNIT(a, 3);
   if (warp == C::kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<512>(ctl->tmem_base);
+    if constexpr (PR)
+      tmem_dealloc_pair<512>(ctl->tmem_base);
+    else
+      tmem_dealloc<512>(ctl->tmem_base);
   }
 }
 
