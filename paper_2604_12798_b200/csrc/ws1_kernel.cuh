@@ -63,6 +63,9 @@ namespace vfa {
 #ifndef VFA_WS1_LA
 #define VFA_WS1_LA 3  // K/V load sequence: S-op(0 .. LA-1), then per element V(g), S-op(g + LA)
 #endif
+#ifndef VFA_WS1_C0
+#define VFA_WS1_C0 32  // columns (per thread) in the first P hand-off of an element: 32 or 16
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
 #define VFA_WS1_REGS_SOFTMAX 104
 #endif
@@ -389,20 +392,23 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         }
         __syncwarp();
       };
-      // PV of P chunk c: K-steps {2c, 2c+1} (half 0) and {4+2c, 5+2c} (half 1)
+      // PV of P chunk c: K-steps [0, C0/16) (chunk 0) or [C0/16, 4) (chunk 1) of each half (+4)
       auto issue_pv = [&](int b, int st, int c, bool first) {
         if (VFA_WS1_DBG_NOMMA) return;
         const uint32_t b_lo = kv_lo + st * (C::kKVBytes >> 4) + kLboV;
         const uint32_t tP = tbase + C::s_off(b);
+        constexpr int K0 = VFA_WS1_C0 / 16;
         if (elect_one()) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int kk = (i >> 1) * 4 + 2 * c + (i & 1);
+          for (int i = 0; i < 8; ++i) {
+            const int kk = (i >> 2) * 4 + (i & 3);
+            if (c == 0 ? (i & 3) >= K0 : (i & 3) < K0) continue;
+            const bool lead = c == 0 && (i & 3) == 0 && (i >> 2) == 0;  // the element's first K-step
             const uint64_t db = (static_cast<uint64_t>(kHi) << 32) | (b_lo + kk * (2048 >> 4));
             if constexpr (PR)
-              mma_ts_pair(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
+              mma_ts_pair(tO, tP + p_col(kk), db, kIdescPV, (first && lead) ? 0u : 1u);
             else
-              mma_ts(tO, tP + p_col(kk), db, kIdescPV, (first && i == 0) ? 0u : 1u);
+              mma_ts(tO, tP + p_col(kk), db, kIdescPV, (first && lead) ? 0u : 1u);
           }
         }
         __syncwarp();
@@ -726,6 +732,11 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         const float nm = (m2 == -INFINITY ? 0.f : -m2);
         // row sum (src/tensor.py:81-89) in two packed accumulators, pairs in column order
         float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // chunk 0 = columns [0, C0), chunk 1 = [C0, 64): a smaller first chunk hands P to the
+        // PV issuer earlier (VFA_WS1_C0)
+        constexpr int C0 = VFA_WS1_C0;
+        static_assert(C0 == 16 || C0 == 32, "first P chunk");
+        uint32_t u[32];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           float nmc = nm;
@@ -733,20 +744,20 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             float z;
             asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(z) : "r"(smem_u32(&ctl->zero)) : "memory");
             nmc = nm + z;
-            if (split) {
+          }
+          const float2 nmu2 = make_float2(nmc, nmc);
+#pragma unroll
+          for (int e = 0; e < CP; e += 2) {
+            if (c == 0 ? e >= C0 : e < C0) continue;
+            if (c == 1 && e == 32 && split) {  // the second 32 columns' TMEM load
               tmem_wait_ld();
               reg_fence32(v + 32);
               if (mask) {
 #pragma unroll
-                for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+                for (int e2 = 32; e2 < CP; ++e2) v[e2] = (e2 > lim) ? -INFINITY : v[e2];
               }
             }
-          }
-          const float2 nmu2 = make_float2(nmc, nmc);
-          uint32_t u[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float2 x = __ffma2_rn(make_float2(v[c * 32 + e], v[c * 32 + e + 1]), cs2, nmu2);
+            const float2 x = __ffma2_rn(make_float2(v[e], v[e + 1]), cs2, nmu2);
             float2 p;
             if (((e >> 1) & 7) >= 8 - VFA_WS1_EMU) {
               p = ex2_poly2(x);  // degree 4, |rel err| < 3e-6
@@ -757,7 +768,14 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             acc[(e >> 1) & 1] = add_ftz2(acc[(e >> 1) & 1], p);
             u[e >> 1] = pack_bf16x2(p.x, p.y);
           }
-          tmem_st16(tS(b) + hf * CP + c * 16, u);
+          if (C0 == 32) {
+            tmem_st16(tS(b) + hf * CP + c * 16, u + c * 16);
+          } else if (c == 0) {
+            tmem_st8(tS(b) + hf * CP, u);
+          } else {
+            tmem_st8(tS(b) + hf * CP + 8, u + 8);
+            tmem_st16(tS(b) + hf * CP + 16, u + 16);
+          }
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
