@@ -113,5 +113,8 @@ int main() {
   run<64, 2, true>(2, "tmem st");
   run<32, 0, true>(4, "tmem st");
   run<32, 1, true>(4, "tmem st");
+  // one thread per row with two independent warps per sub-partition (two softmax groups)
+  run<128, 0, true>(2, "tmem st");
+  run<128, 1, true>(2, "tmem st");
   return 0;
 }
