@@ -66,20 +66,25 @@ namespace vfa {
 #ifndef VFA_WS1_C0
 #define VFA_WS1_C0 32  // columns (per thread) in the first P hand-off of an element: 32 or 16
 #endif
+#ifndef VFA_WS1_NG
+#define VFA_WS1_NG 2  // softmax groups (elements g with g % NG == group); 3: 24 softmax warps
+#endif
 #ifndef VFA_WS1_REGS_SOFTMAX
-#define VFA_WS1_REGS_SOFTMAX 104
+#define VFA_WS1_REGS_SOFTMAX (VFA_WS1_NG == 3 ? 80 : 104)
 #endif
 #ifndef VFA_WS1_REGS_OTHER
-#define VFA_WS1_REGS_OTHER 64
+#define VFA_WS1_REGS_OTHER (VFA_WS1_NG == 3 ? 24 : 64)
 #endif
 
 struct Ws1Cfg {
   static constexpr int D = 128, BC = 128;
-  static constexpr int kThreads = 640;
-  static constexpr int kMmaWarp = 16;  // QK issuer, TMEM allocator
-  static constexpr int kLoadWarp = 17;
-  static constexpr int kPvWarp = 18;   // PV issuer
-  static constexpr int kQk2Warp = 19;  // second QK issuer (VFA_WS1_QK2)
+  static constexpr int kNG = VFA_WS1_NG;  // softmax groups of 8 warps
+  static_assert(kNG == 2 || kNG == 3, "softmax groups");
+  static constexpr int kThreads = 32 * (8 * kNG + 4);
+  static constexpr int kMmaWarp = 8 * kNG;       // QK issuer, TMEM allocator
+  static constexpr int kLoadWarp = 8 * kNG + 1;
+  static constexpr int kPvWarp = 8 * kNG + 2;    // PV issuer
+  static constexpr int kQk2Warp = 8 * kNG + 3;   // second QK issuer (VFA_WS1_QK2)
   static constexpr int kSB = 3;     // S buffers
   static constexpr int kVer = 6;    // running-max version ring
   static constexpr int kQBytes = kBR * D * 2;  // 32 KB
@@ -88,11 +93,12 @@ struct Ws1Cfg {
   // pair MMAs this CTA's half (K-like tiles: BC / 2 key rows; V tiles: D / 2 columns)
   static constexpr int kKVBytes = BC * D * 2 / kPair;
   static constexpr int kStages = VFA_WS1_STAGES;
-  static constexpr int kCtlBytes = 16 * 1024;
+  static constexpr int kCtlBytes = (kNG == 3 ? 20 : 16) * 1024;
   static constexpr int kSmem = kCtlBytes + kQBytes + kStages * kKVBytes;
-  static constexpr int kRegBudget = (4 * VFA_WS1_REGS_SOFTMAX + VFA_WS1_REGS_OTHER) * 128;
+  static constexpr int kRegBudget = (2 * kNG * VFA_WS1_REGS_SOFTMAX + VFA_WS1_REGS_OTHER) * 128;
   static_assert(kSmem <= kMaxSmem, "shared memory");
-  static_assert(kRegBudget <= kThreads * 96, "register budget (640 threads x 96 registers)");
+  // setmaxnreg redistributes the launch allocation (65536 / kThreads, rounded down to 8)
+  static_assert(kRegBudget <= kThreads * ((65536 / kThreads) & ~7), "register budget");
   static __device__ __forceinline__ uint32_t s_off(int b) { return static_cast<uint32_t>(b * 128); }
   static constexpr uint32_t kOOff = 384;
 };
@@ -113,9 +119,9 @@ struct __align__(16) Ws1Ctl {
   float zero;
   float m_pub[Ws1Cfg::kVer][kBR];      // version's running max (log2 units), per row
   int stab_pub[Ws1Cfg::kVer][kBR];     // version's StateTrace stabilisation block, per row
-  float xmax[2][2][2][kBR];            // [group][exact parity][half][row]: row-max exchange
-  float xinit[2][2][kBR];              // [group][half][row]: m-init partial maxima
-  float xl[2][2][kBR];                 // [group][half][row]: final partial row sums
+  float xmax[Ws1Cfg::kNG][2][2][kBR];  // [group][exact parity][half][row]: row-max exchange
+  float xinit[Ws1Cfg::kNG][2][kBR];    // [group][half][row]: m-init partial maxima
+  float xl[Ws1Cfg::kNG][2][kBR];       // [group][half][row]: final partial row sums
   uint8_t xfin[4][kBR];                // [column quarter][row]: output finite flags
 };
 static_assert(sizeof(Ws1Ctl) <= Ws1Cfg::kCtlBytes, "control block");
@@ -153,6 +159,10 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
   using C = Ws1Cfg;
   constexpr int D = C::D, BC = C::BC, NS = C::kStages, SB = C::kSB, NV = C::kVer;
   constexpr bool PR = C::kPair == 2;  // pair MMAs: the leader (rank 0) issues every MMA for both CTAs
+  constexpr int NG = C::kNG;
+  constexpr int kAllBar = 1 + NG;  // named barrier of all softmax warps (1 .. NG: one per group)
+  // three groups: the registers hold 32 S columns at a time (chunks loaded as they are consumed)
+  constexpr bool kLowReg = NG == 3;
   // K tiles ahead of V(g) in the load sequence (SB: as many as S buffers; fewer lets V(g) take
   // an older ring stage, K(g + SB) a younger one)
   constexpr int LA = VFA_WS1_LA;
@@ -510,7 +520,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     // ============================ softmax groups ============================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VFA_WS1_REGS_SOFTMAX));
     VFA_WS1_SETUP();
-    const int gi = warp >> 3;         // group: elements g with g % 2 == gi
+    const int gi = warp >> 3;         // group: elements g with g % NG == gi
     const int hf = (warp >> 2) & 1;   // half of every S row (64 columns)
     const int r = tid & 127;
     constexpr int CP = 64;
@@ -553,23 +563,39 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     float m2 = -INFINITY;  // running max this group's normalizer part is relative to (log2 units)
     if (nchunks > 0) {
       float mx = -INFINITY;
-      for (int g = gi; g < nchunks; g += 2) {
+      for (int g = gi; g < nchunks; g += NG) {
         wait_s(g);
-        float v[CP];
-        tmem_ld32(tS(g % SB) + hf * CP, v);
-        tmem_ld32(tS(g % SB) + hf * CP + 32, v + 32);
-        tmem_wait_ld();
-        reg_fence32(v);
-        reg_fence32(v + 32);
         const int valid = nrep - g * BC - hf * CP;
+        if constexpr (kLowReg) {
 #pragma unroll
-        for (int e = 0; e < CP; ++e)
-          if (e < valid) mx = fmaxf(mx, v[e]);
+          for (int c = 0; c < 2; ++c) {
+            float v[32];
+            tmem_ld32(tS(g % SB) + hf * CP + c * 32, v);
+            tmem_wait_ld();
+            reg_fence32(v);
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c * 32 + e < valid) mx = fmaxf(mx, v[e]);
+          }
+        } else {
+          float v[CP];
+          tmem_ld32(tS(g % SB) + hf * CP, v);
+          tmem_ld32(tS(g % SB) + hf * CP + 32, v + 32);
+          tmem_wait_ld();
+          reg_fence32(v);
+          reg_fence32(v + 32);
+#pragma unroll
+          for (int e = 0; e < CP; ++e)
+            if (e < valid) mx = fmaxf(mx, v[e]);
+        }
         consumed(g);
       }
       ctl->xinit[gi][hf][r] = mx;
-      named_bar_sync(3, 512);
-      m2 = fmaxf(fmaxf(ctl->xinit[0][0][r], ctl->xinit[0][1][r]), fmaxf(ctl->xinit[1][0][r], ctl->xinit[1][1][r])) * cs;
+      named_bar_sync(kAllBar, 256 * NG);
+      float mi = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) mi = fmaxf(mi, fmaxf(ctl->xinit[q][0][r], ctl->xinit[q][1][r]));
+      m2 = mi * cs;
     }
     if ((MODE == kVFA || MODE == kVSA) && a.use_m_init && a.m0_tile != nullptr)
       m2 = a.m0_tile[(static_cast<size_t>(unit.b) * a.Hq + head) * a.Tr + unit.qt] * cs;
@@ -595,7 +621,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     // S of the group's next element is usually ready long before this one is done (QK runs up
     // to three elements ahead): its first 32 columns are loaded right after this element's last
     // P hand-off, so the TMEM load latency overlaps the tail of this element and the loop
-    float v[CP];
+    float v[kLowReg ? 32 : CP];
     bool prefetched = false;  // chunk 0 of element g is already loading into v[0 .. 31]
     // per-position schedule facts (key block, exact / masked, exact positions before it); with
     // VFA_WS1_PIPE the next position's are computed while this position's S loads from TMEM, so
@@ -612,9 +638,9 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       st.E = exact_before<MODE>(sched, pos);
       return st;
     };
-    const int g_first = nchunks + (((gi - nchunks) % 2) + 2) % 2;
+    const int g_first = nchunks + (((gi - nchunks) % NG) + NG) % NG;
     Step nxt = step_at(g_first - nchunks);
-    for (int g = g_first; g < G; g += 2) {
+    for (int g = g_first; g < G; g += NG) {
       const int pos = g - nchunks;
       const int b = g % SB;
       const Step cur = VFA_WS1_PIPE ? nxt : step_at(pos);
@@ -633,32 +659,55 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       if (VFA_WS1_PIPE && g + 2 < G) nxt = step_at(pos + 2);
       if (r == 0 && hf == 0 && pos == 0) VFA_TRACE_UNIT(a, 1);
       const bool split = MODE == kVFA && !special;  // no row statistic before the exponentials
-      if (split) {
-        tmem_wait_ld();
-        reg_fence32(v);
-        tmem_ld32(tS(b) + hf * CP + 32, v + 32);
-      } else {
-        tmem_ld32(tS(b) + hf * CP + 32, v + 32);
-        tmem_wait_ld();
-        reg_fence32(v);
-        reg_fence32(v + 32);
-      }
-      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 15);  // S (first chunk) in registers
       const int lim = R - (j - 1) * BC - hf * CP;
-      if (mask) {  // entrywise causal mask (src/reference.py:93-96)
+      // kLowReg: the 64-column row max of a non-split element (VSA test / exact update), taken
+      // over two sequential 32-column loads; its exponentials then reload chunk 0
+      float pmax_all = -INFINITY;
+      if constexpr (kLowReg) {
+        tmem_wait_ld();
+        reg_fence32(v);
+        if (mask) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+          for (int e = 0; e < 32; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+        }
         if (!split) {
+          const float pm0 = part_max<32>(v);
+          tmem_ld32(tS(b) + hf * CP + 32, v);
+          tmem_wait_ld();
+          reg_fence32(v);
+          if (mask) {
 #pragma unroll
-          for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+            for (int e = 0; e < 32; ++e) v[e] = (e + 32 > lim) ? -INFINITY : v[e];
+          }
+          pmax_all = fmaxf(pm0, part_max<32>(v));
+        }
+      } else {
+        if (split) {
+          tmem_wait_ld();
+          reg_fence32(v);
+          tmem_ld32(tS(b) + hf * CP + 32, v + 32);
+        } else {
+          tmem_ld32(tS(b) + hf * CP + 32, v + 32);
+          tmem_wait_ld();
+          reg_fence32(v);
+          reg_fence32(v + 32);
+        }
+        if (mask) {  // entrywise causal mask (src/reference.py:93-96)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+          if (!split) {
+#pragma unroll
+            for (int e = 32; e < CP; ++e) v[e] = (e > lim) ? -INFINITY : v[e];
+          }
         }
       }
+      if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 15);  // S (first chunk) in registers
       bool skipped = false;
       bool rescale = false;
       float f = 1.0f;
       if (MODE == kVSA && !special) {
         // VSA frozen block: the skip test only (src/sparse.py:296-304), against the frozen max
-        const float pm2 = part_max<CP>(v) * cs;
+        const float pm2 = (kLowReg ? pmax_all : part_max<CP>(v)) * cs;
         const bool below = (pm2 - fmaxf(m2, pm2) < a.log2_lambda) ||
                            (pm2 == -INFINITY && m2 == -INFINITY && a.log2_lambda != -INFINITY);
         if (r == 0 && hf == 0) VFA_TRACE_EVENT(a, pos, 9);  // S in registers, max taken
@@ -668,7 +717,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       } else if (special) {
         // exact update (src/vfa.py:202-208): row max over both halves, then publish version E+1
         const int xp = n_ex & 1;
-        ctl->xmax[gi][xp][hf][r] = part_max<CP>(v);
+        ctl->xmax[gi][xp][hf][r] = kLowReg ? pmax_all : part_max<CP>(v);
         named_bar_sync(1 + gi, 256);
         const float mt2 = fmaxf(ctl->xmax[gi][xp][0][r], ctl->xmax[gi][xp][1][r]) * cs;
         ++n_ex;
@@ -736,6 +785,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         // PV issuer earlier (VFA_WS1_C0)
         constexpr int C0 = VFA_WS1_C0;
         static_assert(C0 == 16 || C0 == 32, "first P chunk");
+        static_assert(!kLowReg || C0 == 32, "three groups: 32-column chunks");
         uint32_t u[32];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -745,11 +795,20 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
             asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(z) : "r"(smem_u32(&ctl->zero)) : "memory");
             nmc = nm + z;
           }
+          if (kLowReg && (c == 1 || !split)) {  // this chunk's 32 columns into the registers
+            tmem_ld32(tS(b) + hf * CP + c * 32, v);
+            tmem_wait_ld();
+            reg_fence32(v);
+            if (mask) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] = (e + c * 32 > lim) ? -INFINITY : v[e];
+            }
+          }
           const float2 nmu2 = make_float2(nmc, nmc);
 #pragma unroll
           for (int e = 0; e < CP; e += 2) {
             if (c == 0 ? e >= C0 : e < C0) continue;
-            if (c == 1 && e == 32 && split) {  // the second 32 columns' TMEM load
+            if (!kLowReg && c == 1 && e == 32 && split) {  // the second 32 columns' TMEM load
               tmem_wait_ld();
               reg_fence32(v + 32);
               if (mask) {
@@ -757,7 +816,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
                 for (int e2 = 32; e2 < CP; ++e2) v[e2] = (e2 > lim) ? -INFINITY : v[e2];
               }
             }
-            const float2 x = __ffma2_rn(make_float2(v[e], v[e + 1]), cs2, nmu2);
+            const int ev = kLowReg ? e - c * 32 : e;
+            const float2 x = __ffma2_rn(make_float2(v[ev], v[ev + 1]), cs2, nmu2);
             float2 p;
             if (((e >> 1) & 7) >= 8 - VFA_WS1_EMU) {
               p = ex2_poly2(x);  // degree 4, |rel err| < 3e-6
@@ -813,9 +873,11 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     // ---- finalize (src/core.py:101-109): both groups' parts relative to the final max
     catch_up(exact_before<MODE>(sched, N));
     ctl->xl[gi][hf][r] = l;
-    named_bar_sync(3, 512);
-    const float lsum = __fadd_rn(__fadd_rn(ctl->xl[0][0][r], ctl->xl[0][1][r]), __fadd_rn(ctl->xl[1][0][r], ctl->xl[1][1][r]));
-    const int qq = warp >> 2;  // this thread's 32-column quarter of the O row
+    named_bar_sync(kAllBar, 256 * NG);
+    float lsum = __fadd_rn(__fadd_rn(ctl->xl[0][0][r], ctl->xl[0][1][r]), __fadd_rn(ctl->xl[1][0][r], ctl->xl[1][1][r]));
+#pragma unroll
+    for (int q = 2; q < NG; ++q) lsum = __fadd_rn(lsum, __fadd_rn(ctl->xl[q][0][r], ctl->xl[q][1][r]));
+    const int qq = warp >> 2;  // this thread's 32-column quarter of the O row (warps 0-15)
     const size_t lrow = (static_cast<size_t>(unit.b) * a.Hq + head) * a.Lq + R;
     const unsigned srow = static_cast<unsigned>(lrow + a.row_base);
     if (qq == 0) {
@@ -836,7 +898,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     const float inv = 1.0f / lsum;
     __nv_bfloat16* orow = a.o + unit.b * a.o_sb + head * a.o_sh + static_cast<long long>(R) * a.o_sr + qq * 32;
     bool finite = true;
-    {
+    if (qq < 4) {
       float o[32];
       tmem_ld32(tbase + C::kOOff + qq * 32 + lane_off, o);
       tmem_wait_ld();
@@ -855,8 +917,8 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       dst[3] = make_uint4(u[12], u[13], u[14], u[15]);
     }
     if (a.status) {
-      ctl->xfin[qq][r] = finite ? 1 : 0;
-      named_bar_sync(3, 512);
+      if (qq < 4) ctl->xfin[qq][r] = finite ? 1 : 0;
+      named_bar_sync(kAllBar, 256 * NG);
       if (qq == 0 && !(ctl->xfin[0][r] && ctl->xfin[1][r] && ctl->xfin[2][r] && ctl->xfin[3][r])) {
         atomicAdd(&a.status[VFA_STATUS_NONFINITE_ROWS], 1u);
         atomicOr(&a.status[VFA_STATUS_FLAGS], 4u);
