@@ -66,6 +66,9 @@ namespace vfa {
 #ifndef VFA_WS1_C0
 #define VFA_WS1_C0 32  // columns (per thread) in the first P hand-off of an element: 32 or 16
 #endif
+#ifndef VFA_WS1_STAB
+#define VFA_WS1_STAB 0  // 1: schedule facts per visit position tabulated in smem once per CTA (VFA -2 %, VSA / skip mode +1-2 %)
+#endif
 #ifndef VFA_WS1_NG
 #define VFA_WS1_NG 2  // softmax groups (elements g with g % NG == group); 3: 24 softmax warps
 #endif
@@ -93,7 +96,8 @@ struct Ws1Cfg {
   // pair MMAs this CTA's half (K-like tiles: BC / 2 key rows; V tiles: D / 2 columns)
   static constexpr int kKVBytes = BC * D * 2 / kPair;
   static constexpr int kStages = VFA_WS1_STAGES;
-  static constexpr int kCtlBytes = (kNG == 3 ? 20 : 16) * 1024;
+  static constexpr int kSchedTab = VFA_WS1_STAB ? 2048 : 1;  // visit positions tabulated per CTA
+  static constexpr int kCtlBytes = (kNG == 3 ? 24 : (VFA_WS1_STAB ? 20 : 16)) * 1024;
   static constexpr int kSmem = kCtlBytes + kQBytes + kStages * kKVBytes;
   static constexpr int kRegBudget = (2 * kNG * VFA_WS1_REGS_SOFTMAX + VFA_WS1_REGS_OTHER) * 128;
   static_assert(kSmem <= kMaxSmem, "shared memory");
@@ -123,6 +127,7 @@ struct __align__(16) Ws1Ctl {
   float xinit[Ws1Cfg::kNG][2][kBR];    // [group][half][row]: m-init partial maxima
   float xl[Ws1Cfg::kNG][2][kBR];       // [group][half][row]: final partial row sums
   uint8_t xfin[4][kBR];                // [column quarter][row]: output finite flags
+  uint16_t sinfo[Ws1Cfg::kSchedTab];   // per visit position: key block | exact << 14 | masked << 15
 };
 static_assert(sizeof(Ws1Ctl) <= Ws1Cfg::kCtlBytes, "control block");
 
@@ -560,6 +565,19 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
       }
     };
     // ---- m-init: m0 = max_j scale * q . krepr_j over visible j <= tc1 (src/vfa.py:91-106)
+    // the schedule facts of every visit position, computed once by all softmax threads (the
+    // per-element integer chains of sched_block & co. otherwise sit on each group's critical path)
+    const bool use_tab = VFA_WS1_STAB && N <= C::kSchedTab;
+    if (use_tab) {
+      for (int p = tid; p < N; p += 256 * NG) {
+        const int jj = sched_block(sched, p);
+        const bool sp = all_exact(MODE) || sched_is_special(sched, jj);
+        const bool mk = sched_needs_mask(unit.qt + 1, jj, kBR, BC, a.causal != 0);
+        ctl->sinfo[p] = static_cast<uint16_t>(jj | (sp ? 1 << 14 : 0) | (mk ? 1 << 15 : 0));
+      }
+      named_bar_sync(kAllBar, 256 * NG);
+    }
+    const bool strace = a.skip_trace != nullptr && r == 0 && hf == 0;
     float m2 = -INFINITY;  // running max this group's normalizer part is relative to (log2 units)
     if (nchunks > 0) {
       float mx = -INFINITY;
@@ -643,7 +661,16 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
     for (int g = g_first; g < G; g += NG) {
       const int pos = g - nchunks;
       const int b = g % SB;
-      const Step cur = VFA_WS1_PIPE ? nxt : step_at(pos);
+      Step cur;
+      if (use_tab) {
+        const uint32_t info = ctl->sinfo[pos];
+        cur.j = static_cast<int>(info & 0x3FFFu);
+        cur.special = (info >> 14) & 1u;
+        cur.mask = (info >> 15) & 1u;
+        cur.E = exact_before<MODE>(sched, pos);
+      } else {
+        cur = VFA_WS1_PIPE ? nxt : step_at(pos);
+      }
       const int j = cur.j;
       const bool special = cur.special;
       const bool mask = cur.mask;
@@ -752,7 +779,7 @@ __global__ void __launch_bounds__(Ws1Cfg::kThreads, 1)
         else
           ctl->skip[b] = skipped ? 1u : 0u;
       }
-      if (a.skip_trace && r == 0 && hf == 0)
+      if (strace)
         a.skip_trace[((static_cast<size_t>(unit.b) * a.Hq + head) * a.Tr + unit.qt) * a.Tc + pos] = skipped ? 2 : 1;
       if (rescale) {
         // O holds PV of every earlier position once PV(pos-1) completed (S(pos) ready implies
